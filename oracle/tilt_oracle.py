@@ -1,0 +1,486 @@
+"""Plain fp64 CPU oracle for the TILT hot path of Ren & Lin, arXiv 1205.5351.
+
+TEST INFRASTRUCTURE ONLY. Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s
+``cpu_baseline`` / ``--impl reference`` legs may import or run this module. The product path
+(``paper_1205_5351_b200``) never imports it, and this module imports nothing from the product.
+
+Every function follows the paper step by step in its notation; citations are ``P:<line>`` of
+``/root/reference/PAPER.md`` with the section / equation label. Where the paper is silent or
+garbled the reading taken is named (R*/Z*/E*), listed in DESIGN.md "Readings of the paper".
+Library primitives used as single steps: ``numpy.linalg.svd`` (the SVD in Eq. S_operator),
+``numpy.linalg.cholesky`` / ``solve`` (the p x p Gram system of Eq. Jperpv). No blocking, fusion or
+reordering beyond what the equations state.
+
+Parity status: every function here is pinned by ``tests/test_oracle_*.py`` (see DESIGN.md table
+"Oracle pins"); nothing is "parity unpinned".
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field, replace
+
+import numpy as np
+
+AFFINE = 0
+HOMOGRAPHY = 1
+
+# per-patch status codes (mirrors include/tilt.h tilt_patch_status; values are the ABI's)
+CONVERGED = 0
+MAX_OUTER = 1
+WINDOW_ESCAPE = 2
+SINGULAR_GRAM = 3
+ZERO_PATCH = 4
+DIVERGED = 5
+
+# outer stop rules (reading Z9)
+STOP_NONE, STOP_OBJECTIVE, STOP_DTAU, STOP_MAX_OUTER = 0, 1, 2, 3
+
+
+@dataclass
+class Params:
+    """Defaults of DESIGN.md "Readings"; the paper states none of them."""
+
+    lam: float = -1.0           # <= 0 -> 1/sqrt(max(m, n))  (reading Z8)
+    mu0_scale: float = 1.25     # mu0 = mu0_scale / sigma_1(D_hat)  (Z3)
+    mu_max_ratio: float = 1e6   # mu_max = ratio * mu0  (Z6)
+    rho0: float = 2.0           # Eq. rho, P:454-463  (Z7)
+    eps1: float = 1e-6          # Eq. Cond1, P:489-492 (Z7)
+    eps2: float = 0.1           # Eq. Cond2 / Eq. rho (Z7)
+    obj_tol: float = 1e-5       # outer stop, relative objective change (Z9)
+    tau_tol: float = 1e-4       # outer stop, ||dtau||_inf (Z9)
+    max_inner: int = 1000
+    max_outer: int = 50
+    constraints: bool = True    # Q = centre + area rows (Z10)
+    vws: bool = True            # variable warm start (Eq. warm_start)
+    fixed_inner_iters: int = 0  # >0: run exactly K inner iterations (test mode)
+    fixed_outer_iters: int = 0  # >0: run exactly F outer iterations (test mode)
+
+
+# ----------------------------------------------------------------------------------------------
+# Proximal operators
+# ----------------------------------------------------------------------------------------------
+
+def shrink(x, eps):
+    """Scalar shrinkage T_eps(x) = sgn(x) max(|x| - eps, 0)  (P:482, P:484-488 Eq. E_1)."""
+    x = np.asarray(x, dtype=np.float64)
+    return np.sign(x) * np.maximum(np.abs(x) - eps, 0.0)
+
+
+def svt(w, eps):
+    """Singular value shrinkage S_eps(W) = U T_eps(Sigma) V^T  (Eqs. A_1, S_operator).
+
+    Returns (S_eps(W), sigma(W)) with sigma the singular values of W (descending).
+    """
+    u, sig, vt = np.linalg.svd(np.asarray(w, dtype=np.float64), full_matrices=False)
+    return (u * shrink(sig, eps)) @ vt, sig
+
+
+def nuclear_norm(a):
+    """||A||_* = sum of singular values."""
+    return float(np.linalg.svd(np.asarray(a, dtype=np.float64), compute_uv=False).sum())
+
+
+def objective(a, e, lam):
+    """||A||_* + lambda ||E||_1  (Eq. TILT_2)."""
+    return nuclear_norm(a) + lam * float(np.abs(e).sum())
+
+
+# ----------------------------------------------------------------------------------------------
+# D o tau and its Jacobian (Alg. 1 Step 1; readings R1-R4 = Z2, Z15, Z16)
+# ----------------------------------------------------------------------------------------------
+
+def frame(box):
+    """Normalised frame of the window (reading Z15): centre c, scale s, pixel offsets du, dv."""
+    x0, y0, w, h = (int(v) for v in box)
+    m, n = h, w
+    s = max(m, n) / 2.0
+    cx = x0 + (n - 1) / 2.0
+    cy = y0 + (m - 1) / 2.0
+    dv = (np.arange(m, dtype=np.float64) - (m - 1) / 2.0)[:, None] * np.ones((1, n))
+    du = (np.arange(n, dtype=np.float64) - (n - 1) / 2.0)[None, :] * np.ones((m, 1))
+    return m, n, s, cx, cy, du, dv
+
+
+def tau_to_h(tau, kind):
+    """(h11, h12, h21, h22, h13, h23[, h31, h32]) -> 3x3 matrix (reading Z16)."""
+    t = np.asarray(tau, dtype=np.float64)
+    h31, h32 = (t[6], t[7]) if kind == HOMOGRAPHY else (0.0, 0.0)
+    return np.array([[t[0], t[1], t[4]], [t[2], t[3], t[5]], [h31, h32, 1.0]])
+
+
+def warp(image, box, tau, kind):
+    """D o tau (bilinear) and J_raw = d(D o tau)/d tau.
+
+    Source point of window pixel (i, j): x = (h11 u + h12 v + h13)/w, y = (h21 u + h22 v + h23)/w,
+    w = h31 u + h32 v + 1 in the normalised frame (Z15, Z16). The Jacobian is the exact derivative
+    of the bilinear interpolant taken from the same 4 taps (Z2), chained through the transform.
+    Returns (d [m, n], J_raw [p, m, n], status); status WINDOW_ESCAPE if any 4-tap stencil leaves
+    the image.
+    """
+    img = np.asarray(image, dtype=np.float64)
+    hh, ww = img.shape
+    m, n, s, cx, cy, du, dv = frame(box)
+    h = tau_to_h(tau, kind)
+    p = 6 if kind == AFFINE else 8
+    w = 1.0 + (h[2, 0] * du + h[2, 1] * dv) / s
+    xs = cx + (h[0, 0] * du + h[0, 1] * dv + s * h[0, 2]) / w
+    ys = cy + (h[1, 0] * du + h[1, 1] * dv + s * h[1, 2]) / w
+    if not (np.all(np.isfinite(xs)) and np.all(np.isfinite(ys))):
+        return None, None, WINDOW_ESCAPE
+    x0 = np.floor(xs)
+    y0 = np.floor(ys)
+    if x0.min() < 0 or x0.max() + 1 > ww - 1 or y0.min() < 0 or y0.max() + 1 > hh - 1:
+        return None, None, WINDOW_ESCAPE
+    fx = xs - x0
+    fy = ys - y0
+    xi = x0.astype(np.int64)
+    yi = y0.astype(np.int64)
+    i00 = img[yi, xi]
+    i01 = img[yi, xi + 1]
+    i10 = img[yi + 1, xi]
+    i11 = img[yi + 1, xi + 1]
+    d = (1 - fy) * ((1 - fx) * i00 + fx * i01) + fy * ((1 - fx) * i10 + fx * i11)
+    # exact derivative of the bilinear interpolant w.r.t. pixel coordinates (Z2)
+    dX = (1 - fy) * (i01 - i00) + fy * (i11 - i10)
+    dY = (1 - fx) * (i10 - i00) + fx * (i11 - i01)
+    # chain rule to the normalised frame: x = (X - cx)/s  =>  dI/dx = s dI/dX
+    u = du / s
+    v = dv / s
+    xn = (xs - cx) / s
+    yn = (ys - cy) / s
+    ix = s * dX
+    iy = s * dY
+    # dx/dh11 = u/w, dx/dh12 = v/w, dx/dh13 = 1/w, dx/dh31 = -x u/w, dx/dh32 = -x v/w (same for y)
+    cols = [ix * u / w, ix * v / w, iy * u / w, iy * v / w, ix / w, iy / w]
+    if kind == HOMOGRAPHY:
+        cols += [-(ix * xn + iy * yn) * u / w, -(ix * xn + iy * yn) * v / w]
+    jraw = np.stack(cols)
+    assert jraw.shape[0] == p
+    return d, jraw, CONVERGED
+
+
+def normalise(d, jraw):
+    """Alg. 1 Step 1: D_hat = d/||d||_F, J = d/dzeta (D o zeta/||D o zeta||_F).
+
+    Quotient rule: J = (J_raw - D_hat (D_hat^T J_raw)) / ||d||_F.
+    """
+    nd = float(np.linalg.norm(d))
+    dh = d / nd
+    c = np.tensordot(jraw, dh, axes=([1, 2], [0, 1]))  # D_hat^T J_raw, one entry per parameter
+    j = (jraw - c[:, None, None] * dh[None, :, :]) / nd
+    return dh, j, nd
+
+
+def constraints_q(tau, kind, m, n):
+    """Q (l=3 rows): centre x, centre y and area of the transformed window (Z10).
+
+    Centre = tau(0, 0) = (h13, h23): rows are the unit vectors on h13, h23. Area = shoelace area of
+    tau applied to the window corners (+-n/N, +-m/N), N = max(m, n); its gradient w.r.t. tau is
+    taken analytically (quotient rule per corner). Each row is scaled to unit norm.
+    """
+    p = 6 if kind == AFFINE else 8
+    h = tau_to_h(tau, kind)
+    big = max(m, n)
+    cu, cv = n / big, m / big
+    corners = [(-cu, -cv), (cu, -cv), (cu, cv), (-cu, cv)]
+    pts, grads = [], []
+    for (u, v) in corners:
+        w = h[2, 0] * u + h[2, 1] * v + 1.0
+        x = (h[0, 0] * u + h[0, 1] * v + h[0, 2]) / w
+        y = (h[1, 0] * u + h[1, 1] * v + h[1, 2]) / w
+        gx = np.zeros(p)
+        gy = np.zeros(p)
+        gx[0], gx[1], gx[4] = u / w, v / w, 1.0 / w
+        gy[2], gy[3], gy[5] = u / w, v / w, 1.0 / w
+        if kind == HOMOGRAPHY:
+            gx[6], gx[7] = -x * u / w, -x * v / w
+            gy[6], gy[7] = -y * u / w, -y * v / w
+        pts.append((x, y))
+        grads.append((gx, gy))
+    garea = np.zeros(p)
+    for k in range(4):
+        (xa, ya), (xb, yb) = pts[k], pts[(k + 1) % 4]
+        (gxa, gya), (gxb, gyb) = grads[k], grads[(k + 1) % 4]
+        # area = 1/2 sum_k (x_k y_{k+1} - x_{k+1} y_k)
+        garea += 0.5 * (gxa * yb + xa * gyb - gxb * ya - xb * gya)
+    q = np.zeros((3, p))
+    q[0, 4] = 1.0
+    q[1, 5] = 1.0
+    q[2] = garea / np.linalg.norm(garea)
+    return q
+
+
+def shoelace_area(tau, kind, m, n):
+    """Area of tau(window corners), the quantity whose gradient is Q's third row (test helper)."""
+    h = tau_to_h(tau, kind)
+    big = max(m, n)
+    cu, cv = n / big, m / big
+    pts = []
+    for (u, v) in [(-cu, -cv), (cu, -cv), (cu, cv), (-cu, cv)]:
+        w = h[2, 0] * u + h[2, 1] * v + 1.0
+        pts.append(((h[0, 0] * u + h[0, 1] * v + h[0, 2]) / w, (h[1, 0] * u + h[1, 1] * v + h[1, 2]) / w))
+    return 0.5 * sum(pts[k][0] * pts[(k + 1) % 4][1] - pts[(k + 1) % 4][0] * pts[k][1] for k in range(4))
+
+
+# ----------------------------------------------------------------------------------------------
+# The operator W^T W = I - J (J^T J + Q^T Q)^{-1} J^T  (P:587-606 Eq. Jperpv)
+# ----------------------------------------------------------------------------------------------
+
+class Projector:
+    """W^T W applied implicitly: v - J((J^T J + Q^T Q)^{-1}(J^T v))  (Eq. Jperpv, Eq. WTW_property).
+
+    With Q = None this is J_perp = I - J (J^T J)^{-1} J^T. ``count`` instruments the number
+    of applications (two per LADMAP iteration).
+    """
+
+    class SingularGram(Exception):
+        pass
+
+    def __init__(self, j, q=None):
+        j = np.asarray(j, dtype=np.float64)
+        self.shape = j.shape[1:]
+        self.jm = j.reshape(j.shape[0], -1).T  # mn x p ("arranged in an mn x p matrix")
+        g = self.jm.T @ self.jm
+        if q is not None:
+            q = np.asarray(q, dtype=np.float64)
+            g = g + q.T @ q
+        self.q = q
+        self.g = g
+        try:
+            self.chol = np.linalg.cholesky(g)  # "(J^T J)^{-1} ... can be pre-computed"
+        except np.linalg.LinAlgError as exc:
+            raise Projector.SingularGram(str(exc)) from exc
+        if not np.all(np.isfinite(self.chol)) or np.min(np.diag(self.chol)) <= 0:
+            raise Projector.SingularGram("non-positive pivot")
+        self.count = 0
+
+    def _gsolve(self, r):
+        y = np.linalg.solve(self.chol, r)
+        return np.linalg.solve(self.chol.T, y)
+
+    def apply(self, v):
+        """W^T W v for an m x n matrix v (vectorised row-major, reading Z1)."""
+        self.count += 1
+        vv = np.asarray(v, dtype=np.float64).reshape(-1)
+        out = vv - self.jm @ self._gsolve(self.jm.T @ vv)
+        return out.reshape(self.shape)
+
+    def delta_tau(self, r):
+        """Delta tau* = (J^T J + Q^T Q)^{-1} J^T r  (Eq. Delta_tau P:376-378 with Q)."""
+        return self._gsolve(self.jm.T @ np.asarray(r, dtype=np.float64).reshape(-1))
+
+
+# ----------------------------------------------------------------------------------------------
+# LADMAP inner loop (P:437-468 Eqs. A, E, Y, mu, rho; P:489-497 Cond1/2; P:708-749 Eq. newvars2)
+# ----------------------------------------------------------------------------------------------
+
+@dataclass
+class InnerResult:
+    A: np.ndarray
+    E: np.ndarray
+    Y: np.ndarray
+    iters: int
+    mu: float               # mu_k used by the last iteration's updates
+    sigma_m: np.ndarray     # singular values of the last M_k (so sigma(A) = T_{1/mu}(sigma_m))
+    crit1: float
+    crit2: float
+    trace: list = field(default_factory=list)   # (mu_k, crit1, crit2, rho_bit) per iteration
+    converged: bool = False
+
+
+def ladmap(dh, proj, lam, mu0, mu_max, rho0, eps1, eps2, max_inner, a0, e0, y0,
+           fixed_iters=0, rho_replay=None):
+    """LADMAP for min ||A||_* + lam ||E||_1  s.t.  W^T W (A + E) = W^T W D  (Eq. reformulated_TILT2).
+
+    Iteration (Eq. newvars2, with errata E1 (+ sign of the dual step, as Eq. Y)
+    and E2 (N_k starts from E_k, as P:451 / Eq. update_y' P:343-347)):
+        M_k     = A_k - Y_k/mu_k - W^TW(A_k + E_k - D)
+        A_{k+1} = S_{1/mu_k}(M_k)                                   (Eq. A_1)
+        N_k     = E_k - Y_k/mu_k - W^TW(A_{k+1} + E_k - D)
+        E_{k+1} = T_{lam/mu_k}(N_k)                                 (Eq. E_1)
+        Y_{k+1} = Y_k + mu_k W^TW(A_{k+1} + E_{k+1} - D)            (Eq. newvars2 / Eq. Y)
+        rho     = rho0 if mu_k max(||dA||, ||dE||)/||W^TW D|| < eps2 else 1   (Eq. rho)
+        mu_{k+1} = min(mu_max, rho mu_k)                             (Eq. mu)
+    The product W^TW(A_{k+1}+E_{k+1}-D) is reused for the next M, so two
+    projector applications are made per iteration. Stop when Cond1 and Cond2 hold (P:489-497,
+    strict inequalities, reading Z12), unless ``fixed_iters`` > 0 (test mode).
+    ``rho_replay`` (sequence of 0/1) overrides the rho decision (parity protocol, reading Z21).
+    """
+    denom = float(np.linalg.norm(proj.apply(dh)))
+    if denom == 0.0:  # D in span(J): the crit denominators degenerate; use 1 (reading R9)
+        denom = 1.0
+    a, e, y = a0.copy(), e0.copy(), y0.copy()
+    r = proj.apply(a + e - dh)
+    mu = mu0
+    trace = []
+    n_iter = fixed_iters if fixed_iters > 0 else max_inner
+    crit1 = crit2 = float("nan")
+    sig = None
+    converged = False
+    k = 0
+    for k in range(n_iter):
+        m_k = a - y / mu - r
+        a1, sig = svt(m_k, 1.0 / mu)
+        n_k = e - y / mu - proj.apply(a1 + e - dh)
+        e1 = shrink(n_k, lam / mu)
+        r = proj.apply(a1 + e1 - dh)
+        y = y + mu * r
+        crit1 = float(np.linalg.norm(r)) / denom
+        crit2 = mu * max(float(np.linalg.norm(a1 - a)), float(np.linalg.norm(e1 - e))) / denom
+        a, e = a1, e1
+        rho_bit = 1 if crit2 < eps2 else 0
+        if rho_replay is not None and k < len(rho_replay):
+            rho_bit = int(rho_replay[k])
+        trace.append((mu, crit1, crit2, rho_bit))
+        mu_used = mu
+        if crit1 < eps1 and crit2 < eps2:
+            converged = True
+            if fixed_iters <= 0:
+                return InnerResult(a, e, y, k + 1, mu_used, sig, crit1, crit2, trace, True)
+        mu = min(mu_max, (rho0 if rho_bit else 1.0) * mu)
+    return InnerResult(a, e, y, n_iter, trace[-1][0] if trace else mu, sig, crit1, crit2, trace,
+                       converged)
+
+
+# ----------------------------------------------------------------------------------------------
+# Algorithm 1: TILT via LADMAP + VWS
+# ----------------------------------------------------------------------------------------------
+
+def relative_rank(sigma_a):
+    """Reading Z19: rank = #{sigma_j(A) > 1e-3 sigma_1(A)}; band flag if a ratio is in [3e-4, 3e-3]."""
+    s = np.sort(np.asarray(sigma_a, dtype=np.float64))[::-1]
+    if s.size == 0 or s[0] <= 0:
+        return 0, False
+    ratio = s / s[0]
+    return int(np.sum(ratio > 1e-3)), bool(np.any((ratio >= 3e-4) & (ratio <= 3e-3)))
+
+
+def tilt(image, box, tau0, kind, prm: Params = Params(), rho_replay=None):
+    """Algorithm 1 for one window; returns a dict (tau, A, E, Y, report fields, traces).
+
+    Step 1: normalise D o tau and compute J; Q per reading Z10.
+    Step 2: LADMAP with the warm starts A_0 = A_inf, E_0 = E_inf (Eq. warm_start) and
+            Y_0 = W^TW Y_inf (Eq. Y_new_warmstart); first pass A_0 = D o tau, E_0 = Y_0 = 0
+            (reading Z4). mu_0 = mu0_scale/sigma_1(D_hat) each inner loop (Z3, Z5).
+    Step 3: Delta tau* (Eq. Delta_tau; with Q the stacked least squares P:671-684).
+    Step 4: tau^{i+1} = tau^i + Delta tau* (P:568-570).
+    Outer stop ("while not converged", reading Z9).
+    ``rho_replay``: optional list (per outer iteration) of 0/1 sequences (reading Z21).
+    """
+    m, n = int(box[3]), int(box[2])
+    lam = prm.lam if prm.lam > 0 else 1.0 / math.sqrt(max(m, n))
+    tau = np.asarray(tau0, dtype=np.float64).copy()
+    a = e = y = None
+    f_prev = None
+    status = MAX_OUTER
+    stop_rule = STOP_NONE
+    outer_traces = []
+    inner_iters = 0
+    res = None
+    nd = float("nan")
+    dtau_inf = float("nan")
+    f = float("nan")
+    n_outer = prm.fixed_outer_iters if prm.fixed_outer_iters > 0 else prm.max_outer
+    it_done = 0
+    for it in range(n_outer):
+        d, jraw, st = warp(image, box, tau, kind)
+        if st != CONVERGED:
+            status = st
+            break
+        nd = float(np.linalg.norm(d))
+        if nd == 0.0:
+            status = ZERO_PATCH
+            break
+        dh, j, nd = normalise(d, jraw)
+        q = constraints_q(tau, kind, m, n) if prm.constraints else None
+        try:
+            proj = Projector(j, q)
+        except Projector.SingularGram:
+            status = SINGULAR_GRAM
+            break
+        if a is None or not prm.vws:
+            a, e, y = dh.copy(), np.zeros_like(dh), np.zeros_like(dh)
+        else:
+            y = proj.apply(y)                      # Eq. Y_new_warmstart
+        sigma1 = float(np.linalg.svd(dh, compute_uv=False)[0])
+        mu0 = prm.mu0_scale / sigma1
+        replay = rho_replay[it] if rho_replay is not None and it < len(rho_replay) else None
+        res = ladmap(dh, proj, lam, mu0, prm.mu_max_ratio * mu0, prm.rho0, prm.eps1, prm.eps2,
+                     prm.max_inner, a, e, y, fixed_iters=prm.fixed_inner_iters, rho_replay=replay)
+        a, e, y = res.A, res.E, res.Y
+        inner_iters += res.iters
+        outer_traces.append(res.trace)
+        dtau = proj.delta_tau(a + e - dh)          # Step 3
+        tau = tau + dtau                           # Step 4
+        dtau_inf = float(np.max(np.abs(dtau)))
+        f = float(shrink(res.sigma_m, 1.0 / res.mu).sum()) + lam * float(np.abs(e).sum())
+        it_done = it + 1
+        if not np.isfinite(f) or f > 1e12 or not np.all(np.isfinite(tau)):
+            status = DIVERGED
+            break
+        rule = STOP_NONE
+        if f_prev is not None and abs(f - f_prev) < prm.obj_tol * abs(f_prev):
+            rule = STOP_OBJECTIVE
+        elif dtau_inf < prm.tau_tol:
+            rule = STOP_DTAU
+        f_prev = f
+        if rule != STOP_NONE:
+            status, stop_rule = CONVERGED, rule
+            if prm.fixed_outer_iters <= 0:
+                break
+        else:
+            status, stop_rule = MAX_OUTER, STOP_MAX_OUTER
+    sig_a = shrink(res.sigma_m, 1.0 / res.mu) if res is not None else np.zeros(1)
+    rank, band = relative_rank(sig_a)
+    return {
+        "status": status, "stop_rule": stop_rule, "tau": tau, "A": a, "E": e, "Y": y,
+        "outer_iters": it_done, "inner_iters": inner_iters, "objective": f,
+        "rank": rank, "rank_band": band, "svt_rank": int(np.sum(res.sigma_m > 1.0 / res.mu)) if res else 0,
+        "crit1": res.crit1 if res else float("nan"), "crit2": res.crit2 if res else float("nan"),
+        "patch_norm": nd, "dtau_inf": dtau_inf, "traces": outer_traces, "lam": lam,
+    }
+
+
+def downsample2x(image):
+    """2x2 box filter for the 2-level pyramid of config 3 (reading Z18; the paper has none)."""
+    img = np.asarray(image, dtype=np.float64)
+    hh, ww = img.shape[0] // 2 * 2, img.shape[1] // 2 * 2
+    img = img[:hh, :ww]
+    return 0.25 * (img[0::2, 0::2] + img[0::2, 1::2] + img[1::2, 0::2] + img[1::2, 1::2])
+
+
+def tilt_pyramid(image, box, tau0, kind, prm: Params = Params(), levels: int = 2):
+    """Coarse-to-fine TILT (reading Z18): solve on the 2x2-downsampled image with box/2, then on the
+    full image starting from the coarse tau (unchanged: the normalised frames coincide)."""
+    if levels <= 1:
+        return tilt(image, box, tau0, kind, prm)
+    coarse_img = np.asarray(image, dtype=np.float64)
+    x0, y0, w, h = (int(v) for v in box)
+    for _ in range(levels - 1):
+        coarse_img = downsample2x(coarse_img)
+        x0, y0, w, h = x0 // 2, y0 // 2, w // 2, h // 2
+    res_c = tilt(coarse_img.astype(np.float32).astype(np.float64), (x0, y0, w, h), tau0, kind,
+                 replace(prm, lam=prm.lam))
+    if res_c["status"] not in (CONVERGED, MAX_OUTER):
+        return res_c
+    res_f = tilt(image, box, res_c["tau"], kind, prm)
+    res_f["coarse"] = res_c
+    return res_f
+
+
+def _tilt_job(args):
+    image, box, tau0, kind, prm, levels = args
+    return tilt_pyramid(image, box, tau0, kind, prm, levels)
+
+
+def tilt_batch(images, patch_image, boxes, tau0, kind, prm: Params = Params(), levels=1,
+               n_workers=1):
+    """Independent patches (north_star: "large batches of independent image patches")."""
+    jobs = [(np.asarray(images[patch_image[b]], dtype=np.float64), boxes[b], tau0[b], kind, prm, levels)
+            for b in range(len(boxes))]
+    if n_workers <= 1 or len(jobs) <= 1:
+        return [_tilt_job(j) for j in jobs]
+    import multiprocessing as mp
+    ctx = mp.get_context("fork")
+    with ctx.Pool(min(n_workers, len(jobs))) as pool:
+        return pool.map(_tilt_job, jobs)

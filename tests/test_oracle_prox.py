@@ -1,0 +1,99 @@
+"""Pins for the oracle's proximal operators and SVD step.
+
+Each check is tied to something other than the oracle's own formula: closed forms printed in the
+paper / SPEC examples, a brute-force grid minimiser, an independent eigen-solver, the subgradient
+characterisation of the nuclear-norm prox, and the paper's pseudocontraction inequality.
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+
+
+def test_shrink_closed_form():
+    # P:482 T_eps(x) = sgn(x) max(|x| - eps, 0); SPEC S:56-57 examples
+    assert O.shrink(1.2, 0.5) == pytest.approx(0.7)
+    assert O.shrink(-0.3, 0.5) == 0.0
+    assert O.shrink(-2.0, 0.5) == pytest.approx(-1.5)
+    assert O.shrink(0.5, 0.5) == 0.0
+
+
+def test_shrink_is_argmin_grid():
+    # T_{lam/mu}(x) = argmin_e lam|e| + mu/2 (e - x)^2  (Eq. E P:444 / Eq. E_1), brute force
+    rng = np.random.default_rng(0)
+    lam, mu = 0.3, 2.0
+    grid = np.arange(-3.0, 3.0, 1e-4)
+    for x in rng.uniform(-2, 2, size=20):
+        f = lam * np.abs(grid) + 0.5 * mu * (grid - x) ** 2
+        assert O.shrink(x, lam / mu) == pytest.approx(grid[np.argmin(f)], abs=2e-4)
+
+
+def test_svt_closed_forms():
+    # diag(3,1), eps=2 -> diag(1,0); eps = 0 -> M
+    a, sig = O.svt(np.diag([3.0, 1.0]), 2.0)
+    np.testing.assert_allclose(a, np.diag([1.0, 0.0]), atol=1e-14)
+    rng = np.random.default_rng(1)
+    m = rng.normal(size=(7, 5))
+    np.testing.assert_allclose(O.svt(m, 0.0)[0], m, atol=1e-12)
+    # eps above sigma_1 kills everything
+    np.testing.assert_allclose(O.svt(m, 1e3)[0], 0.0, atol=0)
+
+
+@pytest.mark.parametrize("shape", [(6, 6), (9, 5), (5, 9), (30, 30)])
+def test_svt_subgradient_certificate(shape):
+    """A = S_eps(M) iff M - A in eps * d||A||_*, i.e. ||M - A||_2 <= eps and <M - A, A> = eps ||A||_*
+    (prox of the nuclear norm). Norms via an independent symmetric eigensolver."""
+    rng = np.random.default_rng(shape[0] * 31 + shape[1])
+    m = rng.normal(size=shape)
+    eps = 0.7 * np.linalg.norm(m, 2) / 3
+    a, _ = O.svt(m, eps)
+    r = m - a
+    spec = np.sqrt(np.max(np.linalg.eigvalsh(r.T @ r)))
+    ev = np.linalg.eigvalsh(a.T @ a)
+    nuc = np.sum(np.sqrt(ev[ev > 1e-12 * ev.max()]))
+    assert spec <= eps * (1 + 1e-12)
+    assert np.sum(r * a) == pytest.approx(eps * nuc, rel=1e-10)
+    # and it beats random perturbations on eps||A||_* + 1/2||A - M||^2
+    def obj(x):
+        return eps * np.sum(np.linalg.svd(x, compute_uv=False)) + 0.5 * np.sum((x - m) ** 2)
+    f0 = obj(a)
+    for _ in range(10):
+        assert obj(a + 1e-3 * rng.normal(size=shape)) >= f0
+
+
+@pytest.mark.parametrize("k", range(1, 9))
+def test_svd_step_reconstruction_tiny(k):
+    # P3: reconstruction / orthogonality on tiny matrices incl. rank-deficient and repeated sigma
+    rng = np.random.default_rng(k)
+    mats = [rng.normal(size=(k, k)), np.eye(k) * 2.0, np.outer(rng.normal(size=k), rng.normal(size=k))]
+    for mm in mats:
+        u, s, vt = np.linalg.svd(mm)
+        assert np.linalg.norm(mm - (u * s) @ vt) <= 1e-12 * max(1.0, np.linalg.norm(mm))
+        assert np.linalg.norm(u.T @ u - np.eye(k)) <= 1e-12
+        assert np.linalg.norm(vt @ vt.T - np.eye(k)) <= 1e-12
+        # sigma^2 vs an independent symmetric eigensolver of M^T M
+        np.testing.assert_allclose(np.sort(s ** 2), np.sort(np.linalg.eigvalsh(mm.T @ mm)), atol=1e-8)
+    _, sig = O.svt(np.eye(3), 0.0)
+    np.testing.assert_allclose(sig, [1, 1, 1])
+
+
+def test_pseudocontraction_inequality():
+    """||S(W1)-S(W2)||^2 <= ||W1-W2||^2 - ||(S(W1)-W1)-(S(W2)-W2)||^2 (and for T_eps)."""
+    rng = np.random.default_rng(4)
+    for _ in range(100):
+        w1, w2 = rng.normal(size=(2, 8, 6))
+        eps = rng.uniform(0.1, 2.0)
+        s1, s2 = O.svt(w1, eps)[0], O.svt(w2, eps)[0]
+        lhs = np.sum((s1 - s2) ** 2)
+        rhs = np.sum((w1 - w2) ** 2) - np.sum(((s1 - w1) - (s2 - w2)) ** 2)
+        assert lhs <= rhs + 1e-8
+        t1, t2 = O.shrink(w1, eps), O.shrink(w2, eps)
+        assert np.sum((t1 - t2) ** 2) <= np.sum((w1 - w2) ** 2) - np.sum(((t1 - w1) - (t2 - w2)) ** 2) + 1e-8
+
+
+def test_objective_closed_forms():
+    # A = diag(2,3), E = 0 -> 5; A = 0, k entries +-1, lam = .5 -> .5k
+    assert O.objective(np.diag([2.0, 3.0]), np.zeros((2, 2)), 1.0) == pytest.approx(5.0)
+    e = np.zeros((4, 4))
+    e[0, 0], e[1, 2], e[3, 3] = 1, -1, 1
+    assert O.objective(np.zeros((4, 4)), e, 0.5) == pytest.approx(1.5)

@@ -1,0 +1,42 @@
+"""The seeded input generator (tilt_synth) is deterministic and follows its stated recipe."""
+import dataclasses
+
+import numpy as np
+
+import tilt_synth as ts
+
+
+def test_deterministic_per_patch_index():
+    cfg = ts.CONFIGS[2]
+    a = ts.gen_patch(cfg, 17)
+    b = ts.gen_batch(cfg, 15, 4)
+    np.testing.assert_array_equal(a["canvas"], b["images"][2])
+    np.testing.assert_array_equal(a["tau_g"], b["tau_g"][2])
+    assert a["canvas"].dtype == np.float32 and a["canvas"].shape == (100, 100)
+    assert tuple(a["box"]) == (25, 25, 50, 50)
+
+
+def test_corruption_count_exact():
+    base = dataclasses.replace(ts.CONFIGS[1], corrupt=0.0, config_id=77)
+    corr = dataclasses.replace(base, corrupt=0.25)
+    a = ts.gen_patch(base, 3)["canvas"]
+    b = ts.gen_patch(corr, 3)["canvas"]
+    # the texture is drawn before the corruption, so only the corrupted pixels differ (reading Z23)
+    assert np.sum(a != b) <= int(round(0.25 * a.size))
+    assert np.sum(a != b) >= int(round(0.25 * a.size)) - 5  # a U[0,1] draw can equal the texel
+
+
+def test_undeformed_texture_has_rank_r():
+    base = dataclasses.replace(ts.CONFIGS[1], corrupt=0.0, config_id=78)
+    for r in (2, 3):
+        p = ts.gen_patch(base, 0, planted=False, rank=r)
+        x0, y0, w, h = p["box"]
+        win = p["canvas"][y0:y0 + h, x0:x0 + w].astype(np.float64)
+        s = np.linalg.svd(win, compute_uv=False)
+        assert np.sum(s > 1e-5 * s[0]) == r
+
+
+def test_table1_instance_shapes():
+    inst = ts.table1_instance(10, 6, 0)
+    assert inst["D"].shape == (10, 10) and inst["J"].shape == (6, 10, 10)
+    assert np.all(np.abs(inst["D"]) <= 0.5)
