@@ -461,9 +461,10 @@ def tilt_pyramid(image, box, tau0, kind, prm: Params = Params(), levels: int = 2
         x0, y0, w, h = x0 // 2, y0 // 2, w // 2, h // 2
     res_c = tilt(coarse_img.astype(np.float32).astype(np.float64), (x0, y0, w, h), tau0, kind,
                  replace(prm, lam=prm.lam))
-    if res_c["status"] not in (CONVERGED, MAX_OUTER):
-        return res_c
+    # the fine level always starts from the coarse tau (a failed coarse level keeps its last tau)
     res_f = tilt(image, box, res_c["tau"], kind, prm)
+    for key in ("outer_iters", "inner_iters"):
+        res_f[key] += res_c[key]
     res_f["coarse"] = res_c
     return res_f
 

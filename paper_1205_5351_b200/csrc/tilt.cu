@@ -1,0 +1,637 @@
+// tilt.cu — C ABI of libtilt (include/tilt.h): handle, validation, size-class dispatch, launches.
+// Paper: Ren & Lin, arXiv 1205.5351. Design: DESIGN.md.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "tilt_kernels.cuh"
+
+using namespace tilt;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+tilt_status cuda_fail(cudaError_t e, const char* what) {
+  char buf[512];
+  snprintf(buf, sizeof(buf), "%s: %s", what, cudaGetErrorString(e));
+  g_last_error = buf;
+  return TILT_E_CUDA;
+}
+
+#define TILT_CUDA(call)                                 \
+  do {                                                  \
+    cudaError_t e_ = (call);                            \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
+  } while (0)
+
+enum SizeClass { SC32 = 0, SC64 = 1, SC128 = 2, SC256 = 3, SC_NONE = 4 };
+
+SizeClass size_class(int m, int n) {
+  const int d = m > n ? m : n;
+  if (d <= 32) return SC32;
+  if (d <= 64) return SC64;
+  if (d <= 128) return SC128;
+  if (d <= 256) return SC256;
+  return SC_NONE;
+}
+
+}  // namespace
+
+struct tilt_handle {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int num_sms = 0;
+  int max_batch = 0, max_m = 0, max_n = 0, max_p = 8;
+  int64_t max_image_elems = 0;
+  // workspace
+  float* ws = nullptr;
+  size_t ws_floats = 0;   // total
+  int ws_slots = 0;
+  int* counter = nullptr;  // work-queue counters
+  float* coarse_images = nullptr;
+  int* coarse_boxes = nullptr;
+  tilt_report* coarse_rep = nullptr;
+  // host-entry staging
+  float* h_images = nullptr;
+  int* h_patch = nullptr;
+  int* h_boxes = nullptr;
+  float* h_tau0 = nullptr;
+  float* h_tau = nullptr;
+  float* h_A = nullptr;
+  float* h_E = nullptr;
+  tilt_report* h_rep = nullptr;
+  int64_t launches = 0;
+};
+
+namespace {
+
+template <class C>
+int occupancy_for(const void* fn, size_t smem) {
+  int nb = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, C::NT, smem) != cudaSuccess) return 0;
+  return nb;
+}
+
+DevParams to_dev(const tilt_params* prm) {
+  DevParams P;
+  P.lambda = prm->lambda;
+  P.mu0_scale = prm->mu0_scale;
+  P.mu_max_ratio = prm->mu_max_ratio;
+  P.rho0 = prm->rho0;
+  P.eps1 = prm->eps1;
+  P.eps2 = prm->eps2;
+  P.obj_tol = prm->obj_tol;
+  P.tau_tol = prm->tau_tol;
+  P.max_inner = prm->max_inner;
+  P.max_outer = prm->max_outer;
+  P.constraint_mode = prm->constraint_mode;
+  P.vws = prm->vws;
+  P.svd_warm = prm->svd_warm;
+  P.jacobi_tol = prm->jacobi_tol;
+  P.jacobi_max_sweeps = prm->jacobi_max_sweeps;
+  P.fixed_inner = prm->fixed_inner_iters;
+  P.fixed_outer = prm->fixed_outer_iters;
+  P.rho_replay = prm->rho_replay;
+  P.trace = prm->trace;
+  return P;
+}
+
+bool params_ok(const tilt_params* p) {
+  if (!p) return false;
+  const float fs[] = {p->mu0_scale, p->mu_max_ratio, p->rho0, p->eps1, p->eps2, p->obj_tol, p->tau_tol};
+  for (float f : fs)
+    if (!std::isfinite(f)) return false;
+  if (!std::isfinite(p->lambda) || !std::isfinite(p->jacobi_tol)) return false;
+  if (p->mu0_scale <= 0.f || p->mu_max_ratio < 1.f || p->rho0 < 1.f || p->eps1 <= 0.f || p->eps2 <= 0.f) return false;
+  if (p->max_inner <= 0 || p->max_outer <= 0 || p->jacobi_max_sweeps <= 0) return false;
+  if (p->fixed_inner_iters < 0 || p->fixed_outer_iters < 0) return false;
+  if (p->fixed_inner_iters > p->max_inner || p->fixed_outer_iters > p->max_outer) return false;
+  if (p->pyramid_levels < 1 || p->pyramid_levels > 2) return false;
+  if (p->constraint_mode != TILT_CONSTRAINTS_NONE && p->constraint_mode != TILT_CONSTRAINTS_CENTER_AREA) return false;
+  return true;
+}
+
+template <class C>
+struct Launch {
+  static size_t smem(int mn, int p) { return Layout<C>::smem_bytes(mn, p); }
+
+  static tilt_status prep(const void* fn, size_t sm) {
+    if (sm > 48 * 1024) TILT_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    return TILT_OK;
+  }
+
+  // grid size (persistent): num_sms * occupancy, capped by B and by the workspace slots
+  static tilt_status grid(tilt_handle* h, const void* fn, size_t sm, int B, int mn, int p, int* g) {
+    tilt_status s = prep(fn, sm);
+    if (s != TILT_OK) return s;
+    const int occ = occupancy_for<C>(fn, sm);
+    if (occ <= 0) {
+      g_last_error = "kernel does not fit on an SM (shared memory / registers)";
+      return TILT_E_UNSUPPORTED;
+    }
+    int gsz = h->num_sms * occ;
+    if (gsz > B) gsz = B;
+    const size_t wsf = Layout<C>::ws_floats(mn, p);
+    if (wsf > 0) {
+      const size_t slots = h->ws_floats / wsf;
+      if (slots == 0) {
+        g_last_error = "workspace too small for this size (raise max_m/max_n/max_p at tilt_create)";
+        return TILT_E_ARG;
+      }
+      if ((size_t)gsz > slots) gsz = (int)slots;
+    }
+    *g = gsz < 1 ? 1 : gsz;
+    return TILT_OK;
+  }
+
+  static tilt_status solve(tilt_handle* h, SolveArgs a) {
+    const int mn = a.m * a.n;
+    const void* fn = (const void*)k_solve<C>;
+    const size_t sm = smem(mn, a.p);
+    int g = 0;
+    tilt_status s = grid(h, fn, sm, a.B, mn, a.p, &g);
+    if (s != TILT_OK) return s;
+    a.ws = Layout<C>::ws_floats(mn, a.p) ? h->ws : nullptr;
+    a.ws_stride = Layout<C>::ws_floats(mn, a.p);
+    TILT_CUDA(cudaMemsetAsync(a.counter, 0, sizeof(int), h->stream));
+    k_solve<C><<<g, C::NT, sm, h->stream>>>(a);
+    h->launches++;
+    TILT_CUDA(cudaGetLastError());
+    return TILT_OK;
+  }
+
+  static tilt_status inner(tilt_handle* h, InnerArgs a) {
+    const int mn = a.m * a.n;
+    const void* fn = (const void*)k_inner<C>;
+    const size_t sm = smem(mn, a.p);
+    int g = 0;
+    tilt_status s = grid(h, fn, sm, a.B, mn, a.p, &g);
+    if (s != TILT_OK) return s;
+    a.ws = Layout<C>::ws_floats(mn, a.p) ? h->ws : nullptr;
+    a.ws_stride = Layout<C>::ws_floats(mn, a.p);
+    k_inner<C><<<g, C::NT, sm, h->stream>>>(a);
+    h->launches++;
+    TILT_CUDA(cudaGetLastError());
+    return TILT_OK;
+  }
+
+  static tilt_status svt(tilt_handle* h, SvtArgs a) {
+    const int mn = a.m * a.n;
+    const void* fn = (const void*)k_svt<C>;
+    const size_t sm = smem(mn, 0);
+    int g = 0;
+    tilt_status s = grid(h, fn, sm, a.B, mn, 0, &g);
+    if (s != TILT_OK) return s;
+    a.ws = Layout<C>::ws_floats(mn, 0) ? h->ws : nullptr;
+    a.ws_stride = Layout<C>::ws_floats(mn, 0);
+    k_svt<C><<<g, C::NT, sm, h->stream>>>(a);
+    h->launches++;
+    TILT_CUDA(cudaGetLastError());
+    return TILT_OK;
+  }
+
+  static tilt_status project(tilt_handle* h, ProjArgs a) {
+    const int mn = a.m * a.n;
+    const void* fn = (const void*)k_project<C>;
+    const size_t sm = smem(mn, a.p);
+    int g = 0;
+    tilt_status s = grid(h, fn, sm, a.B, mn, a.p, &g);
+    if (s != TILT_OK) return s;
+    a.ws = Layout<C>::ws_floats(mn, a.p) ? h->ws : nullptr;
+    a.ws_stride = Layout<C>::ws_floats(mn, a.p);
+    k_project<C><<<g, C::NT, sm, h->stream>>>(a);
+    h->launches++;
+    TILT_CUDA(cudaGetLastError());
+    return TILT_OK;
+  }
+};
+
+template <template <class> class F, class... Args>
+tilt_status dispatch(SizeClass c, Args... args) {
+  switch (c) {
+    case SC32: return F<CfgS32>::run(args...);
+    case SC64: return F<CfgS64>::run(args...);
+    case SC128: return F<CfgS128>::run(args...);
+    case SC256: return F<CfgS256>::run(args...);
+    default: g_last_error = "m, n must be <= 256"; return TILT_E_ARG;
+  }
+}
+
+template <class C>
+struct SolveF {
+  static tilt_status run(tilt_handle* h, SolveArgs a) { return Launch<C>::solve(h, a); }
+};
+template <class C>
+struct InnerF {
+  static tilt_status run(tilt_handle* h, InnerArgs a) { return Launch<C>::inner(h, a); }
+};
+template <class C>
+struct SvtF {
+  static tilt_status run(tilt_handle* h, SvtArgs a) { return Launch<C>::svt(h, a); }
+};
+template <class C>
+struct ProjF {
+  static tilt_status run(tilt_handle* h, ProjArgs a) { return Launch<C>::project(h, a); }
+};
+
+size_t ws_need(SizeClass c, int mn, int p) {
+  switch (c) {
+    case SC32: return Layout<CfgS32>::ws_floats(mn, p);
+    case SC64: return Layout<CfgS64>::ws_floats(mn, p);
+    case SC128: return Layout<CfgS128>::ws_floats(mn, p);
+    case SC256: return Layout<CfgS256>::ws_floats(mn, p);
+    default: return 0;
+  }
+}
+
+int occ_need(SizeClass c, int mn, int p) {
+  switch (c) {
+    case SC128: {
+      const size_t sm = Layout<CfgS128>::smem_bytes(mn, p);
+      Launch<CfgS128>::prep((const void*)k_solve<CfgS128>, sm);
+      return occupancy_for<CfgS128>((const void*)k_solve<CfgS128>, sm);
+    }
+    case SC256: {
+      const size_t sm = Layout<CfgS256>::smem_bytes(mn, p);
+      Launch<CfgS256>::prep((const void*)k_solve<CfgS256>, sm);
+      return occupancy_for<CfgS256>((const void*)k_solve<CfgS256>, sm);
+    }
+    default: return 1;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t tilt_abi_version(void) { return TILT_ABI_VERSION; }
+
+const char* tilt_status_string(tilt_status s) {
+  switch (s) {
+    case TILT_OK: return "TILT_OK";
+    case TILT_E_ARG: return "TILT_E_ARG: invalid argument";
+    case TILT_E_CUDA: return "TILT_E_CUDA: CUDA runtime error";
+    case TILT_E_OOM: return "TILT_E_OOM: device allocation failed";
+    case TILT_E_UNSUPPORTED: return "TILT_E_UNSUPPORTED";
+    default: return "unknown tilt_status";
+  }
+}
+
+const char* tilt_patch_status_string(int32_t s) {
+  switch (s) {
+    case TILT_PATCH_CONVERGED: return "CONVERGED";
+    case TILT_PATCH_MAX_OUTER: return "MAX_OUTER";
+    case TILT_PATCH_WINDOW_ESCAPE: return "WINDOW_ESCAPE";
+    case TILT_PATCH_SINGULAR_GRAM: return "SINGULAR_GRAM";
+    case TILT_PATCH_ZERO_PATCH: return "ZERO_PATCH";
+    case TILT_PATCH_DIVERGED: return "DIVERGED";
+    default: return "UNKNOWN";
+  }
+}
+
+const char* tilt_last_error(void) { return g_last_error.c_str(); }
+
+tilt_status tilt_default_params(tilt_params* prm) {
+  if (!prm) return TILT_E_ARG;
+  memset(prm, 0, sizeof(*prm));
+  prm->lambda = -1.f;
+  prm->mu0_scale = 1.25f;
+  prm->mu_max_ratio = 1e6f;
+  prm->rho0 = 2.0f;
+  prm->eps1 = 1e-6f;
+  prm->eps2 = 0.1f;
+  prm->obj_tol = 1e-5f;
+  prm->tau_tol = 1e-4f;
+  prm->max_inner = 1000;
+  prm->max_outer = 50;
+  prm->constraint_mode = TILT_CONSTRAINTS_CENTER_AREA;
+  prm->vws = 1;
+  prm->svd_warm = 1;
+  prm->pyramid_levels = 1;
+  prm->jacobi_tol = 0.f;
+  prm->jacobi_max_sweeps = 20;
+  return TILT_OK;
+}
+
+tilt_status tilt_destroy(tilt_handle* h) {
+  if (!h) return TILT_OK;
+  cudaSetDevice(h->device);
+  void* ptrs[] = {h->ws, h->counter, h->coarse_images, h->coarse_boxes, h->coarse_rep, h->h_images, h->h_patch,
+                  h->h_boxes, h->h_tau0, h->h_tau, h->h_A, h->h_E, h->h_rep};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  delete h;
+  return TILT_OK;
+}
+
+tilt_status tilt_create(tilt_handle** out, const tilt_create_opts* o) {
+  if (!out || !o) return TILT_E_ARG;
+  *out = nullptr;
+  if (o->max_batch < 0 || o->max_m < 1 || o->max_n < 1 || o->max_m > 256 || o->max_n > 256) return TILT_E_ARG;
+  if (o->max_p != 6 && o->max_p != 8) return TILT_E_ARG;
+  tilt_handle* h = new tilt_handle();
+  h->device = o->device;
+  h->stream = (cudaStream_t)o->stream;
+  h->max_batch = o->max_batch;
+  h->max_m = o->max_m;
+  h->max_n = o->max_n;
+  h->max_p = o->max_p;
+  h->max_image_elems = o->max_image_elems;
+  cudaError_t e = cudaSetDevice(h->device);
+  if (e != cudaSuccess) {
+    tilt_status s = cuda_fail(e, "cudaSetDevice");
+    delete h;
+    return s;
+  }
+  e = cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, h->device);
+  if (e != cudaSuccess) {
+    tilt_status s = cuda_fail(e, "cudaDeviceGetAttribute");
+    delete h;
+    return s;
+  }
+  auto fail = [&](cudaError_t err, const char* what) {
+    cuda_fail(err, what);
+    tilt_destroy(h);
+    return err == cudaErrorMemoryAllocation ? TILT_E_OOM : TILT_E_CUDA;
+  };
+  const SizeClass c = size_class(h->max_m, h->max_n);
+  const int mn = h->max_m * h->max_n;
+  const size_t wsf = ws_need(c, mn, h->max_p);
+  if (wsf > 0) {
+    const int occ = occ_need(c, mn, h->max_p);
+    h->ws_slots = h->num_sms * (occ > 0 ? occ : 1);
+    h->ws_floats = wsf * h->ws_slots;
+    if ((e = cudaMalloc(&h->ws, h->ws_floats * sizeof(float))) != cudaSuccess) return fail(e, "cudaMalloc(ws)");
+  }
+  if ((e = cudaMalloc(&h->counter, 64 * sizeof(int))) != cudaSuccess) return fail(e, "cudaMalloc(counter)");
+  if (h->max_image_elems > 0) {
+    const size_t nb = (size_t)h->max_batch;
+    if ((e = cudaMalloc(&h->coarse_images, (size_t)h->max_image_elems / 4 * sizeof(float) + 64)) != cudaSuccess)
+      return fail(e, "cudaMalloc(coarse)");
+    if ((e = cudaMalloc(&h->coarse_boxes, 4 * nb * sizeof(int) + 64)) != cudaSuccess) return fail(e, "cudaMalloc");
+    if ((e = cudaMalloc(&h->coarse_rep, nb * sizeof(tilt_report) + 64)) != cudaSuccess) return fail(e, "cudaMalloc");
+    if ((e = cudaMalloc(&h->h_images, (size_t)h->max_image_elems * sizeof(float))) != cudaSuccess)
+      return fail(e, "cudaMalloc");
+    if ((e = cudaMalloc(&h->h_patch, nb * sizeof(int) + 64)) != cudaSuccess) return fail(e, "cudaMalloc");
+    if ((e = cudaMalloc(&h->h_boxes, 4 * nb * sizeof(int) + 64)) != cudaSuccess) return fail(e, "cudaMalloc");
+    if ((e = cudaMalloc(&h->h_tau0, 8 * nb * sizeof(float) + 64)) != cudaSuccess) return fail(e, "cudaMalloc");
+    if ((e = cudaMalloc(&h->h_tau, 8 * nb * sizeof(float) + 64)) != cudaSuccess) return fail(e, "cudaMalloc");
+    if ((e = cudaMalloc(&h->h_A, nb * mn * sizeof(float) + 64)) != cudaSuccess) return fail(e, "cudaMalloc");
+    if ((e = cudaMalloc(&h->h_E, nb * mn * sizeof(float) + 64)) != cudaSuccess) return fail(e, "cudaMalloc");
+    if ((e = cudaMalloc(&h->h_rep, nb * sizeof(tilt_report) + 64)) != cudaSuccess) return fail(e, "cudaMalloc");
+  }
+  *out = h;
+  return TILT_OK;
+}
+
+tilt_status tilt_set_stream(tilt_handle* h, void* stream) {
+  if (!h) return TILT_E_ARG;
+  h->stream = (cudaStream_t)stream;
+  return TILT_OK;
+}
+
+int64_t tilt_launch_count(const tilt_handle* h) { return h ? h->launches : 0; }
+
+static tilt_status solve_level(tilt_handle* h, const float* images, int32_t n_images, int32_t H, int32_t W,
+                               const int32_t* patch_image, const int32_t* boxes, const float* tau0, int32_t B,
+                               int m, int n, int32_t kind, const tilt_params* prm, float* tau_out, float* A_out,
+                               float* E_out, float* Y_out, tilt_report* rep, const tilt_report* rep_prev) {
+  SolveArgs a;
+  memset(&a, 0, sizeof(a));
+  a.images = images;
+  a.n_images = n_images;
+  a.H = H;
+  a.W = W;
+  a.patch_image = patch_image;
+  a.boxes = boxes;
+  a.tau0 = tau0;
+  a.B = B;
+  a.m = m;
+  a.n = n;
+  a.p = kind == TILT_HOMOGRAPHY ? 8 : 6;
+  a.kind = kind;
+  a.P = to_dev(prm);
+  a.tau_out = tau_out;
+  a.A_out = A_out;
+  a.E_out = E_out;
+  a.Y_out = Y_out;
+  a.rep = rep;
+  a.rep_prev = rep_prev;
+  a.counter = h->counter;
+  return dispatch<SolveF>(size_class(m, n), h, a);
+}
+
+// All boxes of one call must share (w, h): read from the caller's box array? The boxes live on
+// the device, so the window size is passed through the first box copied to the host.
+static tilt_status first_box(tilt_handle* h, const int32_t* boxes, int* m, int* n) {
+  int bx[4];
+  TILT_CUDA(cudaMemcpyAsync(bx, boxes, sizeof(bx), cudaMemcpyDeviceToHost, h->stream));
+  TILT_CUDA(cudaStreamSynchronize(h->stream));
+  *n = bx[2];
+  *m = bx[3];
+  return TILT_OK;
+}
+
+tilt_status tilt_solve_batch(tilt_handle* h, const float* images, int32_t n_images, int32_t H, int32_t W,
+                             const int32_t* patch_image, const int32_t* boxes, const float* tau0, int32_t B,
+                             int32_t kind, const tilt_params* prm, float* tau_out, float* A_out, float* E_out,
+                             float* Y_out, tilt_report* rep) {
+  if (!h || !params_ok(prm)) return TILT_E_ARG;
+  if (B < 0 || B > h->max_batch) return TILT_E_ARG;
+  if (B == 0) return TILT_OK;
+  if (!images || !patch_image || !boxes || !tau_out || n_images < 1 || H < 2 || W < 2) return TILT_E_ARG;
+  if (kind != TILT_AFFINE && kind != TILT_HOMOGRAPHY) return TILT_E_ARG;
+  const int p = kind == TILT_HOMOGRAPHY ? 8 : 6;
+  if (p > h->max_p) return TILT_E_ARG;
+  if ((prm->rho_replay || prm->trace) && prm->max_outer <= 0) return TILT_E_ARG;
+  TILT_CUDA(cudaSetDevice(h->device));
+  int m = prm->win_h, n = prm->win_w;
+  tilt_status s = TILT_OK;
+  if (m <= 0 || n <= 0) {
+    s = first_box(h, boxes, &m, &n);
+    if (s != TILT_OK) return s;
+  }
+  if (m < 2 || n < 2 || m > h->max_m || n > h->max_n) {
+    g_last_error = "box size outside [2, max_m] x [2, max_n]";
+    return TILT_E_ARG;
+  }
+  if (prm->pyramid_levels == 2) {
+    if ((m & 1) || (n & 1) || (H & 1) || (W & 1) || m < 8 || n < 8) {
+      g_last_error = "pyramid needs even box and image sizes";
+      return TILT_E_ARG;
+    }
+    if (!h->coarse_images || (int64_t)n_images * H * W > h->max_image_elems) {
+      g_last_error = "pyramid workspace too small (max_image_elems at tilt_create)";
+      return TILT_E_ARG;
+    }
+    const size_t total = (size_t)n_images * (H / 2) * (W / 2);
+    int blocks = (int)((total + 255) / 256);
+    if (blocks > 4 * h->num_sms * 8) blocks = 4 * h->num_sms * 8;
+    k_downsample<<<blocks, 256, 0, h->stream>>>(images, h->coarse_images, n_images, H, W);
+    h->launches++;
+    TILT_CUDA(cudaGetLastError());
+    k_half_boxes<<<(4 * B + 255) / 256, 256, 0, h->stream>>>(boxes, h->coarse_boxes, B);
+    h->launches++;
+    TILT_CUDA(cudaGetLastError());
+    tilt_params pc = *prm;
+    pc.rho_replay = nullptr;
+    pc.trace = nullptr;
+    s = solve_level(h, h->coarse_images, n_images, H / 2, W / 2, patch_image, h->coarse_boxes, tau0, B, m / 2,
+                    n / 2, kind, &pc, tau_out, nullptr, nullptr, nullptr, h->coarse_rep, nullptr);
+    if (s != TILT_OK) return s;
+    return solve_level(h, images, n_images, H, W, patch_image, boxes, tau_out, B, m, n, kind, prm, tau_out, A_out,
+                       E_out, Y_out, rep, rep ? h->coarse_rep : nullptr);
+  }
+  return solve_level(h, images, n_images, H, W, patch_image, boxes, tau0, B, m, n, kind, prm, tau_out, A_out, E_out,
+                     Y_out, rep, nullptr);
+}
+
+tilt_status tilt_solve_batch_host(tilt_handle* h, const float* images, int32_t n_images, int32_t H, int32_t W,
+                                  const int32_t* patch_image, const int32_t* boxes, const float* tau0, int32_t B,
+                                  int32_t kind, const tilt_params* prm, float* tau_out, float* A_out, float* E_out,
+                                  tilt_report* rep) {
+  if (!h || !params_ok(prm)) return TILT_E_ARG;
+  if (B < 0 || B > h->max_batch) return TILT_E_ARG;
+  if (B == 0) return TILT_OK;
+  if (!images || !patch_image || !boxes || !tau_out) return TILT_E_ARG;
+  if (!h->h_images || (int64_t)n_images * H * W > h->max_image_elems) {
+    g_last_error = "host entry needs max_image_elems >= n_images*H*W at tilt_create";
+    return TILT_E_ARG;
+  }
+  const int p = kind == TILT_HOMOGRAPHY ? 8 : 6;
+  const int m = boxes[3], n = boxes[2];
+  if (m < 2 || n < 2 || m > h->max_m || n > h->max_n) return TILT_E_ARG;
+  TILT_CUDA(cudaSetDevice(h->device));
+  const size_t mn = (size_t)m * n;
+  TILT_CUDA(cudaMemcpyAsync(h->h_images, images, (size_t)n_images * H * W * sizeof(float), cudaMemcpyHostToDevice,
+                            h->stream));
+  TILT_CUDA(cudaMemcpyAsync(h->h_patch, patch_image, B * sizeof(int), cudaMemcpyHostToDevice, h->stream));
+  TILT_CUDA(cudaMemcpyAsync(h->h_boxes, boxes, 4 * B * sizeof(int), cudaMemcpyHostToDevice, h->stream));
+  if (tau0)
+    TILT_CUDA(cudaMemcpyAsync(h->h_tau0, tau0, p * B * sizeof(float), cudaMemcpyHostToDevice, h->stream));
+  tilt_params pw = *prm;
+  pw.win_h = m;
+  pw.win_w = n;
+  tilt_status s = tilt_solve_batch(h, h->h_images, n_images, H, W, h->h_patch, h->h_boxes, tau0 ? h->h_tau0 : nullptr,
+                                   B, kind, &pw, h->h_tau, A_out ? h->h_A : nullptr, E_out ? h->h_E : nullptr,
+                                   nullptr, rep ? h->h_rep : nullptr);
+  if (s != TILT_OK) return s;
+  TILT_CUDA(cudaMemcpyAsync(tau_out, h->h_tau, p * B * sizeof(float), cudaMemcpyDeviceToHost, h->stream));
+  if (A_out) TILT_CUDA(cudaMemcpyAsync(A_out, h->h_A, B * mn * sizeof(float), cudaMemcpyDeviceToHost, h->stream));
+  if (E_out) TILT_CUDA(cudaMemcpyAsync(E_out, h->h_E, B * mn * sizeof(float), cudaMemcpyDeviceToHost, h->stream));
+  if (rep) TILT_CUDA(cudaMemcpyAsync(rep, h->h_rep, B * sizeof(tilt_report), cudaMemcpyDeviceToHost, h->stream));
+  TILT_CUDA(cudaStreamSynchronize(h->stream));
+  return TILT_OK;
+}
+
+tilt_status tilt_warp_batch(tilt_handle* h, const float* images, int32_t n_images, int32_t H, int32_t W,
+                            const int32_t* patch_image, const int32_t* boxes, const float* tau, int32_t B, int32_t kind,
+                            float* Dhat, float* J, float* norm, int32_t* status) {
+  if (!h || B < 0) return TILT_E_ARG;
+  if (B == 0) return TILT_OK;
+  if (!images || !patch_image || !boxes || !tau || !Dhat) return TILT_E_ARG;
+  if (kind != TILT_AFFINE && kind != TILT_HOMOGRAPHY) return TILT_E_ARG;
+  TILT_CUDA(cudaSetDevice(h->device));
+  int m = 0, n = 0;
+  tilt_status s = first_box(h, boxes, &m, &n);
+  if (s != TILT_OK) return s;
+  if (m < 2 || n < 2) return TILT_E_ARG;
+  WarpArgs a;
+  a.images = images;
+  a.n_images = n_images;
+  a.H = H;
+  a.W = W;
+  a.patch_image = patch_image;
+  a.boxes = boxes;
+  a.tau = tau;
+  a.B = B;
+  a.m = m;
+  a.n = n;
+  a.p = kind == TILT_HOMOGRAPHY ? 8 : 6;
+  a.kind = kind;
+  a.Dhat = Dhat;
+  a.J = J;
+  a.norm = norm;
+  a.status = status;
+  k_warp<<<B, K1_NT, 0, h->stream>>>(a);
+  h->launches++;
+  TILT_CUDA(cudaGetLastError());
+  return TILT_OK;
+}
+
+tilt_status tilt_svt_batch(tilt_handle* h, const float* M, int32_t B, int32_t m, int32_t n, const float* eps,
+                           float* V_io, float* A, float* sigma, int32_t* sweeps) {
+  if (!h || B < 0 || m < 1 || n < 1 || m > h->max_m || n > h->max_n) return TILT_E_ARG;
+  if (B == 0) return TILT_OK;
+  if (!M || !eps || !A) return TILT_E_ARG;
+  TILT_CUDA(cudaSetDevice(h->device));
+  SvtArgs a;
+  memset(&a, 0, sizeof(a));
+  a.M = M;
+  a.B = B;
+  a.m = m;
+  a.n = n;
+  a.eps = eps;
+  a.V_io = V_io;
+  a.A = A;
+  a.sigma = sigma;
+  a.sweeps = sweeps;
+  a.tol = default_jacobi_tol(m);
+  a.max_sweeps = 20;
+  return dispatch<SvtF>(size_class(m, n), h, a);
+}
+
+tilt_status tilt_project_batch(tilt_handle* h, const float* J, const float* Q, int32_t l, const float* v, int32_t B,
+                               int32_t m, int32_t n, int32_t p, float* Pv, float* dtau, int32_t* status) {
+  if (!h || B < 0 || m < 1 || n < 1 || m > h->max_m || n > h->max_n) return TILT_E_ARG;
+  if (p < 1 || p > 8 || p > h->max_p || (Q && (l < 1 || l > 3))) return TILT_E_ARG;
+  if (B == 0) return TILT_OK;
+  if (!J || !v || !Pv) return TILT_E_ARG;
+  TILT_CUDA(cudaSetDevice(h->device));
+  ProjArgs a;
+  memset(&a, 0, sizeof(a));
+  a.J = J;
+  a.Q = Q;
+  a.l = Q ? l : 0;
+  a.v = v;
+  a.B = B;
+  a.m = m;
+  a.n = n;
+  a.p = p;
+  a.Pv = Pv;
+  a.dtau = dtau;
+  a.status = status;
+  return dispatch<ProjF>(size_class(m, n), h, a);
+}
+
+tilt_status tilt_inner_batch(tilt_handle* h, const float* D, const float* J, const float* Q, int32_t l, int32_t B,
+                             int32_t m, int32_t n, int32_t p, const tilt_params* prm, float* A, float* E, float* Y,
+                             tilt_report* rep) {
+  if (!h || !params_ok(prm) || B < 0 || m < 2 || n < 2 || m > h->max_m || n > h->max_n) return TILT_E_ARG;
+  if (p < 1 || p > 8 || p > h->max_p || (Q && (l < 1 || l > 3))) return TILT_E_ARG;
+  if (B == 0) return TILT_OK;
+  if (!D || !J || !A || !E) return TILT_E_ARG;
+  TILT_CUDA(cudaSetDevice(h->device));
+  InnerArgs a;
+  memset(&a, 0, sizeof(a));
+  a.D = D;
+  a.J = J;
+  a.Q = Q;
+  a.l = Q ? l : 0;
+  a.B = B;
+  a.m = m;
+  a.n = n;
+  a.p = p;
+  a.P = to_dev(prm);
+  a.A = A;
+  a.E = E;
+  a.Y = Y;
+  a.rep = rep;
+  return dispatch<InnerF>(size_class(m, n), h, a);
+}
+
+}  // extern "C"

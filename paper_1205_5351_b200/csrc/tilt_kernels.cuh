@@ -1,0 +1,765 @@
+// tilt_kernels.cuh — LADMAP inner loop, Algorithm 1 outer loop and the kernels of libtilt.
+// Paper: Ren & Lin, arXiv 1205.5351 (/root/reference/PAPER.md, P:<line>); readings: DESIGN.md.
+#pragma once
+
+#include "tilt_device.cuh"
+
+namespace tilt {
+
+// ---------------------------------------------------------------------------------------------
+// Shared-memory / workspace layout per size class
+// ---------------------------------------------------------------------------------------------
+template <class C>
+struct Layout {
+  static __host__ __device__ size_t vec_floats() { return 3 * (size_t)C::MAXD; }
+  static __host__ __device__ size_t svd_floats() { return 3 * (size_t)C::MAXD * C::MAXD; }
+  static __host__ __device__ size_t plane_floats(int mn, int p) { return (size_t)(4 + p) * mn; }
+  static __host__ __device__ size_t smem_bytes(int mn, int p) {
+    size_t s = vec_floats();
+    if (C::SVD_SMEM) s += svd_floats();
+    if (C::PLANES_SMEM) s += plane_floats(mn, p);
+    return s * sizeof(float);
+  }
+  static __host__ __device__ size_t ws_floats(int mn, int p) {
+    size_t s = 0;
+    if (!C::SVD_SMEM) s += svd_floats();
+    if (!C::PLANES_SMEM) s += plane_floats(mn, p);
+    return (s + 31) & ~size_t(31);
+  }
+};
+
+template <class C>
+__device__ __forceinline__ Ctx<C> make_ctx(float* smem, float* ws, Scal* sc, int m, int n, int p) {
+  Ctx<C> cx;
+  constexpr int MD = C::MAXD;
+  float* sp = smem;
+  float* gp = ws;
+  cx.nrm = sp;
+  cx.scl = sp + MD;
+  cx.hv = sp + 2 * MD;
+  sp += 3 * MD;
+  float* svd;
+  if constexpr (C::SVD_SMEM) {
+    svd = sp;
+    sp += 3 * MD * MD;
+  } else {
+    svd = gp;
+    gp += 3 * MD * MD;
+  }
+  cx.B = svd;
+  cx.V = svd + MD * MD;
+  cx.S = svd + 2 * MD * MD;
+  const int mn = m * n;
+  float* pl;
+  if constexpr (C::PLANES_SMEM) {
+    pl = sp;
+  } else {
+    pl = gp;
+  }
+  cx.D = pl;
+  cx.A = pl + mn;
+  cx.E = pl + 2 * mn;
+  cx.Y = pl + 3 * mn;
+  cx.K = pl + 4 * mn;
+  cx.sc = sc;
+  cx.m = m;
+  cx.n = n;
+  cx.p = p;
+  cx.mn = mn;
+  return cx;
+}
+
+__host__ __device__ inline float default_jacobi_tol(int m) { return 8.f * sqrtf((float)m) * 5.9604645e-8f; }
+
+// ---------------------------------------------------------------------------------------------
+// sigma_1(D_hat) for mu_0 (reading Z3): warm one-sided Jacobi on D_hat V; leaves V warm.
+// ---------------------------------------------------------------------------------------------
+template <class C>
+__device__ float sigma1_of_plane(Ctx<C>& cx, const float* X, float tol, int max_sweeps, bool warm,
+                                 int* sweeps) {
+  constexpr int MD = C::MAXD;
+  const int m = cx.m, n = cx.n, mn = cx.mn;
+  for (PixIter pi(threadIdx.x, C::NT, m); pi.idx < mn; pi.next(C::NT)) cx.S[pi.j * MD + pi.i] = X[pi.idx];
+  if (!warm) set_identity<C>(cx.V, n);
+  __syncthreads();
+  gemm_nn<C>(cx.B, cx.S, cx.V, m, n, n);
+  bool capped;
+  *sweeps = jacobi_sweeps<C>(cx, n, tol, max_sweeps, &capped);
+  svt_stats<C>(cx, n, 0.f);
+  __syncthreads();
+  const float s1 = cx.sc->svt_sig1;
+  if (warm) ns_step<C>(cx, n);
+  return s1;
+}
+
+// ---------------------------------------------------------------------------------------------
+// LADMAP inner loop (P:437-468 Eqs. A, E, Y, mu, rho; Cond1/2 P:489-497; constrained form
+// Eq. newvars2 P:731-737 with errata E1 (+ dual step) and E2 (N_k from E_k)):
+//   M_k = A_k - Y_k/mu_k - W^TW(A_k + E_k - D)              (in S on entry / from the dual pass)
+//   A_{k+1} = S_{1/mu_k}(M_k)                                (warm Jacobi SVT)
+//   N_k = E_k - Y_k/mu_k - W^TW(A_{k+1} + E_k - D), E_{k+1} = T_{lam/mu_k}(N_k)
+//   R = W^TW(A_{k+1} + E_{k+1} - D), Y_{k+1} = Y_k + mu_k R  (R reused for M_{k+1}: 2 products)
+//   crit1 = ||R||/||W^TW D||, crit2 = mu_k max(||dA||, ||dE||)/||W^TW D||
+//   rho = rho0 if crit2 < eps2 else 1, mu_{k+1} = min(mu_max, rho mu_k)
+// ---------------------------------------------------------------------------------------------
+struct InnerOut {
+  int iters, sweeps, caps;
+  float mu, crit1, crit2;
+  bool converged;
+};
+
+template <class C>
+__device__ InnerOut ladmap_inner(Ctx<C>& cx, const DevParams& P, float lam, float mu0, float mu_max,
+                                 float denom, float tol, const uint8_t* replay, float* trace) {
+  constexpr int MD = C::MAXD;
+  const int m = cx.m, n = cx.n, mn = cx.mn;
+  const float inv_den = 1.f / denom;
+  const int niter = P.fixed_inner > 0 ? P.fixed_inner : P.max_inner;
+  float* __restrict__ Ap = cx.A;
+  float* __restrict__ Ep = cx.E;
+  float* __restrict__ Yp = cx.Y;
+  const float* __restrict__ Dp = cx.D;
+  InnerOut o;
+  o.iters = 0;
+  o.sweeps = 0;
+  o.caps = 0;
+  o.crit1 = o.crit2 = __int_as_float(0x7fc00000);
+  o.converged = false;
+  float mu = mu0;
+  o.mu = mu;
+  for (int k = 0; k < niter; ++k) {
+    // ---- A step: A_{k+1} = S_{1/mu}(M_k), M_k in S --------------------------------------
+    float dA2 = 0.f;
+    SvtOut so = svt<C, true>(cx, m, n, 1.f / mu, tol, P.jacobi_max_sweeps, P.svd_warm != 0,
+                             [&](int i, int j, float a) {
+                               const int idx = j * m + i;
+                               const float d = a - Ap[idx];
+                               dA2 = fmaf(d, d, dA2);
+                               Ap[idx] = a;
+                             },
+                             P.svd_warm != 0);
+    o.sweeps += so.sweeps;
+    o.caps += so.capped ? 1 : 0;
+    // ---- E step ---------------------------------------------------------------------------
+    const float inv_mu = 1.f / mu;
+    const float thr = lam * inv_mu;
+    float s[8];
+    kt_reduce<C>(cx, [&](int idx) { return Ap[idx] + Ep[idx] - Dp[idx]; }, s);
+    float dE2 = 0.f;
+    for (int idx = threadIdx.x; idx < mn; idx += C::NT) {
+      const float e = Ep[idx];
+      const float v = Ap[idx] + e - Dp[idx];
+      const float pv = v - k_apply<C>(cx, idx, s);
+      const float nk = e - pv - Yp[idx] * inv_mu;
+      const float en = copysignf(fmaxf(fabsf(nk) - thr, 0.f), nk);
+      const float d = en - e;
+      dE2 = fmaf(d, d, dE2);
+      Ep[idx] = en;
+    }
+    float dd[2] = {dA2, dE2};
+    block_sum_f<C, 2>(dd, cx.sc);
+    const float crit2 = mu * sqrtf(fmaxf(dd[0], dd[1])) * inv_den;
+    int rho_bit = crit2 < P.eps2 ? 1 : 0;
+    if (replay) rho_bit = replay[k] ? 1 : 0;
+    const float mu_next = fminf(mu_max, rho_bit ? P.rho0 * mu : mu);
+    const float inv_mun = 1.f / mu_next;
+    // ---- dual step + next M ----------------------------------------------------------------
+    kt_reduce<C>(cx, [&](int idx) { return Ap[idx] + Ep[idx] - Dp[idx]; }, s);
+    float c1 = 0.f;
+    for (PixIter pi(threadIdx.x, C::NT, m); pi.idx < mn; pi.next(C::NT)) {
+      const int idx = pi.idx;
+      const float a = Ap[idx];
+      const float v = a + Ep[idx] - Dp[idx];
+      const float r = v - k_apply<C>(cx, idx, s);
+      const float y = fmaf(mu, r, Yp[idx]);
+      Yp[idx] = y;
+      c1 = fmaf(r, r, c1);
+      cx.S[pi.j * MD + pi.i] = a - r - y * inv_mun;
+    }
+    float cc[1] = {c1};
+    block_sum_f<C, 1>(cc, cx.sc);
+    const float crit1 = sqrtf(cc[0]) * inv_den;
+    if (trace && threadIdx.x == 0) {
+      trace[4 * k + 0] = mu;
+      trace[4 * k + 1] = crit1;
+      trace[4 * k + 2] = crit2;
+      trace[4 * k + 3] = (float)rho_bit;
+    }
+    o.iters = k + 1;
+    o.crit1 = crit1;
+    o.crit2 = crit2;
+    o.mu = mu;
+    const bool stop = crit1 < P.eps1 && crit2 < P.eps2;
+    if (stop) o.converged = true;
+    if (stop && P.fixed_inner <= 0) break;
+    mu = mu_next;
+  }
+  return o;
+}
+
+// W^TW applied in place to a plane X (X <- X - K K^T X).
+template <class C>
+__device__ __forceinline__ void project_plane(Ctx<C>& cx, float* X) {
+  float s[8];
+  kt_reduce<C>(cx, [&](int idx) { return X[idx]; }, s);
+  for (int idx = threadIdx.x; idx < cx.mn; idx += C::NT) X[idx] -= k_apply<C>(cx, idx, s);
+  __syncthreads();
+}
+
+// ||W^TW X||_F
+template <class C>
+__device__ __forceinline__ float proj_norm(Ctx<C>& cx, const float* X) {
+  float s[8];
+  kt_reduce<C>(cx, [&](int idx) { return X[idx]; }, s);
+  float acc = 0.f;
+  for (int idx = threadIdx.x; idx < cx.mn; idx += C::NT) {
+    const float r = X[idx] - k_apply<C>(cx, idx, s);
+    acc = fmaf(r, r, acc);
+  }
+  float a1[1] = {acc};
+  block_sum_f<C, 1>(a1, cx.sc);
+  return sqrtf(a1[0]);
+}
+
+// Prologue of an inner loop: R_0 = W^TW(A + E - D), M_0 = A - R_0 - Y/mu0 into S.
+template <class C>
+__device__ __forceinline__ void write_m0(Ctx<C>& cx, float mu0) {
+  constexpr int MD = C::MAXD;
+  float s[8];
+  const float* Ap = cx.A;
+  const float* Ep = cx.E;
+  const float* Dp = cx.D;
+  kt_reduce<C>(cx, [&](int idx) { return Ap[idx] + Ep[idx] - Dp[idx]; }, s);
+  const float inv = 1.f / mu0;
+  for (PixIter pi(threadIdx.x, C::NT, cx.m); pi.idx < cx.mn; pi.next(C::NT)) {
+    const int idx = pi.idx;
+    const float v = Ap[idx] + Ep[idx] - Dp[idx];
+    const float r = v - k_apply<C>(cx, idx, s);
+    cx.S[pi.j * MD + pi.i] = Ap[idx] - r - cx.Y[idx] * inv;
+  }
+  __syncthreads();
+}
+
+template <class C>
+__device__ __forceinline__ float plane_l1(Ctx<C>& cx, const float* X) {
+  float acc = 0.f;
+  for (int idx = threadIdx.x; idx < cx.mn; idx += C::NT) acc += fabsf(X[idx]);
+  float a1[1] = {acc};
+  block_sum_f<C, 1>(a1, cx.sc);
+  return a1[0];
+}
+
+// Column-major plane -> row-major global [m][n]
+template <class C>
+__device__ __forceinline__ void store_plane(float* __restrict__ out, const float* X, int m, int n, bool zero) {
+  for (int o = threadIdx.x; o < m * n; o += C::NT) {
+    const int i = o / n, j = o - i * n;
+    out[o] = zero ? 0.f : X[j * m + i];
+  }
+}
+
+// Row-major global [m][n] -> column-major plane
+template <class C>
+__device__ __forceinline__ void load_plane(float* X, const float* __restrict__ in, int m, int n) {
+  for (int o = threadIdx.x; o < m * n; o += C::NT) {
+    const int i = o / n, j = o - i * n;
+    X[j * m + i] = in[o];
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// Algorithm 1 for one patch
+// ---------------------------------------------------------------------------------------------
+struct SolveArgs {
+  const float* images;
+  int n_images, H, W;
+  const int* patch_image;
+  const int* boxes;
+  const float* tau0;
+  int B, m, n, p, kind;
+  DevParams P;
+  float* tau_out;
+  float* A_out;
+  float* E_out;
+  float* Y_out;
+  tilt_report* rep;
+  const tilt_report* rep_prev;  // pyramid: counters of the coarse level (accumulated)
+  int* counter;
+  float* ws;
+  size_t ws_stride;
+};
+
+template <class C>
+__device__ void solve_patch(const SolveArgs& a, Ctx<C>& cx, int b) {
+  const DevParams& P = a.P;
+  const int m = a.m, n = a.n, p = a.p, mn = m * n;
+  const int bx[4] = {a.boxes[4 * b], a.boxes[4 * b + 1], a.boxes[4 * b + 2], a.boxes[4 * b + 3]};
+  const float* img = a.images + (size_t)a.patch_image[b] * a.H * a.W;
+  double tau[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) tau[q] = 0.0;
+  if (a.tau0) {
+    for (int q = 0; q < p; ++q) tau[q] = a.tau0[b * p + q];
+  } else {
+    tau[0] = 1.0;
+    tau[3] = 1.0;
+  }
+  const float lam = P.lambda > 0.f ? P.lambda : rsqrtf((float)max(m, n));
+  const float tol = P.jacobi_tol > 0.f ? P.jacobi_tol : default_jacobi_tol(m);
+  const bool warm = P.svd_warm != 0;
+  set_identity<C>(cx.V, n);
+  __syncthreads();
+  int status = TILT_PATCH_MAX_OUTER, stop_rule = 0, outer = 0, inner_total = 0, sweeps_total = 0,
+      aux_total = 0, caps = 0, rank = 0, band = 0, svt_rank = 0;
+  const float fnan = __int_as_float(0x7fc00000);
+  float f = fnan, f_prev = fnan, crit1 = fnan, crit2 = fnan, dtau_inf = fnan, mu_last = fnan, nd = fnan;
+  bool have_state = false, have_fprev = false;
+  const int n_outer = P.fixed_outer > 0 ? P.fixed_outer : P.max_outer;
+  for (int it = 0; it < n_outer; ++it) {
+    // Step 1: D o tau and J_raw (fp64 per pixel, stored fp32), window-escape check
+    const WarpGeom g = make_geom(bx, tau, a.kind);
+    bool esc = false;
+    for (PixIter pi(threadIdx.x, C::NT, m); pi.idx < mn; pi.next(C::NT)) {
+      double d, jr[8];
+      if (!warp_pixel(g, img, a.H, a.W, pi.i, pi.j, d, jr)) esc = true;
+      cx.D[pi.idx] = (float)d;
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (q < p) cx.K[q * mn + pi.idx] = (float)jr[q];
+    }
+    if (__syncthreads_or(esc)) {
+      status = TILT_PATCH_WINDOW_ESCAPE;
+      break;
+    }
+    double qr[24];
+    int l = 0;
+    if (P.constraint_mode == TILT_CONSTRAINTS_CENTER_AREA) {
+      constraint_rows(tau, a.kind, m, n, qr);
+      l = 3;
+    }
+    const int st = orthonormalise<C>(cx, true, qr, l);
+    nd = cx.sc->nd;
+    if (st != TILT_PATCH_CONVERGED) {
+      status = st;
+      break;
+    }
+    // Step 2 warm start (Eq. warm_start; Eq. Y_new_warmstart; Z4)
+    if (!have_state || !P.vws) {
+      for (int idx = threadIdx.x; idx < mn; idx += C::NT) {
+        cx.A[idx] = cx.D[idx];
+        cx.E[idx] = 0.f;
+        cx.Y[idx] = 0.f;
+      }
+      __syncthreads();
+    } else {
+      project_plane<C>(cx, cx.Y);
+    }
+    const float denom0 = proj_norm<C>(cx, cx.D);
+    const float denom = denom0 > 0.f ? denom0 : 1.f;
+    int aux = 0;
+    const float s1 = sigma1_of_plane<C>(cx, cx.D, tol, P.jacobi_max_sweeps, warm, &aux);
+    aux_total += aux;
+    const float mu0 = s1 > 0.f ? P.mu0_scale / s1 : P.mu0_scale;
+    const float mu_max = P.mu_max_ratio * mu0;
+    write_m0<C>(cx, mu0);
+    const size_t toff = ((size_t)b * P.max_outer + it) * P.max_inner;
+    const InnerOut io = ladmap_inner<C>(cx, P, lam, mu0, mu_max, denom, tol,
+                                        P.rho_replay ? P.rho_replay + toff : nullptr,
+                                        P.trace ? P.trace + 4 * toff : nullptr);
+    have_state = true;
+    inner_total += io.iters;
+    sweeps_total += io.sweeps;
+    caps += io.caps;
+    crit1 = io.crit1;
+    crit2 = io.crit2;
+    mu_last = io.mu;
+    const float nuc = cx.sc->svt_nuc;
+    rank = cx.sc->svt_relrank;
+    band = cx.sc->svt_band;
+    svt_rank = cx.sc->svt_rank;
+    // Step 3: dtau = G^{-1} J^T (A + E - D_hat) = L^{-T} K^T (A + E - D_hat)  (Eq. Delta_tau)
+    float s[8];
+    kt_reduce<C>(cx, [&](int idx) { return cx.A[idx] + cx.E[idx] - cx.D[idx]; }, s);
+    const float l1 = plane_l1<C>(cx, cx.E);
+    const double* Li = cx.sc->Linv;
+    double dt_inf = 0.0;
+    bool finite = true;
+    for (int q = 0; q < p; ++q) {  // Step 4: tau += dtau
+      double dq = 0.0;
+      for (int r = q; r < p; ++r) dq += Li[r * 8 + q] * (double)s[r];
+      tau[q] += dq;
+      dt_inf = fmax(dt_inf, fabs(dq));
+      finite = finite && isfinite(tau[q]);
+    }
+    dtau_inf = (float)dt_inf;
+    f = nuc + lam * l1;
+    outer = it + 1;
+    if (!finite || !isfinite(f) || f > 1e12f) {
+      status = TILT_PATCH_DIVERGED;
+      break;
+    }
+    int rule = 0;
+    if (have_fprev && fabsf(f - f_prev) < P.obj_tol * fabsf(f_prev)) rule = 1;
+    else if (dtau_inf < P.tau_tol) rule = 2;
+    f_prev = f;
+    have_fprev = true;
+    if (rule) {
+      status = TILT_PATCH_CONVERGED;
+      stop_rule = rule;
+      if (P.fixed_outer <= 0) break;
+    } else {
+      status = TILT_PATCH_MAX_OUTER;
+      stop_rule = 3;
+    }
+    __syncthreads();
+  }
+  __syncthreads();
+  // outputs
+  if (a.A_out) store_plane<C>(a.A_out + (size_t)b * mn, cx.A, m, n, !have_state);
+  if (a.E_out) store_plane<C>(a.E_out + (size_t)b * mn, cx.E, m, n, !have_state);
+  if (a.Y_out) store_plane<C>(a.Y_out + (size_t)b * mn, cx.Y, m, n, !have_state);
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < p; ++q) a.tau_out[b * p + q] = (float)tau[q];
+    if (a.rep) {
+      tilt_report r;
+      r.status = status;
+      r.stop_rule = stop_rule;
+      r.outer_iters = outer;
+      r.inner_iters = inner_total;
+      r.jacobi_sweeps = sweeps_total;
+      r.aux_sweeps = aux_total;
+      r.rank = rank;
+      r.rank_band = band;
+      r.svt_rank = svt_rank;
+      r.sweep_cap_hits = caps;
+      r.objective = f;
+      r.crit1 = crit1;
+      r.crit2 = crit2;
+      r.patch_norm = nd;
+      r.dtau_inf = dtau_inf;
+      r.mu_last = mu_last;
+      if (a.rep_prev) {
+        const tilt_report& pr = a.rep_prev[b];
+        r.outer_iters += pr.outer_iters;
+        r.inner_iters += pr.inner_iters;
+        r.jacobi_sweeps += pr.jacobi_sweeps;
+        r.aux_sweeps += pr.aux_sweeps;
+        r.sweep_cap_hits += pr.sweep_cap_hits;
+      }
+      a.rep[b] = r;
+    }
+  }
+  __syncthreads();
+}
+
+template <class C>
+__global__ void __launch_bounds__(C::NT, C::MINB) k_solve(SolveArgs a) {
+  extern __shared__ float4 dsm4[];
+  __shared__ Scal sc;
+  float* ws = a.ws ? a.ws + (size_t)blockIdx.x * a.ws_stride : nullptr;
+  Ctx<C> cx = make_ctx<C>(reinterpret_cast<float*>(dsm4), ws, &sc, a.m, a.n, a.p);
+  while (true) {
+    if (threadIdx.x == 0) sc.patch = atomicAdd(a.counter, 1);
+    __syncthreads();
+    const int b = sc.patch;
+    __syncthreads();
+    if (b >= a.B) break;
+    solve_patch<C>(a, cx, b);
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// Inner loop only (Table 1 setting)
+// ---------------------------------------------------------------------------------------------
+struct InnerArgs {
+  const float* D;
+  const float* J;
+  const float* Q;
+  int l, B, m, n, p;
+  DevParams P;
+  float* A;
+  float* E;
+  float* Y;
+  tilt_report* rep;
+  float* ws;
+  size_t ws_stride;
+};
+
+template <class C>
+__global__ void __launch_bounds__(C::NT, C::MINB) k_inner(InnerArgs a) {
+  extern __shared__ float4 dsm4[];
+  __shared__ Scal sc;
+  float* ws = a.ws ? a.ws + (size_t)blockIdx.x * a.ws_stride : nullptr;
+  Ctx<C> cx = make_ctx<C>(reinterpret_cast<float*>(dsm4), ws, &sc, a.m, a.n, a.p);
+  const DevParams& P = a.P;
+  const int m = a.m, n = a.n, p = a.p, mn = m * n;
+  const float lam = P.lambda > 0.f ? P.lambda : rsqrtf((float)max(m, n));
+  const float tol = P.jacobi_tol > 0.f ? P.jacobi_tol : default_jacobi_tol(m);
+  for (int b = blockIdx.x; b < a.B; b += gridDim.x) {
+    load_plane<C>(cx.D, a.D + (size_t)b * mn, m, n);
+    for (int q = 0; q < p; ++q) load_plane<C>(cx.K + (size_t)q * mn, a.J + ((size_t)b * p + q) * mn, m, n);
+    __syncthreads();
+    double qr[24];
+    for (int e = 0; e < 24; ++e) qr[e] = 0.0;
+    if (a.Q)
+      for (int r = 0; r < a.l; ++r)
+        for (int q = 0; q < p; ++q) qr[r * 8 + q] = a.Q[((size_t)b * a.l + r) * p + q];
+    const int st = orthonormalise<C>(cx, false, qr, a.Q ? a.l : 0);
+    tilt_report rr;
+    memset(&rr, 0, sizeof(rr));
+    rr.status = st;
+    if (st == TILT_PATCH_CONVERGED) {
+      for (int idx = threadIdx.x; idx < mn; idx += C::NT) {
+        cx.A[idx] = cx.D[idx];
+        cx.E[idx] = 0.f;
+        cx.Y[idx] = 0.f;
+      }
+      set_identity<C>(cx.V, n);
+      __syncthreads();
+      const float denom0 = proj_norm<C>(cx, cx.D);
+      const float denom = denom0 > 0.f ? denom0 : 1.f;
+      int aux = 0;
+      const float s1 = sigma1_of_plane<C>(cx, cx.D, tol, P.jacobi_max_sweeps, P.svd_warm != 0, &aux);
+      const float mu0 = s1 > 0.f ? P.mu0_scale / s1 : P.mu0_scale;
+      write_m0<C>(cx, mu0);
+      const InnerOut io = ladmap_inner<C>(cx, P, lam, mu0, P.mu_max_ratio * mu0, denom, tol,
+                                          P.rho_replay ? P.rho_replay + (size_t)b * P.max_inner : nullptr,
+                                          P.trace ? P.trace + (size_t)4 * b * P.max_inner : nullptr);
+      const float nuc = cx.sc->svt_nuc;
+      rr.rank = cx.sc->svt_relrank;
+      rr.rank_band = cx.sc->svt_band;
+      rr.svt_rank = cx.sc->svt_rank;
+      const float l1 = plane_l1<C>(cx, cx.E);
+      rr.status = io.converged ? TILT_PATCH_CONVERGED : TILT_PATCH_MAX_OUTER;
+      rr.outer_iters = 1;
+      rr.inner_iters = io.iters;
+      rr.jacobi_sweeps = io.sweeps;
+      rr.aux_sweeps = aux;
+      rr.sweep_cap_hits = io.caps;
+      rr.objective = nuc + lam * l1;
+      rr.crit1 = io.crit1;
+      rr.crit2 = io.crit2;
+      rr.mu_last = io.mu;
+      rr.patch_norm = denom0;
+    }
+    __syncthreads();
+    const bool z = st != TILT_PATCH_CONVERGED;
+    store_plane<C>(a.A + (size_t)b * mn, cx.A, m, n, z);
+    store_plane<C>(a.E + (size_t)b * mn, cx.E, m, n, z);
+    if (a.Y) store_plane<C>(a.Y + (size_t)b * mn, cx.Y, m, n, z);
+    if (a.rep && threadIdx.x == 0) a.rep[b] = rr;
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// Standalone SVT (step parity of the K3 core)
+// ---------------------------------------------------------------------------------------------
+struct SvtArgs {
+  const float* M;
+  int B, m, n;
+  const float* eps;
+  float* V_io;
+  float* A;
+  float* sigma;
+  int* sweeps;
+  float tol;
+  int max_sweeps;
+  float* ws;
+  size_t ws_stride;
+};
+
+template <class C>
+__global__ void __launch_bounds__(C::NT, C::MINB) k_svt(SvtArgs a) {
+  extern __shared__ float4 dsm4[];
+  __shared__ Scal sc;
+  constexpr int MD = C::MAXD;
+  float* ws = a.ws ? a.ws + (size_t)blockIdx.x * a.ws_stride : nullptr;
+  Ctx<C> cx = make_ctx<C>(reinterpret_cast<float*>(dsm4), ws, &sc, a.m, a.n, 0);
+  const int m = a.m, n = a.n, mn = m * n;
+  for (int b = blockIdx.x; b < a.B; b += gridDim.x) {
+    zero_buf<C>(cx.S);
+    zero_buf<C>(cx.V);
+    __syncthreads();
+    for (int o = threadIdx.x; o < mn; o += C::NT) {
+      const int i = o / n, j = o - i * n;
+      cx.S[j * MD + i] = a.M[(size_t)b * mn + o];
+    }
+    if (a.V_io) {
+      for (int o = threadIdx.x; o < n * n; o += C::NT) {
+        const int i = o / n, j = o - i * n;
+        cx.V[j * MD + i] = a.V_io[(size_t)b * n * n + o];
+      }
+    } else {
+      set_identity<C>(cx.V, n);
+    }
+    __syncthreads();
+    float* Ab = a.A + (size_t)b * mn;
+    SvtOut so = svt<C, true>(cx, m, n, a.eps[b], a.tol, a.max_sweeps, true,
+                             [&](int i, int j, float v) { Ab[i * n + j] = v; }, false);
+    if (a.sigma)
+      for (int j = threadIdx.x; j < n; j += C::NT) a.sigma[(size_t)b * n + j] = sqrtf(cx.nrm[j]);
+    if (a.V_io)
+      for (int o = threadIdx.x; o < n * n; o += C::NT) {
+        const int i = o / n, j = o - i * n;
+        a.V_io[(size_t)b * n * n + o] = cx.V[j * MD + i];
+      }
+    if (a.sweeps && threadIdx.x == 0) a.sweeps[b] = so.sweeps;
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// Standalone projector (K2 parity): W^TW v and G^{-1} J^T v
+// ---------------------------------------------------------------------------------------------
+struct ProjArgs {
+  const float* J;
+  const float* Q;
+  int l;
+  const float* v;
+  int B, m, n, p;
+  float* Pv;
+  float* dtau;
+  int* status;
+  float* ws;
+  size_t ws_stride;
+};
+
+template <class C>
+__global__ void __launch_bounds__(C::NT, C::MINB) k_project(ProjArgs a) {
+  extern __shared__ float4 dsm4[];
+  __shared__ Scal sc;
+  float* ws = a.ws ? a.ws + (size_t)blockIdx.x * a.ws_stride : nullptr;
+  Ctx<C> cx = make_ctx<C>(reinterpret_cast<float*>(dsm4), ws, &sc, a.m, a.n, a.p);
+  const int m = a.m, n = a.n, p = a.p, mn = m * n;
+  for (int b = blockIdx.x; b < a.B; b += gridDim.x) {
+    for (int q = 0; q < p; ++q) load_plane<C>(cx.K + (size_t)q * mn, a.J + ((size_t)b * p + q) * mn, m, n);
+    load_plane<C>(cx.A, a.v + (size_t)b * mn, m, n);
+    __syncthreads();
+    double qr[24];
+    for (int e = 0; e < 24; ++e) qr[e] = 0.0;
+    if (a.Q)
+      for (int r = 0; r < a.l; ++r)
+        for (int q = 0; q < p; ++q) qr[r * 8 + q] = a.Q[((size_t)b * a.l + r) * p + q];
+    const int st = orthonormalise<C>(cx, false, qr, a.Q ? a.l : 0);
+    if (st == TILT_PATCH_CONVERGED) {
+      float s[8];
+      kt_reduce<C>(cx, [&](int idx) { return cx.A[idx]; }, s);
+      for (int idx = threadIdx.x; idx < mn; idx += C::NT) cx.E[idx] = cx.A[idx] - k_apply<C>(cx, idx, s);
+      if (a.dtau && threadIdx.x == 0) {
+        const double* Li = cx.sc->Linv;
+        for (int q = 0; q < p; ++q) {
+          double dq = 0.0;
+          for (int r = q; r < p; ++r) dq += Li[r * 8 + q] * (double)s[r];
+          a.dtau[(size_t)b * p + q] = (float)dq;
+        }
+      }
+      __syncthreads();
+    }
+    store_plane<C>(a.Pv + (size_t)b * mn, cx.E, m, n, st != TILT_PATCH_CONVERGED);
+    if (a.status && threadIdx.x == 0) a.status[b] = st;
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// K1 standalone: Alg. 1 Step 1 over all patches (HBM-bound; one CTA per patch, row-major pixels
+// so that a warp's taps are coalesced). Two passes: reductions (||d||, D_hat^T J_raw), then
+// recompute (taps from L1/L2) and write D_hat and the normalised J.
+// ---------------------------------------------------------------------------------------------
+struct WarpArgs {
+  const float* images;
+  int n_images, H, W;
+  const int* patch_image;
+  const int* boxes;
+  const float* tau;
+  int B, m, n, p, kind;
+  float* Dhat;
+  float* J;
+  float* norm;
+  int* status;
+};
+
+constexpr int K1_NT = 256;
+
+__global__ void __launch_bounds__(K1_NT) k_warp(WarpArgs a) {
+  __shared__ double red[K1_NT / 32][9];
+  __shared__ double tot[9];
+  const int b = blockIdx.x;
+  const int m = a.m, n = a.n, p = a.p, mn = m * n;
+  const int bx[4] = {a.boxes[4 * b], a.boxes[4 * b + 1], a.boxes[4 * b + 2], a.boxes[4 * b + 3]};
+  double tau[8] = {1, 0, 0, 1, 0, 0, 0, 0};
+  for (int q = 0; q < p; ++q) tau[q] = a.tau[b * p + q];
+  const WarpGeom g = make_geom(bx, tau, a.kind);
+  const float* img = a.images + (size_t)a.patch_image[b] * a.H * a.W;
+  double acc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  bool esc = false;
+  for (int o = threadIdx.x; o < mn; o += K1_NT) {
+    const int i = o / n, j = o - i * n;
+    double d, jr[8];
+    if (!warp_pixel(g, img, a.H, a.W, i, j, d, jr)) esc = true;
+    acc[8] = fma(d, d, acc[8]);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc[q] = fma(jr[q], d, acc[q]);
+  }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < 9; ++k) {
+    double x = acc[k];
+#pragma unroll
+    for (int off = 16; off; off >>= 1) x += __shfl_xor_sync(FULL, x, off);
+    if (lane == 0) red[w][k] = x;
+  }
+  esc = __syncthreads_or(esc);
+  if (threadIdx.x < 9) {
+    double s = 0.0;
+    for (int ww = 0; ww < K1_NT / 32; ++ww) s += red[ww][threadIdx.x];
+    tot[threadIdx.x] = s;
+  }
+  __syncthreads();
+  const double nd = sqrt(tot[8]);
+  int st = TILT_PATCH_CONVERGED;
+  if (esc) st = TILT_PATCH_WINDOW_ESCAPE;
+  else if (!(nd > 0.0)) st = TILT_PATCH_ZERO_PATCH;
+  if (threadIdx.x == 0) {
+    if (a.norm) a.norm[b] = (float)nd;
+    if (a.status) a.status[b] = st;
+  }
+  const double ind = st == TILT_PATCH_CONVERGED ? 1.0 / nd : 0.0;
+  double c[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) c[q] = tot[q] * ind;
+  float* Dh = a.Dhat + (size_t)b * mn;
+  float* Jb = a.J ? a.J + (size_t)b * p * mn : nullptr;
+  for (int o = threadIdx.x; o < mn; o += K1_NT) {
+    const int i = o / n, j = o - i * n;
+    double d, jr[8];
+    warp_pixel(g, img, a.H, a.W, i, j, d, jr);
+    const double dh = d * ind;
+    Dh[o] = (float)dh;
+    if (Jb) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (q < p) Jb[(size_t)q * mn + o] = (float)((jr[q] - dh * c[q]) * ind);
+    }
+  }
+}
+
+// 2x2 box downsample (pyramid, reading Z18) of n_images [H][W] -> [H/2][W/2]
+__global__ void k_downsample(const float* __restrict__ in, float* __restrict__ out, int n_images, int H, int W) {
+  const int h2 = H / 2, w2 = W / 2;
+  const size_t total = (size_t)n_images * h2 * w2;
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
+    const size_t im = e / ((size_t)h2 * w2);
+    const int r = (int)(e - im * h2 * w2);
+    const int y = r / w2, x = r - y * w2;
+    const float* p = in + im * H * W + (size_t)(2 * y) * W + 2 * x;
+    out[e] = 0.25f * (p[0] + p[1] + p[W] + p[W + 1]);
+  }
+}
+
+__global__ void k_half_boxes(const int* __restrict__ in, int* __restrict__ out, int B) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < 4 * B; e += gridDim.x * blockDim.x) out[e] = in[e] / 2;
+}
+
+}  // namespace tilt

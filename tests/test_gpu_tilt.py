@@ -1,0 +1,199 @@
+"""End-to-end GPU parity of tilt_solve_batch (the hot entry) against the fp64 oracle.
+
+Protocol:
+* fixed count: one outer iteration with exactly K inner iterations and the oracle's rho decisions
+  replayed: A and E within 1e-4 relative Frobenius (BASELINE.json north_star);
+* convergence: the oracle runs free; the GPU replays its outer-iteration count; tau within 1e-3
+  max-abs (normalised coordinates), rank of A equal (outside the Z19 band), objective within 1e-3;
+* full size: config 2's 1024-patch batch in the bench launch configuration, sampled patches vs
+  the oracle plus properties that hold for every patch;
+* edge cases: empty batch, ragged/odd sizes, m != n, failures (escape, zero patch, singular Gram),
+  sharding determinism, the 2-level pyramid.
+"""
+import dataclasses
+
+import numpy as np
+import pytest
+
+import oracle as O
+import tilt_synth as ts
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def T():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import __graft_entry__ as g
+    g.build()
+    import paper_1205_5351_b200 as T
+    return T
+
+
+@pytest.fixture(scope="module")
+def solver(T):
+    s = T.TiltSolver(0, max_batch=1024, max_m=128, max_n=128, max_p=8, max_image_elems=64 * 200 * 200)
+    yield s
+    s.close()
+
+
+def _replay_tensor(traces_per_patch, max_outer, max_inner):
+    import torch
+    B = len(traces_per_patch)
+    arr = np.zeros((B, max_outer, max_inner), np.uint8)
+    for b, trs in enumerate(traces_per_patch):
+        for it, tr in enumerate(trs):
+            arr[b, it, :len(tr)] = [t[3] for t in tr]
+    return torch.as_tensor(arr, device="cuda")
+
+
+@pytest.mark.parametrize("cfg_id,K", [(1, 20), (1, 50), (2, 20), (2, 50)])
+def test_fixed_count_parity(solver, T, cfg_id, K):
+    cfg = ts.CONFIGS[cfg_id]
+    B = 4
+    b = ts.gen_batch(cfg, 0, B)
+    prm_o = O.Params(fixed_inner_iters=K, fixed_outer_iters=1, max_inner=K, max_outer=1)
+    refs = [O.tilt(b["images"][k], b["boxes"][k], b["tau0"][k], cfg.kind, prm_o) for k in range(B)]
+    rr = _replay_tensor([r["traces"] for r in refs], 1, K)
+    prm = T.default_params(fixed_inner_iters=K, fixed_outer_iters=1, max_inner=K, max_outer=1)
+    prm.rho_replay = rr.data_ptr()
+    out = solver.solve(b["images"], b["patch_image"], b["boxes"], b["tau0"], cfg.kind, prm, want_Y=True)
+    rep = T.reports_to_numpy(out["rep"])
+    for k in range(B):
+        a = out["A"][k].double().cpu().numpy()
+        e = out["E"][k].double().cpu().numpy()
+        ra = np.linalg.norm(a - refs[k]["A"]) / np.linalg.norm(refs[k]["A"])
+        re = np.linalg.norm(e - refs[k]["E"]) / np.linalg.norm(refs[k]["E"])
+        assert ra < 1e-4 and re < 1e-4, (cfg_id, K, k, ra, re)
+        tau = out["tau"][k].double().cpu().numpy()
+        assert np.max(np.abs(tau - refs[k]["tau"])) < 1e-3
+        assert rep["inner_iters"][k] == K and rep["outer_iters"][k] == 1
+
+
+def _convergence_case(solver, T, cfg, idx_list, **gen):
+    b = ts.gen_batch(cfg, idx_list[0], len(idx_list), **gen)
+    refs = [O.tilt(b["images"][k], b["boxes"][k], b["tau0"][k], cfg.kind) for k in range(len(idx_list))]
+    results = []
+    for k, r in enumerate(refs):
+        prm = T.default_params(fixed_outer_iters=max(1, r["outer_iters"]))
+        out = solver.solve(b["images"][k:k + 1], [0], b["boxes"][k:k + 1], b["tau0"][k:k + 1], cfg.kind, prm)
+        rep = T.reports_to_numpy(out["rep"])[0]
+        tau = out["tau"][0].double().cpu().numpy()
+        results.append((r, rep, tau))
+    return results
+
+
+@pytest.mark.parametrize("cfg_id", [1])
+def test_convergence_parity(solver, T, cfg_id):
+    cfg = ts.CONFIGS[cfg_id]
+    res = _convergence_case(solver, T, cfg, list(range(8)))
+    bad = []
+    for k, (r, rep, tau) in enumerate(res):
+        dt = np.max(np.abs(tau - r["tau"]))
+        dobj = abs(rep["objective"] - r["objective"]) / r["objective"]
+        rank_ok = (rep["rank"] == r["rank"]) or r["rank_band"] or rep["rank_band"]
+        if not (dt < 1e-3 and dobj < 1e-3 and rank_ok):
+            bad.append((k, dt, dobj, int(rep["rank"]), r["rank"], r["outer_iters"], r["stop_rule"]))
+    # reading Z22: a patch near a bifurcation of the nonconvex outer loop may split; allow 1 of 8
+    assert len(bad) <= 1, bad
+
+
+def test_full_size_config2(solver, T):
+    """Config 2 (1024 x 50x50 homography) in the bench launch configuration."""
+    cfg = ts.CONFIGS[2]
+    b = ts.gen_batch(cfg, 0, cfg.batch)
+    out = solver.solve(b["images"], b["patch_image"], b["boxes"], b["tau0"], cfg.kind)
+    rep = T.reports_to_numpy(out["rep"])
+    tau = out["tau"].double().cpu().numpy()
+    assert np.all(np.isfinite(tau))
+    assert set(np.unique(rep["status"])) <= {T.CONVERGED, T.MAX_OUTER, T.WINDOW_ESCAPE}
+    conv = rep["status"] == T.CONVERGED
+    assert conv.mean() > 0.5
+    ok = rep["status"] <= T.MAX_OUTER
+    assert np.all(rep["outer_iters"][ok] >= 1) and np.all(rep["inner_iters"][ok] >= rep["outer_iters"][ok])
+    assert np.all(np.abs(rep["patch_norm"][ok]) > 0)
+    # determinism: the same batch solved again gives identical bits (persistent queue order-free)
+    out2 = solver.solve(b["images"], b["patch_image"], b["boxes"], b["tau0"], cfg.kind)
+    assert np.array_equal(out2["tau"].cpu().numpy(), out["tau"].cpu().numpy())
+    assert np.array_equal(out2["A"].cpu().numpy(), out["A"].cpu().numpy())
+    # sampled patches vs the oracle (outer count replayed)
+    for k in (0, 517):
+        r = O.tilt(b["images"][k], b["boxes"][k], b["tau0"][k], cfg.kind)
+        prm = T.default_params(fixed_outer_iters=max(1, r["outer_iters"]))
+        o1 = solver.solve(b["images"][k:k + 1], [0], b["boxes"][k:k + 1], b["tau0"][k:k + 1], cfg.kind, prm)
+        t1 = o1["tau"][0].double().cpu().numpy()
+        assert np.max(np.abs(t1 - r["tau"])) < 1e-3 or r["stop_rule"] == O.STOP_MAX_OUTER, (k, t1, r["tau"])
+
+
+def test_sharding_bit_identical(solver, T):
+    cfg = ts.CONFIGS[1]
+    b = ts.gen_batch(cfg, 0, 6)
+    prm = T.default_params(max_outer=5)
+    full = solver.solve(b["images"], b["patch_image"], b["boxes"], b["tau0"], cfg.kind, prm)
+    for sl in (slice(0, 2), slice(2, 6)):
+        part = solver.solve(b["images"], b["patch_image"][sl], b["boxes"][sl], b["tau0"][sl], cfg.kind,
+                            T.default_params(max_outer=5))
+        assert np.array_equal(part["tau"].cpu().numpy(), full["tau"][sl].cpu().numpy())
+        assert np.array_equal(part["E"].cpu().numpy(), full["E"][sl].cpu().numpy())
+
+
+def test_edge_cases(solver, T):
+    import torch
+    cfg = ts.CONFIGS[1]
+    # empty batch is a no-op
+    b = ts.gen_batch(cfg, 0, 3)
+    out = solver.solve(b["images"], b["patch_image"][:0], b["boxes"][:0], b["tau0"][:0], cfg.kind,
+                       T.default_params(win_h=32, win_w=32))
+    assert out["tau"].shape == (0, 6)
+    # failure statuses never abort the batch
+    imgs = b["images"].copy()
+    imgs[1] = 0.0                        # zero patch
+    imgs[2] = 0.5                        # constant image: J = 0, Gram singular
+    tau0 = b["tau0"].copy()
+    tau0[0, 4] = 1.5                     # window escapes the canvas
+    out = solver.solve(imgs, b["patch_image"], b["boxes"], tau0, cfg.kind, T.default_params(max_outer=3))
+    rep = T.reports_to_numpy(out["rep"])
+    assert rep["status"].tolist() == [T.WINDOW_ESCAPE, T.ZERO_PATCH, T.SINGULAR_GRAM]
+    np.testing.assert_allclose(out["tau"][0].cpu().numpy(), tau0[0], atol=0)
+    # bad arguments
+    with pytest.raises(T.TiltError):
+        solver.solve(b["images"], b["patch_image"], b["boxes"], b["tau0"], cfg.kind,
+                     T.default_params(rho0=0.5))
+    del torch
+
+
+@pytest.mark.parametrize("m,n,kind", [(33, 33, O.AFFINE), (40, 56, O.HOMOGRAPHY), (63, 45, O.AFFINE)])
+def test_ragged_sizes_fixed_count(solver, T, m, n, kind):
+    cfg = dataclasses.replace(ts.CONFIGS[1], m=m, n=n, kind=kind, config_id=950 + m)
+    B, K = 2, 20
+    b = ts.gen_batch(cfg, 0, B)
+    prm_o = O.Params(fixed_inner_iters=K, fixed_outer_iters=2, max_inner=K, max_outer=2)
+    refs = [O.tilt(b["images"][k], b["boxes"][k], b["tau0"][k], kind, prm_o) for k in range(B)]
+    rr = _replay_tensor([r["traces"] for r in refs], 2, K)
+    prm = T.default_params(fixed_inner_iters=K, fixed_outer_iters=2, max_inner=K, max_outer=2)
+    prm.rho_replay = rr.data_ptr()
+    out = solver.solve(b["images"], b["patch_image"], b["boxes"], b["tau0"], kind, prm)
+    for k in range(B):
+        a = out["A"][k].double().cpu().numpy()
+        ra = np.linalg.norm(a - refs[k]["A"]) / np.linalg.norm(refs[k]["A"])
+        assert ra < 1e-3, (m, n, k, ra)  # two outer iterations: the Y~ warm start carries fp32 noise
+        assert np.max(np.abs(out["tau"][k].double().cpu().numpy() - refs[k]["tau"])) < 1e-3
+
+
+def test_pyramid_config3_small(solver, T):
+    cfg = ts.CONFIGS[3]
+    B, K = 2, 20
+    b = ts.gen_batch(cfg, 0, B)
+    prm_o = O.Params(fixed_inner_iters=K, fixed_outer_iters=2, max_inner=K, max_outer=2)
+    refs = [O.tilt_pyramid(b["images"][k], b["boxes"][k], b["tau0"][k], cfg.kind, prm_o, levels=2)
+            for k in range(B)]
+    prm = T.default_params(fixed_inner_iters=K, fixed_outer_iters=2, max_inner=K, max_outer=2, pyramid_levels=2)
+    out = solver.solve(b["images"], b["patch_image"], b["boxes"], b["tau0"], cfg.kind, prm)
+    rep = T.reports_to_numpy(out["rep"])
+    for k in range(B):
+        assert np.max(np.abs(out["tau"][k].double().cpu().numpy() - refs[k]["tau"])) < 1e-3
+        a = out["A"][k].double().cpu().numpy()
+        assert np.linalg.norm(a - refs[k]["A"]) / np.linalg.norm(refs[k]["A"]) < 1e-3
+        assert rep["outer_iters"][k] == 4 and rep["inner_iters"][k] == 4 * K
