@@ -172,7 +172,7 @@ template <class C>
 __device__ __forceinline__ void gemm_nn(float* __restrict__ Cm, const float* __restrict__ Lm,
                                         const float* __restrict__ Rm, int rows_valid, int inner, int cols) {
   constexpr int MD = C::MAXD;
-  const int rt = (rows_valid + 3) >> 2;
+  constexpr int rt = MD / 4;  // every row group of the padded column is written (zeros below rows_valid)
   const int ct = (cols + 1) >> 1;
   const int ntiles = rt * ct;
   for (int tile = threadIdx.x; tile < ntiles; tile += C::NT) {
@@ -184,8 +184,9 @@ __device__ __forceinline__ void gemm_nn(float* __restrict__ Cm, const float* __r
     const float* lp = Lm + i0;
     const float* r0 = Rm + j0 * MD;
     const float* r1 = r0 + MD;
+    const int kend = i0 < rows_valid ? inner : 0;
 #pragma unroll 4
-    for (int k = 0; k < inner; ++k) {
+    for (int k = 0; k < kend; ++k) {
       const float4 a = *reinterpret_cast<const float4*>(lp + k * MD);
       const float b0 = r0[k], b1 = r1[k];
       acc[0] = fmaf(a.x, b0, acc[0]);
@@ -340,32 +341,50 @@ __device__ __forceinline__ void col_pass(Ctx<C>& cx, int n, float eps) {
     }
 #pragma unroll
     for (int off = L / 2; off; off >>= 1) ss += __shfl_xor_sync(FULL, ss, off);
+    float y[RPL];
+    float vv = 1.f;
+    if (MODE != 0) {
+      if constexpr (RPL >= 4) {
+#pragma unroll
+        for (int r = 0; r < RPL; r += 4) {
+          const float4 t = *reinterpret_cast<const float4*>(vp + r);
+          y[r] = t.x * s; y[r + 1] = t.y * s; y[r + 2] = t.z * s; y[r + 3] = t.w * s;
+        }
+      } else {
+        const float2 t = *reinterpret_cast<const float2*>(vp);
+        y[0] = t.x * s; y[1] = t.y * s;
+      }
+    }
+    if (MODE == 2) {
+      // rotations are orthogonal only to fp32 rounding, which drifts the column norms of V by a
+      // few 1e-6 per SVT: B = M V holds for the drifted V, so sigma_j = ||b_j|| / ||v_j|| and
+      // A = sum_j h_j b_j v_j^T / ||v_j||^2 remove that scale exactly.
+      vv = 0.f;
+#pragma unroll
+      for (int r = 0; r < RPL; ++r) vv = fmaf(y[r], y[r], vv);
+#pragma unroll
+      for (int off = L / 2; off; off >>= 1) vv += __shfl_xor_sync(FULL, vv, off);
+      ss = vv > 0.f ? ss / vv : 0.f;
+    }
     float h = 1.f;
     if (MODE == 2) {
       const float sg = sqrtf(ss);
       h = (sg > eps) ? (sg - eps) / sg : 0.f;
     }
     if (valid && MODE != 0) {
+      const float hb = (MODE == 2) ? (vv > 0.f ? h / vv : 0.f) : 1.f;
 #pragma unroll
-      for (int r = 0; r < RPL; ++r) x[r] *= (MODE == 2 ? h : 1.f);
-      // B columns are stored pre-multiplied by h in MODE 2 (ready for A = B' V^T)
-      if constexpr (RPL >= 4) {
-#pragma unroll
-        for (int r = 0; r < RPL; r += 4) *reinterpret_cast<float4*>(bp + r) = make_float4(x[r], x[r + 1], x[r + 2], x[r + 3]);
-      } else {
-        *reinterpret_cast<float2*>(bp) = make_float2(x[0], x[1]);
-      }
-      float y[RPL];
+      for (int r = 0; r < RPL; ++r) x[r] *= hb;
+      // B columns are stored pre-multiplied by h/||v||^2 in MODE 2 (ready for A = B' V^T)
       if constexpr (RPL >= 4) {
 #pragma unroll
         for (int r = 0; r < RPL; r += 4) {
-          float4 t = *reinterpret_cast<float4*>(vp + r);
-          y[r] = t.x * s; y[r + 1] = t.y * s; y[r + 2] = t.z * s; y[r + 3] = t.w * s;
+          *reinterpret_cast<float4*>(bp + r) = make_float4(x[r], x[r + 1], x[r + 2], x[r + 3]);
           *reinterpret_cast<float4*>(vp + r) = make_float4(y[r], y[r + 1], y[r + 2], y[r + 3]);
         }
       } else {
-        float2 t = *reinterpret_cast<float2*>(vp);
-        *reinterpret_cast<float2*>(vp) = make_float2(t.x * s, t.y * s);
+        *reinterpret_cast<float2*>(bp) = make_float2(x[0], x[1]);
+        *reinterpret_cast<float2*>(vp) = make_float2(y[0], y[1]);
       }
     }
     if (valid && lu == 0) {

@@ -85,6 +85,7 @@ __device__ float sigma1_of_plane(Ctx<C>& cx, const float* X, float tol, int max_
   gemm_nn<C>(cx.B, cx.S, cx.V, m, n, n);
   bool capped;
   *sweeps = jacobi_sweeps<C>(cx, n, tol, max_sweeps, &capped);
+  col_pass<C, 2>(cx, n, 0.f);  // sigma_j = ||b_j|| / ||v_j||
   svt_stats<C>(cx, n, 0.f);
   __syncthreads();
   const float s1 = cx.sc->svt_sig1;

@@ -84,7 +84,7 @@ def test_svt_parity(solver, m, n):
         err = np.linalg.norm(A[k] - ref) / np.linalg.norm(Ms[k])
         assert err < 3e-5, (m, n, k, err)
         gs = np.sort(out["sigma"][k].double().cpu().numpy())[::-1][:min(m, n)]
-        np.testing.assert_allclose(gs, s[:min(m, n)], atol=2e-6 * s[0])
+        np.testing.assert_allclose(gs, s[:min(m, n)], atol=1e-5 * s[0])
     assert int(out["sweeps"].max()) < 20
 
 
