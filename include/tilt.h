@@ -89,7 +89,8 @@ typedef struct {
   /* test-only controls (0 / NULL in production) */
   int32_t fixed_inner_iters;  /* > 0: exactly this many inner iterations (no early stop) */
   int32_t fixed_outer_iters;  /* > 0: exactly this many outer iterations */
-  const uint8_t* rho_replay;  /* device [B][max_outer][max_inner] 0/1 rho decisions or NULL (Z21) */
+  const uint8_t* rho_replay;  /* device [B][max_outer][max_inner] or NULL (Z21): bit 0 = rho decision
+                                 (1: rho0), bit 1 = end the inner loop after this iteration */
   float* trace;               /* device [B][max_outer][max_inner][4] (mu, crit1, crit2, rho) or NULL */
   /* window size of the call (all boxes share it). 0: read back from boxes[0] with a stream sync;
    * > 0: taken as given (no host sync; the call is then graph-capturable). */

@@ -115,9 +115,18 @@ bool params_ok(const tilt_params* p) {
   return true;
 }
 
+// Per-call geometry: leading dimension (ld_of), columns, extra planes of the projector
+struct Geo {
+  int ld, n, gplanes;
+};
+
+template <class C>
+inline Geo geo_of(int m, int n, int gplanes) { return Geo{ld_of<C>(m, n), n, gplanes}; }
+
 template <class C>
 struct Launch {
-  static size_t smem(int mn, int p) { return Layout<C>::smem_bytes(mn, p); }
+  static size_t smem(Geo g) { return Layout<C>::smem_bytes(g.ld, g.n, g.gplanes); }
+  static size_t wsf(Geo g) { return Layout<C>::ws_floats(g.ld, g.n, g.gplanes); }
 
   static tilt_status prep(const void* fn, size_t sm) {
     if (sm > 48 * 1024) TILT_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
@@ -125,7 +134,8 @@ struct Launch {
   }
 
   // grid size (persistent): num_sms * occupancy, capped by B and by the workspace slots
-  static tilt_status grid(tilt_handle* h, const void* fn, size_t sm, int B, int mn, int p, int* g) {
+  static tilt_status grid(tilt_handle* h, const void* fn, Geo geo, int B, int* g) {
+    const size_t sm = smem(geo);
     tilt_status s = prep(fn, sm);
     if (s != TILT_OK) return s;
     const int occ = occupancy_for<C>(fn, sm);
@@ -135,9 +145,9 @@ struct Launch {
     }
     int gsz = h->num_sms * occ;
     if (gsz > B) gsz = B;
-    const size_t wsf = Layout<C>::ws_floats(mn, p);
-    if (wsf > 0) {
-      const size_t slots = h->ws_floats / wsf;
+    const size_t w = wsf(geo);
+    if (w > 0) {
+      const size_t slots = h->ws_floats / w;
       if (slots == 0) {
         g_last_error = "workspace too small for this size (raise max_m/max_n/max_p at tilt_create)";
         return TILT_E_ARG;
@@ -148,62 +158,60 @@ struct Launch {
     return TILT_OK;
   }
 
+  template <class Args>
+  static void set_ws(tilt_handle* h, Args& a, Geo geo) {
+    a.ws = wsf(geo) ? h->ws : nullptr;
+    a.ws_stride = wsf(geo);
+  }
+
   static tilt_status solve(tilt_handle* h, SolveArgs a) {
-    const int mn = a.m * a.n;
+    const Geo geo = geo_of<C>(a.m, a.n, a.p == 8 ? 3 : 2);
     const void* fn = (const void*)k_solve<C>;
-    const size_t sm = smem(mn, a.p);
     int g = 0;
-    tilt_status s = grid(h, fn, sm, a.B, mn, a.p, &g);
+    tilt_status s = grid(h, fn, geo, a.B, &g);
     if (s != TILT_OK) return s;
-    a.ws = Layout<C>::ws_floats(mn, a.p) ? h->ws : nullptr;
-    a.ws_stride = Layout<C>::ws_floats(mn, a.p);
+    set_ws(h, a, geo);
     TILT_CUDA(cudaMemsetAsync(a.counter, 0, sizeof(int), h->stream));
-    k_solve<C><<<g, C::NT, sm, h->stream>>>(a);
+    k_solve<C><<<g, C::NT, smem(geo), h->stream>>>(a);
     h->launches++;
     TILT_CUDA(cudaGetLastError());
     return TILT_OK;
   }
 
   static tilt_status inner(tilt_handle* h, InnerArgs a) {
-    const int mn = a.m * a.n;
+    const Geo geo = geo_of<C>(a.m, a.n, a.p);
     const void* fn = (const void*)k_inner<C>;
-    const size_t sm = smem(mn, a.p);
     int g = 0;
-    tilt_status s = grid(h, fn, sm, a.B, mn, a.p, &g);
+    tilt_status s = grid(h, fn, geo, a.B, &g);
     if (s != TILT_OK) return s;
-    a.ws = Layout<C>::ws_floats(mn, a.p) ? h->ws : nullptr;
-    a.ws_stride = Layout<C>::ws_floats(mn, a.p);
-    k_inner<C><<<g, C::NT, sm, h->stream>>>(a);
+    set_ws(h, a, geo);
+    k_inner<C><<<g, C::NT, smem(geo), h->stream>>>(a);
     h->launches++;
     TILT_CUDA(cudaGetLastError());
     return TILT_OK;
   }
 
   static tilt_status svt(tilt_handle* h, SvtArgs a) {
-    const int mn = a.m * a.n;
+    const Geo geo = geo_of<C>(a.m, a.n, 0);
     const void* fn = (const void*)k_svt<C>;
-    const size_t sm = smem(mn, 0);
     int g = 0;
-    tilt_status s = grid(h, fn, sm, a.B, mn, 0, &g);
+    tilt_status s = grid(h, fn, geo, a.B, &g);
     if (s != TILT_OK) return s;
-    a.ws = Layout<C>::ws_floats(mn, 0) ? h->ws : nullptr;
-    a.ws_stride = Layout<C>::ws_floats(mn, 0);
-    k_svt<C><<<g, C::NT, sm, h->stream>>>(a);
+    set_ws(h, a, geo);
+    k_svt<C><<<g, C::NT, smem(geo), h->stream>>>(a);
     h->launches++;
     TILT_CUDA(cudaGetLastError());
     return TILT_OK;
   }
 
   static tilt_status project(tilt_handle* h, ProjArgs a) {
-    const int mn = a.m * a.n;
+    const Geo geo = geo_of<C>(a.m, a.n, a.p);
     const void* fn = (const void*)k_project<C>;
-    const size_t sm = smem(mn, a.p);
     int g = 0;
-    tilt_status s = grid(h, fn, sm, a.B, mn, a.p, &g);
+    tilt_status s = grid(h, fn, geo, a.B, &g);
     if (s != TILT_OK) return s;
-    a.ws = Layout<C>::ws_floats(mn, a.p) ? h->ws : nullptr;
-    a.ws_stride = Layout<C>::ws_floats(mn, a.p);
-    k_project<C><<<g, C::NT, sm, h->stream>>>(a);
+    set_ws(h, a, geo);
+    k_project<C><<<g, C::NT, smem(geo), h->stream>>>(a);
     h->launches++;
     TILT_CUDA(cudaGetLastError());
     return TILT_OK;
@@ -238,28 +246,37 @@ struct ProjF {
   static tilt_status run(tilt_handle* h, ProjArgs a) { return Launch<C>::project(h, a); }
 };
 
-size_t ws_need(SizeClass c, int mn, int p) {
+// workspace floats per slot for the largest geometry of any entry (explicit K: p planes)
+size_t ws_need(SizeClass c, int m, int n, int gpl) {
   switch (c) {
-    case SC32: return Layout<CfgS32>::ws_floats(mn, p);
-    case SC64: return Layout<CfgS64>::ws_floats(mn, p);
-    case SC128: return Layout<CfgS128>::ws_floats(mn, p);
-    case SC256: return Layout<CfgS256>::ws_floats(mn, p);
+    case SC32: return Launch<CfgS32>::wsf(geo_of<CfgS32>(m, n, gpl));
+    case SC64: return Launch<CfgS64>::wsf(geo_of<CfgS64>(m, n, gpl));
+    case SC128: return Launch<CfgS128>::wsf(geo_of<CfgS128>(m, n, gpl));
+    case SC256: return Launch<CfgS256>::wsf(geo_of<CfgS256>(m, n, gpl));
     default: return 0;
   }
 }
 
-int occ_need(SizeClass c, int mn, int p) {
+template <class C>
+int occ_of(Geo g) {
+  const size_t sm = Launch<C>::smem(g);
+  int best = 0;
+  const void* fns[] = {(const void*)k_solve<C>, (const void*)k_inner<C>, (const void*)k_svt<C>,
+                       (const void*)k_project<C>};
+  for (const void* fn : fns) {
+    Launch<C>::prep(fn, sm);
+    const int o = occupancy_for<C>(fn, sm);
+    best = o > best ? o : best;
+  }
+  return best;
+}
+
+int occ_need(SizeClass c, int m, int n, int gpl) {
   switch (c) {
-    case SC128: {
-      const size_t sm = Layout<CfgS128>::smem_bytes(mn, p);
-      Launch<CfgS128>::prep((const void*)k_solve<CfgS128>, sm);
-      return occupancy_for<CfgS128>((const void*)k_solve<CfgS128>, sm);
-    }
-    case SC256: {
-      const size_t sm = Layout<CfgS256>::smem_bytes(mn, p);
-      Launch<CfgS256>::prep((const void*)k_solve<CfgS256>, sm);
-      return occupancy_for<CfgS256>((const void*)k_solve<CfgS256>, sm);
-    }
+    case SC32: return occ_of<CfgS32>(geo_of<CfgS32>(m, n, gpl));
+    case SC64: return occ_of<CfgS64>(geo_of<CfgS64>(m, n, gpl));
+    case SC128: return occ_of<CfgS128>(geo_of<CfgS128>(m, n, gpl));
+    case SC256: return occ_of<CfgS256>(geo_of<CfgS256>(m, n, gpl));
     default: return 1;
   }
 }
@@ -360,9 +377,10 @@ tilt_status tilt_create(tilt_handle** out, const tilt_create_opts* o) {
   };
   const SizeClass c = size_class(h->max_m, h->max_n);
   const int mn = h->max_m * h->max_n;
-  const size_t wsf = ws_need(c, mn, h->max_p);
+  const int gpl = h->max_p > 3 ? h->max_p : 3;
+  const size_t wsf = ws_need(c, h->max_m, h->max_n, gpl);
   if (wsf > 0) {
-    const int occ = occ_need(c, mn, h->max_p);
+    const int occ = occ_need(c, h->max_m, h->max_n, gpl);
     h->ws_slots = h->num_sms * (occ > 0 ? occ : 1);
     h->ws_floats = wsf * h->ws_slots;
     if ((e = cudaMalloc(&h->ws, h->ws_floats * sizeof(float))) != cudaSuccess) return fail(e, "cudaMalloc(ws)");

@@ -1,14 +1,15 @@
-// tilt_device.cuh — sm_100a device code of the batched TILT hot path.
+// tilt_device.cuh — sm_100a device building blocks of the batched TILT hot path.
 //
 // Paper: Ren & Lin, arXiv 1205.5351 (/root/reference/PAPER.md, cited P:<line>). Readings R*/Z*/E*
-// are listed in DESIGN.md. The kernels in tilt.cu instantiate these templates per size class.
+// are listed in DESIGN.md. tilt_kernels.cuh assembles these into the kernels.
 //
-// Data layout inside a CTA (one patch at a time):
-//   planes   D_hat, A, E, Y~ and K (p planes): column-major m x n, pixel (i,j) at j*m + i
-//   SVD      B = M V, V, S (M or the Newton-Schulz matrix): column-major, ld = MAXD (padded rows 0)
-//   vectors  nrm[MAXD] (column norms^2), scl[MAXD] (fast-rotation column scales), hv[MAXD]
-// Size classes put everything in shared memory (S32, S64), only the SVD buffers (S128) or nothing
-// (S256, per-CTA global workspace slot, L2 resident).
+// Data layout inside a CTA (one patch at a time). Every per-patch matrix
+// is column-major with one leading dimension LD = round_up(max(m, n), 4); rows >= m (>= n for V)
+// are kept at zero, so elementwise passes may run over the padded index space:
+//   planes   D_hat, A, E, Y~, then either the Jacobian factors GX, GY[, GZ] (implicit projector,
+//            TILT path) or K = J L^{-T} (p planes, explicit projector, generic-J entries)
+//   SVD      B = M V, V, S (M, or a Newton-Schulz temporary)
+//   vectors  ns[MAXD] = (||x_j||^2, scale_j) per Jacobi column, hv[MAXD]
 #pragma once
 
 #include <cuda_runtime.h>
@@ -28,7 +29,7 @@ constexpr unsigned FULL = 0xffffffffu;
 template <int LANES_, int RPL_, int NWARPS_, bool PLANES_SMEM_, bool SVD_SMEM_, int MINB_>
 struct Cfg {
   static constexpr int LANES = LANES_;   // lanes per Jacobi pair unit (16: half warp, 32: warp)
-  static constexpr int RPL = RPL_;       // rows per lane (B and V columns padded to MAXD rows)
+  static constexpr int RPL = RPL_;       // rows per lane (a column holds up to MAXD rows)
   static constexpr int NWARPS = NWARPS_;
   static constexpr int NT = NWARPS_ * 32;
   static constexpr int MAXD = LANES_ * RPL_;
@@ -38,8 +39,11 @@ struct Cfg {
   static constexpr int MINB = MINB_;
 };
 
-using CfgS32 = Cfg<16, 2, 8, true, true, 2>;
-using CfgS64 = Cfg<16, 4, 16, true, true, 1>;
+// S64: planes (D, A, E, Y, GX, GY, GZ; 73 KB at 50x50) live in the per-CTA global workspace slot
+// (L2-resident, touched only by the elementwise passes); B, V, S (31 KB) stay in shared memory, so
+// 4 independent patches share an SM and hide each other's per-round barrier and shuffle latency.
+using CfgS32 = Cfg<8, 4, 8, true, true, 4>;
+using CfgS64 = Cfg<8, 8, 8, false, true, 4>;
 using CfgS128 = Cfg<16, 8, 32, false, true, 1>;
 using CfgS256 = Cfg<32, 8, 32, false, false, 1>;
 
@@ -55,15 +59,12 @@ struct DevParams {
 
 // Scalars and reduction scratch of one CTA (static shared memory).
 struct Scal {
-  double L[64];      // Cholesky factor of G = J^TJ + Q^TQ (row-major p x p, lower)
-  double Linv[64];   // L^{-1}
-  double c[8];       // D_hat^T J_raw (quotient rule, Alg. 1 Step 1)
-  double tau[8];
-  double dtau[8];
-  double q[24];      // Q (3 x p)
-  double dred[32 * 12];
+  double Linv[64];   // L^{-1}, L L^T = G = J^TJ + Q^TQ (row-major p x p, lower)
+  double dred[16 * 12];
   double dout[12];
-  float fred[32 * 9];
+  float Lp[64];      // L^{-1} / ||d|| (fp32, implicit projector)
+  float cp[8];       // L^{-1} c / ||d||, c = D_hat^T J_raw
+  float fred[32 * 10];
   float fout[12];
   float nd;          // ||D o tau||_F
   float svt_nuc;     // sum_j max(sigma_j - eps, 0) of the last SVT (= ||A||_*)
@@ -81,6 +82,7 @@ struct Scal {
 
 template <class C, int KV>
 __device__ __forceinline__ void block_sum_f(float (&v)[KV], Scal* sc) {
+  static_assert(KV <= 10, "fred holds 10 values per warp");
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
 #pragma unroll
   for (int k = 0; k < KV; ++k) {
@@ -91,12 +93,12 @@ __device__ __forceinline__ void block_sum_f(float (&v)[KV], Scal* sc) {
   }
   if (lane == 0) {
 #pragma unroll
-    for (int k = 0; k < KV; ++k) sc->fred[w * KV + k] = v[k];
+    for (int k = 0; k < KV; ++k) sc->fred[w * 10 + k] = v[k];
   }
   __syncthreads();
   if (threadIdx.x < KV) {
     float s = 0.f;
-    for (int ww = 0; ww < C::NWARPS; ++ww) s += sc->fred[ww * KV + threadIdx.x];
+    for (int ww = 0; ww < C::NWARPS; ++ww) s += sc->fred[ww * 10 + threadIdx.x];
     sc->fout[threadIdx.x] = s;
   }
   __syncthreads();
@@ -104,8 +106,10 @@ __device__ __forceinline__ void block_sum_f(float (&v)[KV], Scal* sc) {
   for (int k = 0; k < KV; ++k) v[k] = sc->fout[k];
 }
 
+// fp64 block sum (used once per outer iteration): warp shuffles, then warps 0..KV-1 finish.
 template <class C, int KV>
 __device__ __forceinline__ void block_sum_d(double (&v)[KV], Scal* sc) {
+  static_assert(KV <= 12, "dout holds 12 values");
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
 #pragma unroll
   for (int k = 0; k < KV; ++k) {
@@ -114,17 +118,21 @@ __device__ __forceinline__ void block_sum_d(double (&v)[KV], Scal* sc) {
     for (int off = 16; off; off >>= 1) x += __shfl_xor_sync(FULL, x, off);
     v[k] = x;
   }
-  if (lane == 0) {
+  // two stages so that dred (16 x 12) suffices for up to 32 warps
+  for (int half = 0; half < (C::NWARPS + 15) / 16; ++half) {
+    if (lane == 0 && (w >> 4) == half) {
 #pragma unroll
-    for (int k = 0; k < KV; ++k) sc->dred[w * KV + k] = v[k];
+      for (int k = 0; k < KV; ++k) sc->dred[(w & 15) * 12 + k] = v[k];
+    }
+    __syncthreads();
+    if (threadIdx.x < KV) {
+      double s = half ? sc->dout[threadIdx.x] : 0.0;
+      const int nw = min(16, C::NWARPS - 16 * half);
+      for (int ww = 0; ww < nw; ++ww) s += sc->dred[ww * 12 + threadIdx.x];
+      sc->dout[threadIdx.x] = s;
+    }
+    __syncthreads();
   }
-  __syncthreads();
-  if (threadIdx.x < KV) {
-    double s = 0.0;
-    for (int ww = 0; ww < C::NWARPS; ++ww) s += sc->dred[ww * KV + threadIdx.x];
-    sc->dout[threadIdx.x] = s;
-  }
-  __syncthreads();
 #pragma unroll
   for (int k = 0; k < KV; ++k) v[k] = sc->dout[k];
 }
@@ -135,59 +143,74 @@ __device__ __forceinline__ void block_sum_d(double (&v)[KV], Scal* sc) {
 
 template <class C>
 struct Ctx {
-  float *D, *A, *E, *Y, *K;  // planes (col-major, ld = m); K holds p planes back to back
-  float *B, *V, *S;          // SVD buffers (col-major, ld = MAXD)
-  float *nrm, *scl, *hv;
+  float *D, *A, *E, *Y;  // planes (col-major, ld)
+  float *G;              // implicit projector: GX, GY, GZ planes; explicit: K (p planes)
+  float *B, *V, *S;      // SVD buffers (col-major, ld)
+  float4* ns;            // (norm^2, scale, 1/scale, -) per Jacobi column
+  float* hv;
   Scal* sc;
-  int m, n, p, mn;
+  int m, n, p, ld, pl;   // pl = ld * n (plane size)
+  float ci, cj, inv_s;   // normalised frame: u = (j - cj) inv_s, v = (i - ci) inv_s
 };
 
-// Pixel iterator over the column-major plane index idx = j*m + i with stride NT.
+__host__ __device__ inline int round4(int x) { return (x + 3) & ~3; }
+
+// Leading dimension of every per-patch matrix: a multiple of 4 (float4 tiles; Jacobi lanes mask
+// the float4 chunks beyond ld, so a lane never touches the next column).
+template <class C>
+__host__ __device__ inline int ld_of(int m, int n) {
+  static_assert(C::RPL % 4 == 0, "Jacobi lanes move float4 chunks");
+  return round4(m > n ? m : n);
+}
+
+// Pixel iterator over the column-major padded index idx = j*ld + i with stride NT.
 struct PixIter {
-  int idx, i, j, di, dj, m;
-  __device__ __forceinline__ PixIter(int start, int stride, int m_) : idx(start), m(m_) {
-    j = start / m_;
-    i = start - j * m_;
-    dj = stride / m_;
-    di = stride - dj * m_;
+  int idx, i, j, di, dj, ld;
+  __device__ __forceinline__ PixIter(int start, int stride, int ld_) : idx(start), ld(ld_) {
+    j = start / ld_;
+    i = start - j * ld_;
+    dj = stride / ld_;
+    di = stride - dj * ld_;
   }
   __device__ __forceinline__ void next(int stride) {
     idx += stride;
     i += di;
     j += dj;
-    if (i >= m) {
-      i -= m;
+    if (i >= ld) {
+      i -= ld;
       ++j;
     }
   }
 };
 
 // --------------------------------------------------------------------------------------------
-// Small dense kernels on the padded SVD buffers (column-major, ld = MAXD)
+// Small dense kernels on the padded column-major buffers
 // --------------------------------------------------------------------------------------------
 
-// C = L * R, L: rows x inner, R: inner x cols (C must not alias L or R). Rows >= rows_valid of C
-// are written as 0. Thread tile: 4 rows x 2 columns (one float4 of L and two scalars of R per k).
+// C = L * R (L: ld x inner, R: inner x cols; C must not alias L or R). Every row group of the
+// padded column is written; rows >= rows_valid are written as 0. Thread tile: 4 rows x 2 columns,
+// one float4 of L and two broadcast scalars of R per k, float4 stores.
 template <class C>
 __device__ __forceinline__ void gemm_nn(float* __restrict__ Cm, const float* __restrict__ Lm,
-                                        const float* __restrict__ Rm, int rows_valid, int inner, int cols) {
-  constexpr int MD = C::MAXD;
-  constexpr int rt = MD / 4;  // every row group of the padded column is written (zeros below rows_valid)
+                                        const float* __restrict__ Rm, int ld, int rows_valid, int inner,
+                                        int cols) {
+  const int rt = ld >> 2;
   const int ct = (cols + 1) >> 1;
   const int ntiles = rt * ct;
   for (int tile = threadIdx.x; tile < ntiles; tile += C::NT) {
     const int i0 = (tile % rt) * 4;
     const int j0 = (tile / rt) * 2;
+    const bool two = j0 + 1 < cols;
     float acc[8];
 #pragma unroll
     for (int e = 0; e < 8; ++e) acc[e] = 0.f;
     const float* lp = Lm + i0;
-    const float* r0 = Rm + j0 * MD;
-    const float* r1 = r0 + MD;
+    const float* r0 = Rm + j0 * ld;
+    const float* r1 = two ? r0 + ld : r0;
     const int kend = i0 < rows_valid ? inner : 0;
 #pragma unroll 4
     for (int k = 0; k < kend; ++k) {
-      const float4 a = *reinterpret_cast<const float4*>(lp + k * MD);
+      const float4 a = *reinterpret_cast<const float4*>(lp + k * ld);
       const float b0 = r0[k], b1 = r1[k];
       acc[0] = fmaf(a.x, b0, acc[0]);
       acc[1] = fmaf(a.y, b0, acc[1]);
@@ -200,54 +223,20 @@ __device__ __forceinline__ void gemm_nn(float* __restrict__ Cm, const float* __r
     }
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
-      const bool ok = (i0 + r) < rows_valid;
-      Cm[j0 * MD + i0 + r] = ok ? acc[r] : 0.f;
-      if (j0 + 1 < cols) Cm[(j0 + 1) * MD + i0 + r] = ok ? acc[4 + r] : 0.f;
-    }
-  }
-  __syncthreads();
-}
-
-// Z = 1.5 I - 0.5 V^T V (one Newton-Schulz step for the polar factor: V <- V Z), into Zm.
-template <class C>
-__device__ __forceinline__ void ns_matrix(float* Zm, const float* Vm, int n) {
-  constexpr int MD = C::MAXD;
-  const int rt = (n + 3) >> 2;
-  const int ct = (n + 1) >> 1;
-  const int ntiles = rt * ct;
-  for (int tile = threadIdx.x; tile < ntiles; tile += C::NT) {
-    const int i0 = (tile % rt) * 4;
-    const int j0 = (tile / rt) * 2;
-    float acc[8];
-#pragma unroll
-    for (int e = 0; e < 8; ++e) acc[e] = 0.f;
-    for (int k = 0; k < n; k += 4) {  // rows of V (padded with zeros up to MAXD)
-      float4 vi[4];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) vi[c] = *reinterpret_cast<const float4*>(Vm + (i0 + c) * MD + k);
-      const float4 w0 = *reinterpret_cast<const float4*>(Vm + j0 * MD + k);
-      const float4 w1 = *reinterpret_cast<const float4*>(Vm + (j0 + 1) * MD + k);
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        acc[c] = fmaf(vi[c].x, w0.x, fmaf(vi[c].y, w0.y, fmaf(vi[c].z, w0.z, fmaf(vi[c].w, w0.w, acc[c]))));
-        acc[4 + c] =
-            fmaf(vi[c].x, w1.x, fmaf(vi[c].y, w1.y, fmaf(vi[c].z, w1.z, fmaf(vi[c].w, w1.w, acc[4 + c]))));
+      if (i0 + r >= rows_valid) {
+        acc[r] = 0.f;
+        acc[4 + r] = 0.f;
       }
     }
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const int i = i0 + c;
-      Zm[j0 * MD + i] = (i < n) ? ((i == j0 ? 1.5f : 0.f) - 0.5f * acc[c]) : 0.f;
-      if (j0 + 1 < n) Zm[(j0 + 1) * MD + i] = (i < n) ? ((i == j0 + 1 ? 1.5f : 0.f) - 0.5f * acc[4 + c]) : 0.f;
-    }
+    *reinterpret_cast<float4*>(Cm + j0 * ld + i0) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+    if (two) *reinterpret_cast<float4*>(Cm + (j0 + 1) * ld + i0) = make_float4(acc[4], acc[5], acc[6], acc[7]);
   }
   __syncthreads();
 }
 
-// out(i, j) = sum_k B'[i][k] V[j][k] (B' = B diag(h), pre-scaled), i < m, j < n.
+// out(i0, j, float4 of rows i0..i0+3) for C = B' V^T (B' = B diag(h) pre-scaled): i0 < m, j < n.
 template <class C, class Out>
-__device__ __forceinline__ void gemm_bvt(const float* Bm, const float* Vm, int m, int n, Out out) {
-  constexpr int MD = C::MAXD;
+__device__ __forceinline__ void gemm_bvt(const float* Bm, const float* Vm, int ld, int m, int n, Out out) {
   const int rt = (m + 3) >> 2;
   const int ct = (n + 1) >> 1;
   const int ntiles = rt * ct;
@@ -259,8 +248,8 @@ __device__ __forceinline__ void gemm_bvt(const float* Bm, const float* Vm, int m
     for (int e = 0; e < 8; ++e) acc[e] = 0.f;
 #pragma unroll 4
     for (int k = 0; k < n; ++k) {
-      const float4 a = *reinterpret_cast<const float4*>(Bm + k * MD + i0);
-      const float2 v = *reinterpret_cast<const float2*>(Vm + k * MD + j0);
+      const float4 a = *reinterpret_cast<const float4*>(Bm + k * ld + i0);
+      const float2 v = *reinterpret_cast<const float2*>(Vm + k * ld + j0);
       acc[0] = fmaf(a.x, v.x, acc[0]);
       acc[1] = fmaf(a.y, v.x, acc[1]);
       acc[2] = fmaf(a.z, v.x, acc[2]);
@@ -270,271 +259,40 @@ __device__ __forceinline__ void gemm_bvt(const float* Bm, const float* Vm, int m
       acc[6] = fmaf(a.z, v.y, acc[6]);
       acc[7] = fmaf(a.w, v.y, acc[7]);
     }
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      if (i0 + r < m) {
-        out(i0 + r, j0, acc[r]);
-        if (j0 + 1 < n) out(i0 + r, j0 + 1, acc[4 + r]);
-      }
-    }
+    out(i0, j0, make_float4(acc[0], acc[1], acc[2], acc[3]));
+    if (j0 + 1 < n) out(i0, j0 + 1, make_float4(acc[4], acc[5], acc[6], acc[7]));
   }
 }
 
 template <class C>
-__device__ __forceinline__ void set_identity(float* Vm, int n) {
-  constexpr int MD = C::MAXD;
-  for (int e = threadIdx.x; e < MD * MD; e += C::NT) {
-    const int j = e / MD, i = e - j * MD;
-    Vm[e] = (i == j && i < n) ? 1.f : 0.f;
+__device__ __forceinline__ void set_identity(float* Vm, int ld, int n) {
+  for (int e = threadIdx.x; e < ld * n; e += C::NT) {
+    const int j = e / ld, i = e - j * ld;
+    Vm[e] = (i == j) ? 1.f : 0.f;
   }
 }
 
+// Y = X^T for an n x n block (ld-padded, rows >= n of Y zero); conflict-light via 33-stride reads.
 template <class C>
-__device__ __forceinline__ void zero_buf(float* Xm) {
-  constexpr int MD = C::MAXD;
-  for (int e = threadIdx.x; e < MD * MD; e += C::NT) Xm[e] = 0.f;
-}
-
-// --------------------------------------------------------------------------------------------
-// One-sided (Hestenes) Jacobi on B = M V with fast (scaled) rotations
-// --------------------------------------------------------------------------------------------
-// Column pair (i, j): gamma = b_i . b_j; if |gamma| > tol sqrt(alpha beta) rotate so that the two
-// columns become orthogonal (t = sgn(zeta)/(|zeta| + sqrt(1 + zeta^2)), zeta = (beta-alpha)/2gamma).
-// Columns are stored scaled, b_j = scl_j x_j, so a rotation costs 2 FMAs per row instead of 4:
-// x_i <- x_i - t (scl_j/scl_i) x_j, x_j <- x_j + t (scl_i/scl_j) x_i, scl <- c scl. The same
-// transformation is applied to V, so B = M V holds throughout. Pair schedule: round-robin
-// (circle method), n/2 disjoint pairs per round, one pair per LANES-lane unit, barrier per round.
-
-template <class C, int MODE>
-__device__ __forceinline__ void col_pass(Ctx<C>& cx, int n, float eps) {
-  // MODE 0: nrm_j = ||x_j||^2, scl_j = 1 (no scaling applied)
-  // MODE 1: apply scl to B and V columns, nrm_j fresh, scl_j = 1
-  // MODE 2: as 1, then compute sigma_j = sqrt(nrm_j) and h_j = max(sigma-eps,0)/sigma (into hv)
-  constexpr int MD = C::MAXD, L = C::LANES, RPL = C::RPL;
-  const int unit = threadIdx.x / L, lu = threadIdx.x % L;
-  const int warp = threadIdx.x >> 5;
-  constexpr int UPW = 32 / L;  // units per warp
-  for (int jb = warp * UPW; jb < n; jb += C::UNITS) {
-    const int j = jb + (unit - warp * UPW);
-    const bool valid = j < n;
-    const int jj = valid ? j : 0;
-    float* bp = cx.B + jj * MD + lu * RPL;
-    float* vp = cx.V + jj * MD + lu * RPL;
-    float x[RPL];
-#pragma unroll
-    for (int r = 0; r < RPL; r += 4) {
-      if constexpr (RPL >= 4) {
-        float4 t = *reinterpret_cast<float4*>(bp + r);
-        x[r] = t.x; x[r + 1] = t.y; x[r + 2] = t.z; x[r + 3] = t.w;
-      }
-    }
-    if constexpr (RPL == 2) {
-      float2 t = *reinterpret_cast<float2*>(bp);
-      x[0] = t.x; x[1] = t.y;
-    }
-    const float s = (MODE == 0) ? 1.f : cx.scl[jj];
-    float ss = 0.f;
-#pragma unroll
-    for (int r = 0; r < RPL; ++r) {
-      x[r] *= s;
-      ss = fmaf(x[r], x[r], ss);
-    }
-#pragma unroll
-    for (int off = L / 2; off; off >>= 1) ss += __shfl_xor_sync(FULL, ss, off);
-    float y[RPL];
-    float vv = 1.f;
-    if (MODE != 0) {
-      if constexpr (RPL >= 4) {
-#pragma unroll
-        for (int r = 0; r < RPL; r += 4) {
-          const float4 t = *reinterpret_cast<const float4*>(vp + r);
-          y[r] = t.x * s; y[r + 1] = t.y * s; y[r + 2] = t.z * s; y[r + 3] = t.w * s;
-        }
-      } else {
-        const float2 t = *reinterpret_cast<const float2*>(vp);
-        y[0] = t.x * s; y[1] = t.y * s;
-      }
-    }
-    if (MODE == 2) {
-      // rotations are orthogonal only to fp32 rounding, which drifts the column norms of V by a
-      // few 1e-6 per SVT: B = M V holds for the drifted V, so sigma_j = ||b_j|| / ||v_j|| and
-      // A = sum_j h_j b_j v_j^T / ||v_j||^2 remove that scale exactly.
-      vv = 0.f;
-#pragma unroll
-      for (int r = 0; r < RPL; ++r) vv = fmaf(y[r], y[r], vv);
-#pragma unroll
-      for (int off = L / 2; off; off >>= 1) vv += __shfl_xor_sync(FULL, vv, off);
-      ss = vv > 0.f ? ss / vv : 0.f;
-    }
-    float h = 1.f;
-    if (MODE == 2) {
-      const float sg = sqrtf(ss);
-      h = (sg > eps) ? (sg - eps) / sg : 0.f;
-    }
-    if (valid && MODE != 0) {
-      const float hb = (MODE == 2) ? (vv > 0.f ? h / vv : 0.f) : 1.f;
-#pragma unroll
-      for (int r = 0; r < RPL; ++r) x[r] *= hb;
-      // B columns are stored pre-multiplied by h/||v||^2 in MODE 2 (ready for A = B' V^T)
-      if constexpr (RPL >= 4) {
-#pragma unroll
-        for (int r = 0; r < RPL; r += 4) {
-          *reinterpret_cast<float4*>(bp + r) = make_float4(x[r], x[r + 1], x[r + 2], x[r + 3]);
-          *reinterpret_cast<float4*>(vp + r) = make_float4(y[r], y[r + 1], y[r + 2], y[r + 3]);
-        }
-      } else {
-        *reinterpret_cast<float2*>(bp) = make_float2(x[0], x[1]);
-        *reinterpret_cast<float2*>(vp) = make_float2(y[0], y[1]);
-      }
-    }
-    if (valid && lu == 0) {
-      cx.nrm[j] = ss;
-      cx.scl[j] = 1.f;
-      if (MODE == 2) cx.hv[j] = h;
-    }
-  }
-  __syncthreads();
-}
-
-__device__ __forceinline__ void rr_pair(int r, int k, int Nn, int& i, int& j) {
-  if (k == 0) {
-    i = Nn - 1;
-    j = r;
-  } else {
-    const int q = Nn - 1;
-    i = (r + k) % q;
-    j = (r - k + q) % q;
+__device__ __forceinline__ void transpose_nn(float* __restrict__ Ym, const float* __restrict__ Xm, int ld, int n) {
+  for (int e = threadIdx.x; e < ld * n; e += C::NT) {
+    const int j = e / ld, i = e - j * ld;  // Y(i, j) = X(j, i)
+    Ym[e] = (i < n) ? Xm[i * ld + j] : 0.f;
   }
 }
 
-// Returns the number of sweeps; *capped = the last sweep still rotated at the sweep cap.
+#include "tilt_jacobi.cuh"
+
+// sigma_j = sqrt(ns_j.x) stats after the final pass: nuclear norm of S_eps, ranks (Z19), sigma_1.
 template <class C>
-__device__ int jacobi_sweeps(Ctx<C>& cx, int n, float tol, int max_sweeps, bool* capped) {
-  constexpr int MD = C::MAXD, L = C::LANES, RPL = C::RPL;
-  constexpr int UPW = 32 / L;
-  const int unit = threadIdx.x / L, lu = threadIdx.x % L;
-  const int warp = threadIdx.x >> 5;
-  const int Nn = n + (n & 1);
-  const int npairs = Nn >> 1;
-  float* __restrict__ Bm = cx.B;
-  float* __restrict__ Vm = cx.V;
-  float* __restrict__ nrm = cx.nrm;
-  float* __restrict__ scl = cx.scl;
-  col_pass<C, 0>(cx, n, 0.f);
-  int sweeps = 0;
-  bool any = false;
-  while (sweeps < max_sweeps) {
-    bool rot = false;
-    for (int r = 0; r < Nn - 1; ++r) {
-      for (int kb = warp * UPW; kb < npairs; kb += C::UNITS) {
-        const int k = kb + (unit - warp * UPW);
-        int i = 0, j = 0;
-        if (k < npairs) rr_pair(r, k, Nn, i, j);
-        const bool valid = (k < npairs) && (i < n) && (j < n);
-        if (!valid) { i = 0; j = 0; }
-        float* bi = Bm + i * MD + lu * RPL;
-        float* bj = Bm + j * MD + lu * RPL;
-        float* vi = Vm + i * MD + lu * RPL;
-        float* vj = Vm + j * MD + lu * RPL;
-        float xi[RPL], xj[RPL];
-        if constexpr (RPL >= 4) {
-#pragma unroll
-          for (int q = 0; q < RPL; q += 4) {
-            const float4 a = *reinterpret_cast<const float4*>(bi + q);
-            const float4 b = *reinterpret_cast<const float4*>(bj + q);
-            xi[q] = a.x; xi[q + 1] = a.y; xi[q + 2] = a.z; xi[q + 3] = a.w;
-            xj[q] = b.x; xj[q + 1] = b.y; xj[q + 2] = b.z; xj[q + 3] = b.w;
-          }
-        } else {
-          const float2 a = *reinterpret_cast<const float2*>(bi);
-          const float2 b = *reinterpret_cast<const float2*>(bj);
-          xi[0] = a.x; xi[1] = a.y; xj[0] = b.x; xj[1] = b.y;
-        }
-        float g = 0.f;
-#pragma unroll
-        for (int q = 0; q < RPL; ++q) g = fmaf(xi[q], xj[q], g);
-#pragma unroll
-        for (int off = L / 2; off; off >>= 1) g += __shfl_xor_sync(FULL, g, off);
-        const float al = nrm[i], be = nrm[j], di = scl[i], dj = scl[j];
-        const float gam = g * di * dj;
-        if (valid && al > 0.f && be > 0.f && fabsf(gam) > tol * sqrtf(al * be)) {
-          const float zeta = (be - al) / (2.f * gam);
-          const float az = fabsf(zeta);
-          float t = (az > 1e18f) ? 0.5f / zeta : copysignf(1.f, zeta) / (az + sqrtf(fmaf(zeta, zeta, 1.f)));
-          const float x = fmaf(t, t, 1.f);
-          float c = rsqrtf(x);
-          c = c * fmaf(-0.5f * x * c, c, 1.5f);  // one Newton step: c = 1/sqrt(1+t^2) to ~1 ulp
-          const float ca = t * (dj / di);
-          const float cb = t * (di / dj);
-#pragma unroll
-          for (int q = 0; q < RPL; ++q) {
-            const float o = xi[q];
-            xi[q] = fmaf(-ca, xj[q], o);
-            xj[q] = fmaf(cb, o, xj[q]);
-          }
-          float yi[RPL], yj[RPL];
-          if constexpr (RPL >= 4) {
-#pragma unroll
-            for (int q = 0; q < RPL; q += 4) {
-              const float4 a = *reinterpret_cast<const float4*>(vi + q);
-              const float4 b = *reinterpret_cast<const float4*>(vj + q);
-              yi[q] = a.x; yi[q + 1] = a.y; yi[q + 2] = a.z; yi[q + 3] = a.w;
-              yj[q] = b.x; yj[q + 1] = b.y; yj[q + 2] = b.z; yj[q + 3] = b.w;
-            }
-          } else {
-            const float2 a = *reinterpret_cast<const float2*>(vi);
-            const float2 b = *reinterpret_cast<const float2*>(vj);
-            yi[0] = a.x; yi[1] = a.y; yj[0] = b.x; yj[1] = b.y;
-          }
-#pragma unroll
-          for (int q = 0; q < RPL; ++q) {
-            const float o = yi[q];
-            yi[q] = fmaf(-ca, yj[q], o);
-            yj[q] = fmaf(cb, o, yj[q]);
-          }
-          if constexpr (RPL >= 4) {
-#pragma unroll
-            for (int q = 0; q < RPL; q += 4) {
-              *reinterpret_cast<float4*>(bi + q) = make_float4(xi[q], xi[q + 1], xi[q + 2], xi[q + 3]);
-              *reinterpret_cast<float4*>(bj + q) = make_float4(xj[q], xj[q + 1], xj[q + 2], xj[q + 3]);
-              *reinterpret_cast<float4*>(vi + q) = make_float4(yi[q], yi[q + 1], yi[q + 2], yi[q + 3]);
-              *reinterpret_cast<float4*>(vj + q) = make_float4(yj[q], yj[q + 1], yj[q + 2], yj[q + 3]);
-            }
-          } else {
-            *reinterpret_cast<float2*>(bi) = make_float2(xi[0], xi[1]);
-            *reinterpret_cast<float2*>(bj) = make_float2(xj[0], xj[1]);
-            *reinterpret_cast<float2*>(vi) = make_float2(yi[0], yi[1]);
-            *reinterpret_cast<float2*>(vj) = make_float2(yj[0], yj[1]);
-          }
-          if (lu == 0) {
-            nrm[i] = fmaxf(fmaf(-t, gam, al), 0.f);
-            nrm[j] = fmaf(t, gam, be);
-            scl[i] = c * di;
-            scl[j] = c * dj;
-          }
-          rot = true;
-        }
-      }
-      __syncthreads();
-    }
-    ++sweeps;
-    any = __syncthreads_or(rot);
-    col_pass<C, 1>(cx, n, 0.f);  // re-normalise (apply scales, fresh norms)
-    if (!any) break;
-  }
-  *capped = any;
-  return sweeps;
-}
-
-// sigma_j = sqrt(nrm_j) stats after the final pass: nuclear norm of S_eps, ranks (Z19), sigma_1.
-template <class C>
-__device__ __forceinline__ void svt_stats(Ctx<C>& cx, int n, float eps) {
+__device__ __forceinline__ void svt_stats(Ctx<C>& cx, float eps) {
+  const int n = cx.n;
   if (threadIdx.x < 32) {
     const int lane = threadIdx.x;
     float nuc = 0.f, smax = 0.f, amax = 0.f;
     int cnt = 0;
     for (int j = lane; j < n; j += 32) {
-      const float sg = sqrtf(cx.nrm[j]);
+      const float sg = sqrtf(cx.ns[j].x);
       const float a = fmaxf(sg - eps, 0.f);
       nuc += a;
       smax = fmaxf(smax, sg);
@@ -550,7 +308,7 @@ __device__ __forceinline__ void svt_stats(Ctx<C>& cx, int n, float eps) {
     }
     int rel = 0, band = 0;
     for (int j = lane; j < n; j += 32) {
-      const float a = fmaxf(sqrtf(cx.nrm[j]) - eps, 0.f);
+      const float a = fmaxf(sqrtf(cx.ns[j].x) - eps, 0.f);
       if (amax > 0.f) {
         const float ratio = a / amax;
         rel += ratio > 1e-3f;
@@ -573,13 +331,21 @@ __device__ __forceinline__ void svt_stats(Ctx<C>& cx, int n, float eps) {
 }
 
 // Newton-Schulz re-orthonormalisation of V (reading Z14): V <- V (1.5 I - 0.5 V^T V).
-// Uses S as the n x n temporary and B as the output, then swaps B and V.
+// S <- V^T, B <- S V, B <- 1.5 I - 0.5 B, S <- V B, swap(S, V). B and S must be free.
 template <class C>
-__device__ __forceinline__ void ns_step(Ctx<C>& cx, int n) {
-  ns_matrix<C>(cx.S, cx.V, n);
-  gemm_nn<C>(cx.B, cx.V, cx.S, n, n, n);
-  float* t = cx.B;
-  cx.B = cx.V;
+__device__ __forceinline__ void ns_step(Ctx<C>& cx) {
+  const int n = cx.n, ld = cx.ld;
+  transpose_nn<C>(cx.S, cx.V, ld, n);
+  __syncthreads();
+  gemm_nn<C>(cx.B, cx.S, cx.V, ld, n, n, n);
+  for (int e = threadIdx.x; e < ld * n; e += C::NT) {
+    const int j = e / ld, i = e - j * ld;
+    cx.B[e] = (i == j ? 1.5f : 0.f) - 0.5f * cx.B[e];
+  }
+  __syncthreads();
+  gemm_nn<C>(cx.S, cx.V, cx.B, ld, n, n, n);
+  float* t = cx.S;
+  cx.S = cx.V;
   cx.V = t;
 }
 
@@ -588,23 +354,29 @@ struct SvtOut {
   bool capped;
 };
 
-// S_eps(M) with M in S (padded col-major). Leaves V (orthonormalised by one Newton-Schulz step)
-// warm for the next call, calls out(i, j, a_ij) for every entry of the result.
+// S_eps(X) for X (= M, or D_hat) in a padded buffer. Leaves V warm (orthonormalised by one
+// Newton-Schulz step if ns_after) and calls out(i0, j, float4 rows i0..i0+3 of the result).
 template <class C, bool DO_OUT, class Out>
-__device__ SvtOut svt(Ctx<C>& cx, int m, int n, float eps, float tol, int max_sweeps, bool warm, Out out,
-                      bool orthonormalise_after) {
+__device__ SvtOut svt(Ctx<C>& cx, const float* X, float eps, float tol, int max_sweeps, bool warm, Out out,
+                      bool ns_after) {
   if (!warm) {
-    set_identity<C>(cx.V, n);
+    set_identity<C>(cx.V, cx.ld, cx.n);
     __syncthreads();
   }
-  gemm_nn<C>(cx.B, cx.S, cx.V, m, n, n);  // B = M V
+  gemm_nn<C>(cx.B, X, cx.V, cx.ld, cx.m, cx.n, cx.n);  // B = X V
   SvtOut r;
-  r.sweeps = jacobi_sweeps<C>(cx, n, tol, max_sweeps, &r.capped);
-  col_pass<C, 2>(cx, n, eps);  // sigma_j, h_j, B <- B diag(h)
-  svt_stats<C>(cx, n, eps);
-  if constexpr (DO_OUT) gemm_bvt<C>(cx.B, cx.V, m, n, out);  // A = B diag(h) V^T
+  if constexpr (C::SVD_SMEM) {
+    int capped = 0;
+    r.sweeps = jacobi_sweeps_smem<C>(cx.B, cx.V, cx.ns, cx.n, cx.ld, tol, max_sweeps, &capped);
+    r.capped = capped != 0;
+  } else {
+    r.sweeps = jacobi_sweeps<C>(cx, tol, max_sweeps, &r.capped);
+  }
+  col_pass<C, 2>(cx, eps);  // sigma_j, h_j, B <- B diag(h / ||v||^2)
+  svt_stats<C>(cx, eps);
+  if constexpr (DO_OUT) gemm_bvt<C>(cx.B, cx.V, cx.ld, cx.m, cx.n, out);  // A = B diag(h) V^T
   __syncthreads();
-  if (orthonormalise_after) ns_step<C>(cx, n);
+  if (ns_after) ns_step<C>(cx);
   return r;
 }
 
@@ -633,9 +405,11 @@ __device__ __forceinline__ WarpGeom make_geom(const int* box, const double* tau,
   return g;
 }
 
-// Bilinear sample d and J_raw row (p entries) at window pixel (i, j). Returns false on escape.
+// Bilinear sample d and the Jacobian factors (gx, gy, gz) at window pixel (i, j):
+// J_raw = (gx u, gx v, gy u, gy v, gx, gy, gz u, gz v) with gx = s I_X / w, gy = s I_Y / w,
+// gz = -(gx x + gy y) (normalised frame). Returns false on window escape.
 __device__ __forceinline__ bool warp_pixel(const WarpGeom& g, const float* __restrict__ img, int H, int W,
-                                           int i, int j, double& d, double (&jr)[8]) {
+                                           int i, int j, double& d, double& gx, double& gy, double& gz) {
   const double du = j - 0.5 * (g.n - 1);
   const double dv = i - 0.5 * (g.m - 1);
   const double w = 1.0 + (g.h31 * du + g.h32 * dv) / g.s;
@@ -643,9 +417,7 @@ __device__ __forceinline__ bool warp_pixel(const WarpGeom& g, const float* __res
   const double Y = g.cy + (g.h21 * du + g.h22 * dv + g.s * g.h23) / w;
   const double X0 = floor(X), Y0 = floor(Y);
   if (!(X0 >= 0.0 && X0 + 1.0 <= W - 1 && Y0 >= 0.0 && Y0 + 1.0 <= H - 1)) {
-    d = 0.0;
-#pragma unroll
-    for (int q = 0; q < 8; ++q) jr[q] = 0.0;
+    d = gx = gy = gz = 0.0;
     return false;
   }
   const double fx = X - X0, fy = Y - Y0;
@@ -655,16 +427,19 @@ __device__ __forceinline__ bool warp_pixel(const WarpGeom& g, const float* __res
   d = (1.0 - fy) * ((1.0 - fx) * i00 + fx * i01) + fy * ((1.0 - fx) * i10 + fx * i11);
   const double dX = (1.0 - fy) * (i01 - i00) + fy * (i11 - i10);
   const double dY = (1.0 - fx) * (i10 - i00) + fx * (i11 - i01);
-  const double u = du / g.s, v = dv / g.s;
   const double xn = (X - g.cx) / g.s, yn = (Y - g.cy) / g.s;
-  const double gx = g.s * dX / w, gy = g.s * dY / w;
-  jr[0] = gx * u; jr[1] = gx * v; jr[2] = gy * u; jr[3] = gy * v; jr[4] = gx; jr[5] = gy;
-  const double gz = -(gx * xn + gy * yn);
-  jr[6] = gz * u; jr[7] = gz * v;
+  gx = g.s * dX / w;
+  gy = g.s * dY / w;
+  gz = -(gx * xn + gy * yn);
   return true;
 }
 
-// Centre + area constraint rows (reading Z10), unit-norm rows, into q[3][p].
+__device__ __forceinline__ void jraw_row(double gx, double gy, double gz, double u, double v, double (&jr)[8]) {
+  jr[0] = gx * u; jr[1] = gx * v; jr[2] = gy * u; jr[3] = gy * v; jr[4] = gx; jr[5] = gy;
+  jr[6] = gz * u; jr[7] = gz * v;
+}
+
+// Centre + area constraint rows (reading Z10), unit-norm rows, into q[3][8].
 __device__ __forceinline__ void constraint_rows(const double* tau, int kind, int m, int n, double* q) {
   const int p = kind == TILT_HOMOGRAPHY ? 8 : 6;
   const double h11 = tau[0], h12 = tau[1], h21 = tau[2], h22 = tau[3], h13 = tau[4], h23 = tau[5];
@@ -702,28 +477,171 @@ __device__ __forceinline__ void constraint_rows(const double* tau, int kind, int
   for (int e = 0; e < p; ++e) q[2 * 8 + e] = nrm > 0 ? ga[e] / nrm : 0.0;
 }
 
+// Cholesky of G (+ Q^T Q), L^{-1} (fp64, one thread). Returns false if G is not positive definite.
+__device__ __forceinline__ bool chol_inverse(const double* G36, const double* qrows, int l, int p, double* Li) {
+  double Gf[64], Lm[64];
+  int e = 0;
+  for (int a = 0; a < 8; ++a)
+    for (int b = a; b < 8; ++b) {
+      Gf[a * 8 + b] = G36[e];
+      Gf[b * 8 + a] = G36[e];
+      ++e;
+    }
+  for (int r = 0; r < l; ++r)
+    for (int a = 0; a < p; ++a)
+      for (int b = 0; b < p; ++b) Gf[a * 8 + b] += qrows[r * 8 + a] * qrows[r * 8 + b];
+  for (int a = 0; a < 64; ++a) { Lm[a] = 0.0; Li[a] = 0.0; }
+  double dmax = 0.0;
+  for (int a = 0; a < p; ++a) dmax = fmax(dmax, Gf[a * 8 + a]);
+  if (!(dmax > 0.0) || !isfinite(dmax)) return false;
+  for (int a = 0; a < p; ++a) {
+    double s = Gf[a * 8 + a];
+    for (int k = 0; k < a; ++k) s -= Lm[a * 8 + k] * Lm[a * 8 + k];
+    if (!(s > 1e-14 * dmax)) return false;
+    const double la = sqrt(s);
+    Lm[a * 8 + a] = la;
+    for (int b = a + 1; b < p; ++b) {
+      double t = Gf[b * 8 + a];
+      for (int k = 0; k < a; ++k) t -= Lm[b * 8 + k] * Lm[a * 8 + k];
+      Lm[b * 8 + a] = t / la;
+    }
+  }
+  for (int a = 0; a < p; ++a) {  // L^{-1} column by column (forward substitution)
+    Li[a * 8 + a] = 1.0 / Lm[a * 8 + a];
+    for (int b = a + 1; b < p; ++b) {
+      double s = 0.0;
+      for (int k = a; k < b; ++k) s += Lm[b * 8 + k] * Li[k * 8 + a];
+      Li[b * 8 + a] = -s / Lm[b * 8 + b];
+    }
+  }
+  return true;
+}
+
 // --------------------------------------------------------------------------------------------
-// Orthonormalise (K2): from D (raw d, fp32) and K planes holding J_raw (fp32) build
-//   D_hat = d/||d||, J = (J_raw - D_hat c^T)/||d||  (quotient rule) [if normalise]
-//   G = J^TJ + Q^TQ = L L^T (fp64), K = J L^{-T} (fp64 per pixel, stored fp32)
-// so that W^TW v = v - K K^T v (Eq. Jperpv, Eq. WTW_property).
-// Returns a tilt_patch_status (ZERO_PATCH / SINGULAR_GRAM / CONVERGED=ok).
+// Projectors W^T W v = v - K K^T v, K = J L^{-T} (Eq. Jperpv, Eq. WTW_property)
 // --------------------------------------------------------------------------------------------
-template <class C, int CH>
-__device__ __forceinline__ void gram_chunk(Ctx<C>& cx, bool normalise, double ind, const double (&c)[8],
-                                           double* Gout) {
-  // entries e in [12*CH, 12*CH+12) of the 8x8 upper triangle (row-major); q >= p columns are 0
-  const int mn = cx.mn, p = cx.p;
-  const float* __restrict__ Dp = cx.D;
-  const float* __restrict__ Kp = cx.K;
+// Implicit (TILT path): J = (J_raw - D_hat c^T)/||d|| with J_raw rows built per pixel from the
+// GX, GY, GZ planes and (u, v); K^T v = L' J_raw^T v - c' (D_hat^T v), L' = L^{-1}/||d||,
+// c' = L^{-1}c/||d||; K y = J_raw (L'^T y) - D_hat (c'^T y). No mn x p matrix is stored.
+struct ProjImplicit {
+  template <class C, class VF>
+  static __device__ __forceinline__ void reduce(Ctx<C>& cx, VF vf, float (&s)[8]) {
+    const int ld = cx.ld, pl = cx.pl;
+    const bool homog = cx.p == 8;
+    const float* __restrict__ GX = cx.G;
+    const float* __restrict__ GY = cx.G + pl;
+    const float* __restrict__ GZ = cx.G + 2 * pl;
+    const float* __restrict__ Dp = cx.D;
+    float a[10];
+#pragma unroll
+    for (int k = 0; k < 10; ++k) a[k] = 0.f;
+    for (PixIter pi(threadIdx.x, C::NT, ld); pi.idx < pl; pi.next(C::NT)) {
+      const int idx = pi.idx;
+      const float val = vf(idx);
+      const float u = ((float)pi.j - cx.cj) * cx.inv_s;
+      const float v = ((float)pi.i - cx.ci) * cx.inv_s;
+      const float ga = GX[idx] * val, gb = GY[idx] * val;
+      a[0] = fmaf(ga, u, a[0]);
+      a[1] = fmaf(ga, v, a[1]);
+      a[2] = fmaf(gb, u, a[2]);
+      a[3] = fmaf(gb, v, a[3]);
+      a[4] += ga;
+      a[5] += gb;
+      if (homog) {
+        const float gc = GZ[idx] * val;
+        a[6] = fmaf(gc, u, a[6]);
+        a[7] = fmaf(gc, v, a[7]);
+      }
+      a[8] = fmaf(Dp[idx], val, a[8]);
+    }
+    float r[9];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) r[k] = a[k];
+    block_sum_f<C, 9>(r, cx.sc);
+    // s = L' r[0:p] - c' r[8]  (K^T v)
+    const float* Lp = cx.sc->Lp;
+    const float* cp = cx.sc->cp;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      float acc = -cp[q] * r[8];
+#pragma unroll
+      for (int b = 0; b <= q; ++b) acc = fmaf(Lp[q * 8 + b], r[b], acc);
+      s[q] = acc;
+    }
+  }
+  // coefficients for apply: z = L'^T s (8), w = c'^T s
+  template <class C>
+  static __device__ __forceinline__ void coeffs(const Ctx<C>& cx, const float (&s)[8], float (&z)[9]) {
+    const float* Lp = cx.sc->Lp;
+    const float* cp = cx.sc->cp;
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+      float acc = 0.f;
+#pragma unroll
+      for (int q = b; q < 8; ++q) acc = fmaf(Lp[q * 8 + b], s[q], acc);
+      z[b] = acc;
+    }
+    float w = 0.f;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) w = fmaf(cp[q], s[q], w);
+    z[8] = w;
+  }
+  // (K y)(pixel) with y the K^T v of reduce(); z from coeffs()
+  template <class C>
+  static __device__ __forceinline__ float apply(const Ctx<C>& cx, int idx, int i, int j, const float (&z)[9]) {
+    const float u = ((float)j - cx.cj) * cx.inv_s;
+    const float v = ((float)i - cx.ci) * cx.inv_s;
+    float r = cx.G[idx] * fmaf(z[0], u, fmaf(z[1], v, z[4])) + cx.G[cx.pl + idx] * fmaf(z[2], u, fmaf(z[3], v, z[5]));
+    if (cx.p == 8) r = fmaf(cx.G[2 * cx.pl + idx], fmaf(z[6], u, z[7] * v), r);
+    return fmaf(-cx.D[idx], z[8], r);
+  }
+};
+
+// Explicit (generic J entries): K planes stored.
+struct ProjExplicit {
+  template <class C, class VF>
+  static __device__ __forceinline__ void reduce(Ctx<C>& cx, VF vf, float (&s)[8]) {
+    const int pl = cx.pl, p = cx.p;
+    const float* __restrict__ Kp = cx.G;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) s[q] = 0.f;
+    for (int idx = threadIdx.x; idx < pl; idx += C::NT) {
+      const float v = vf(idx);
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (q < p) s[q] = fmaf(Kp[q * pl + idx], v, s[q]);
+    }
+    block_sum_f<C, 8>(s, cx.sc);
+  }
+  template <class C>
+  static __device__ __forceinline__ void coeffs(const Ctx<C>&, const float (&s)[8], float (&z)[9]) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) z[q] = s[q];
+    z[8] = 0.f;
+  }
+  template <class C>
+  static __device__ __forceinline__ float apply(const Ctx<C>& cx, int idx, int, int, const float (&z)[9]) {
+    float r = 0.f;
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (q < cx.p) r = fmaf(cx.G[q * cx.pl + idx], z[q], r);
+    return r;
+  }
+};
+
+// --------------------------------------------------------------------------------------------
+// Orthonormalise (K2), implicit: from D (raw d) and GX, GY, GZ planes build ||d||, c = D_hat^T
+// J_raw, the Gram of J = (J_raw - D_hat c^T)/||d|| plus Q^T Q, its Cholesky L, and L', c' for
+// ProjImplicit; D is normalised in place (Alg. 1 Step 1). fp64 throughout.
+// --------------------------------------------------------------------------------------------
+template <class C, int CH, class RowF>
+__device__ __forceinline__ void gram_chunk(Ctx<C>& cx, RowF rowf, double* Gout) {
   double acc[12];
 #pragma unroll
   for (int e = 0; e < 12; ++e) acc[e] = 0.0;
-  for (int idx = threadIdx.x; idx < mn; idx += C::NT) {
-    const double dh = normalise ? Dp[idx] * ind : 0.0;
+  for (PixIter pi(threadIdx.x, C::NT, cx.ld); pi.idx < cx.pl; pi.next(C::NT)) {
     double jn[8];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) jn[q] = (q < p) ? ((double)Kp[q * mn + idx] - dh * c[q]) * ind : 0.0;
+    rowf(pi.idx, pi.i, pi.j, jn);
     int e = 0;
 #pragma unroll
     for (int a = 0; a < 8; ++a)
@@ -739,128 +657,103 @@ __device__ __forceinline__ void gram_chunk(Ctx<C>& cx, bool normalise, double in
 }
 
 template <class C>
-__device__ int orthonormalise(Ctx<C>& cx, bool normalise, const double* qrows, int l) {
+__device__ int orthonormalise_implicit(Ctx<C>& cx, const double* qrows, int l) {
   Scal* sc = cx.sc;
-  const int mn = cx.mn, p = cx.p;
+  const int p = cx.p, pl = cx.pl;
   float* __restrict__ Dp = cx.D;
-  float* __restrict__ Kp = cx.K;
-  double nd = 1.0;
-  double c[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  if (normalise) {
-    double acc[9];
+  const float* GX = cx.G;
+  const float* GY = cx.G + pl;
+  const float* GZ = cx.G + 2 * pl;
+  const bool homog = p == 8;
+  auto raw = [&](int idx, int i, int j, double (&jr)[8]) {
+    const double u = ((double)j - cx.cj) * cx.inv_s, v = ((double)i - cx.ci) * cx.inv_s;
+    jraw_row(GX[idx], GY[idx], homog ? (double)GZ[idx] : 0.0, u, v, jr);
+  };
+  double acc[9];
 #pragma unroll
-    for (int e = 0; e < 9; ++e) acc[e] = 0.0;
-    for (int idx = threadIdx.x; idx < mn; idx += C::NT) {
-      const double d = Dp[idx];
-      acc[8] = fma(d, d, acc[8]);
+  for (int e = 0; e < 9; ++e) acc[e] = 0.0;
+  for (PixIter pi(threadIdx.x, C::NT, cx.ld); pi.idx < pl; pi.next(C::NT)) {
+    const double d = Dp[pi.idx];
+    double jr[8];
+    raw(pi.idx, pi.i, pi.j, jr);
+    acc[8] = fma(d, d, acc[8]);
 #pragma unroll
-      for (int q = 0; q < 8; ++q)
-        if (q < p) acc[q] = fma((double)Kp[q * mn + idx], d, acc[q]);
-    }
-    block_sum_d<C, 9>(acc, sc);
-    nd = sqrt(acc[8]);
-    if (threadIdx.x == 0) sc->nd = (float)nd;
-    if (!(nd > 0.0)) return TILT_PATCH_ZERO_PATCH;
-#pragma unroll
-    for (int q = 0; q < 8; ++q) c[q] = acc[q] / nd;
+    for (int q = 0; q < 8; ++q) acc[q] = fma(jr[q], d, acc[q]);
   }
+  block_sum_d<C, 9>(acc, sc);
+  const double nd = sqrt(acc[8]);
+  if (threadIdx.x == 0) sc->nd = (float)nd;
+  if (!(nd > 0.0)) return TILT_PATCH_ZERO_PATCH;
   const double ind = 1.0 / nd;
+  double c[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) c[q] = acc[q] * ind;  // D_hat^T J_raw
+  auto rown = [&](int idx, int i, int j, double (&jn)[8]) {
+    double jr[8];
+    raw(idx, i, j, jr);
+    const double dh = Dp[idx] * ind;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) jn[q] = (q < p) ? (jr[q] - dh * c[q]) * ind : 0.0;
+  };
   double G[36];
-  gram_chunk<C, 0>(cx, normalise, ind, c, G);
-  gram_chunk<C, 1>(cx, normalise, ind, c, G);
-  gram_chunk<C, 2>(cx, normalise, ind, c, G);
+  gram_chunk<C, 0>(cx, rown, G);
+  gram_chunk<C, 1>(cx, rown, G);
+  gram_chunk<C, 2>(cx, rown, G);
   if (threadIdx.x == 0) {
-    // G (8x8 upper-triangle layout) + Q^T Q, Cholesky L L^T, then L^{-1}  (fp64, one thread)
-    double Gf[64];
-    int e = 0;
-    for (int a = 0; a < 8; ++a)
-      for (int b = a; b < 8; ++b) {
-        Gf[a * 8 + b] = G[e];
-        Gf[b * 8 + a] = G[e];
-        ++e;
-      }
-    for (int r = 0; r < l; ++r)
-      for (int a = 0; a < p; ++a)
-        for (int b = 0; b < p; ++b) Gf[a * 8 + b] += qrows[r * 8 + a] * qrows[r * 8 + b];
-    double* Lm = sc->L;
-    double* Li = sc->Linv;
-    for (int a = 0; a < 64; ++a) { Lm[a] = 0.0; Li[a] = 0.0; }
-    double dmax = 0.0;
-    for (int a = 0; a < p; ++a) dmax = fmax(dmax, Gf[a * 8 + a]);
-    bool ok = dmax > 0.0 && isfinite(dmax);
-    for (int a = 0; a < p && ok; ++a) {
-      double s = Gf[a * 8 + a];
-      for (int k = 0; k < a; ++k) s -= Lm[a * 8 + k] * Lm[a * 8 + k];
-      if (!(s > 1e-14 * dmax)) { ok = false; break; }
-      const double la = sqrt(s);
-      Lm[a * 8 + a] = la;
-      for (int b = a + 1; b < p; ++b) {
-        double t = Gf[b * 8 + a];
-        for (int k = 0; k < a; ++k) t -= Lm[b * 8 + k] * Lm[a * 8 + k];
-        Lm[b * 8 + a] = t / la;
-      }
-    }
-    if (ok) {
-      for (int a = 0; a < p; ++a) {  // L^{-1} column by column (forward substitution)
-        Li[a * 8 + a] = 1.0 / Lm[a * 8 + a];
-        for (int b = a + 1; b < p; ++b) {
-          double s = 0.0;
-          for (int k = a; k < b; ++k) s += Lm[b * 8 + k] * Li[k * 8 + a];
-          Li[b * 8 + a] = -s / Lm[b * 8 + b];
-        }
-      }
-    }
-    for (int q = 0; q < 8; ++q) sc->c[q] = c[q];
+    const bool ok = chol_inverse(G, qrows, l, p, sc->Linv);
     sc->flag = ok ? 1 : 0;
+    if (ok) {
+      for (int a = 0; a < 8; ++a) {
+        double cpa = 0.0;
+        for (int b = 0; b < 8; ++b) {
+          sc->Lp[a * 8 + b] = (float)(sc->Linv[a * 8 + b] * ind);
+          cpa += sc->Linv[a * 8 + b] * c[b];
+        }
+        sc->cp[a] = (float)(cpa * ind);
+      }
+    }
   }
   __syncthreads();
   if (!sc->flag) return TILT_PATCH_SINGULAR_GRAM;
-  // K = J L^{-T}: K[:, a] = sum_{b <= a} Linv[a][b] J[:, b]; D_hat stored fp32
+  for (int idx = threadIdx.x; idx < pl; idx += C::NT) Dp[idx] = (float)(Dp[idx] * ind);
+  __syncthreads();
+  return TILT_PATCH_CONVERGED;
+}
+
+// Explicit: K planes hold J (generic, already "normalised" as given); D untouched.
+template <class C>
+__device__ int orthonormalise_explicit(Ctx<C>& cx, const double* qrows, int l) {
+  Scal* sc = cx.sc;
+  const int p = cx.p, pl = cx.pl;
+  float* __restrict__ Kp = cx.G;
+  auto rowj = [&](int idx, int, int, double (&jn)[8]) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) jn[q] = (q < p) ? (double)Kp[q * pl + idx] : 0.0;
+  };
+  double G[36];
+  gram_chunk<C, 0>(cx, rowj, G);
+  gram_chunk<C, 1>(cx, rowj, G);
+  gram_chunk<C, 2>(cx, rowj, G);
+  if (threadIdx.x == 0) sc->flag = chol_inverse(G, qrows, l, p, sc->Linv) ? 1 : 0;
+  __syncthreads();
+  if (!sc->flag) return TILT_PATCH_SINGULAR_GRAM;
   const double* Li = sc->Linv;
-  for (int idx = threadIdx.x; idx < mn; idx += C::NT) {
-    const double dh = normalise ? Dp[idx] * ind : 0.0;
+  for (int idx = threadIdx.x; idx < pl; idx += C::NT) {
     double jn[8];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) jn[q] = (q < p) ? ((double)Kp[q * mn + idx] - dh * c[q]) * ind : 0.0;
+    for (int q = 0; q < 8; ++q) jn[q] = (q < p) ? (double)Kp[q * pl + idx] : 0.0;
 #pragma unroll
     for (int a = 0; a < 8; ++a) {
       if (a < p) {
         double s = 0.0;
 #pragma unroll
         for (int b = 0; b <= a; ++b) s = fma(Li[a * 8 + b], jn[b], s);
-        Kp[a * mn + idx] = (float)s;
+        Kp[a * pl + idx] = (float)s;
       }
     }
-    if (normalise) Dp[idx] = (float)dh;
   }
   __syncthreads();
   return TILT_PATCH_CONVERGED;
-}
-
-// s = K^T v for v(idx) given by a functor; result (p floats) returned in s (all threads).
-template <class C, class VF>
-__device__ __forceinline__ void kt_reduce(Ctx<C>& cx, VF vf, float (&s)[8]) {
-  const int mn = cx.mn, p = cx.p;
-  const float* __restrict__ Kp = cx.K;
-#pragma unroll
-  for (int q = 0; q < 8; ++q) s[q] = 0.f;
-  for (int idx = threadIdx.x; idx < mn; idx += C::NT) {
-    const float v = vf(idx);
-#pragma unroll
-    for (int q = 0; q < 8; ++q)
-      if (q < p) s[q] = fmaf(Kp[q * mn + idx], v, s[q]);
-  }
-  block_sum_f<C, 8>(s, cx.sc);
-}
-
-template <class C>
-__device__ __forceinline__ float k_apply(const Ctx<C>& cx, int idx, const float (&s)[8]) {
-  const int mn = cx.mn, p = cx.p;
-  float r = 0.f;
-#pragma unroll
-  for (int q = 0; q < 8; ++q)
-    if (q < p) r = fmaf(cx.K[q * mn + idx], s[q], r);
-  return r;
 }
 
 }  // namespace tilt

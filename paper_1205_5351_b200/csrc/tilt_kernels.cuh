@@ -7,23 +7,24 @@
 namespace tilt {
 
 // ---------------------------------------------------------------------------------------------
-// Shared-memory / workspace layout per size class
+// Shared-memory / workspace layout per size class. gplanes = 3 (implicit homography), 2 (implicit
+// affine) or p (explicit K).
 // ---------------------------------------------------------------------------------------------
 template <class C>
 struct Layout {
-  static __host__ __device__ size_t vec_floats() { return 3 * (size_t)C::MAXD; }
-  static __host__ __device__ size_t svd_floats() { return 3 * (size_t)C::MAXD * C::MAXD; }
-  static __host__ __device__ size_t plane_floats(int mn, int p) { return (size_t)(4 + p) * mn; }
-  static __host__ __device__ size_t smem_bytes(int mn, int p) {
+  static __host__ __device__ size_t vec_floats() { return 5 * (size_t)C::MAXD; }
+  static __host__ __device__ size_t svd_floats(int ld, int n) { return 3 * (size_t)ld * n; }
+  static __host__ __device__ size_t plane_floats(int ld, int n, int gplanes) { return (size_t)(4 + gplanes) * ld * n; }
+  static __host__ __device__ size_t smem_bytes(int ld, int n, int gplanes) {
     size_t s = vec_floats();
-    if (C::SVD_SMEM) s += svd_floats();
-    if (C::PLANES_SMEM) s += plane_floats(mn, p);
+    if (C::SVD_SMEM) s += svd_floats(ld, n);
+    if (C::PLANES_SMEM) s += plane_floats(ld, n, gplanes);
     return s * sizeof(float);
   }
-  static __host__ __device__ size_t ws_floats(int mn, int p) {
+  static __host__ __device__ size_t ws_floats(int ld, int n, int gplanes) {
     size_t s = 0;
-    if (!C::SVD_SMEM) s += svd_floats();
-    if (!C::PLANES_SMEM) s += plane_floats(mn, p);
+    if (!C::SVD_SMEM) s += svd_floats(ld, n);
+    if (!C::PLANES_SMEM) s += plane_floats(ld, n, gplanes);
     return (s + 31) & ~size_t(31);
   }
 };
@@ -31,25 +32,24 @@ struct Layout {
 template <class C>
 __device__ __forceinline__ Ctx<C> make_ctx(float* smem, float* ws, Scal* sc, int m, int n, int p) {
   Ctx<C> cx;
-  constexpr int MD = C::MAXD;
+  const int ld = ld_of<C>(m, n);
   float* sp = smem;
   float* gp = ws;
-  cx.nrm = sp;
-  cx.scl = sp + MD;
-  cx.hv = sp + 2 * MD;
-  sp += 3 * MD;
+  cx.ns = reinterpret_cast<float4*>(sp);
+  cx.hv = sp + 4 * C::MAXD;
+  sp += 5 * C::MAXD;
+  const int blk = ld * n;
   float* svd;
   if constexpr (C::SVD_SMEM) {
     svd = sp;
-    sp += 3 * MD * MD;
+    sp += 3 * blk;
   } else {
     svd = gp;
-    gp += 3 * MD * MD;
+    gp += 3 * blk;
   }
   cx.B = svd;
-  cx.V = svd + MD * MD;
-  cx.S = svd + 2 * MD * MD;
-  const int mn = m * n;
+  cx.V = svd + blk;
+  cx.S = svd + 2 * blk;
   float* pl;
   if constexpr (C::PLANES_SMEM) {
     pl = sp;
@@ -57,40 +57,39 @@ __device__ __forceinline__ Ctx<C> make_ctx(float* smem, float* ws, Scal* sc, int
     pl = gp;
   }
   cx.D = pl;
-  cx.A = pl + mn;
-  cx.E = pl + 2 * mn;
-  cx.Y = pl + 3 * mn;
-  cx.K = pl + 4 * mn;
+  cx.A = pl + blk;
+  cx.E = pl + 2 * blk;
+  cx.Y = pl + 3 * blk;
+  cx.G = pl + 4 * blk;
   cx.sc = sc;
   cx.m = m;
   cx.n = n;
   cx.p = p;
-  cx.mn = mn;
+  cx.ld = ld;
+  cx.pl = blk;
+  const float s = 0.5f * (float)max(m, n);
+  cx.inv_s = 1.f / s;
+  cx.ci = 0.5f * (float)(m - 1);
+  cx.cj = 0.5f * (float)(n - 1);
   return cx;
 }
 
 __host__ __device__ inline float default_jacobi_tol(int m) { return 8.f * sqrtf((float)m) * 5.9604645e-8f; }
 
+template <class C>
+__device__ __forceinline__ void zero_planes(float* X, size_t count) {
+  for (size_t e = threadIdx.x; e < count; e += C::NT) X[e] = 0.f;
+}
+
 // ---------------------------------------------------------------------------------------------
-// sigma_1(D_hat) for mu_0 (reading Z3): warm one-sided Jacobi on D_hat V; leaves V warm.
+// sigma_1 of a plane (mu_0 = mu0_scale / sigma_1(D_hat), reading Z3): warm Jacobi; leaves V warm.
 // ---------------------------------------------------------------------------------------------
 template <class C>
-__device__ float sigma1_of_plane(Ctx<C>& cx, const float* X, float tol, int max_sweeps, bool warm,
-                                 int* sweeps) {
-  constexpr int MD = C::MAXD;
-  const int m = cx.m, n = cx.n, mn = cx.mn;
-  for (PixIter pi(threadIdx.x, C::NT, m); pi.idx < mn; pi.next(C::NT)) cx.S[pi.j * MD + pi.i] = X[pi.idx];
-  if (!warm) set_identity<C>(cx.V, n);
-  __syncthreads();
-  gemm_nn<C>(cx.B, cx.S, cx.V, m, n, n);
-  bool capped;
-  *sweeps = jacobi_sweeps<C>(cx, n, tol, max_sweeps, &capped);
-  col_pass<C, 2>(cx, n, 0.f);  // sigma_j = ||b_j|| / ||v_j||
-  svt_stats<C>(cx, n, 0.f);
-  __syncthreads();
-  const float s1 = cx.sc->svt_sig1;
-  if (warm) ns_step<C>(cx, n);
-  return s1;
+__device__ float sigma1_of_plane(Ctx<C>& cx, const float* X, float tol, int max_sweeps, bool warm, int* sweeps) {
+  auto none = [](int, int, float4) {};
+  SvtOut so = svt<C, false>(cx, X, 0.f, tol, max_sweeps, warm, none, warm);
+  *sweeps = so.sweeps;
+  return cx.sc->svt_sig1;
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -109,11 +108,10 @@ struct InnerOut {
   bool converged;
 };
 
-template <class C>
-__device__ InnerOut ladmap_inner(Ctx<C>& cx, const DevParams& P, float lam, float mu0, float mu_max,
-                                 float denom, float tol, const uint8_t* replay, float* trace) {
-  constexpr int MD = C::MAXD;
-  const int m = cx.m, n = cx.n, mn = cx.mn;
+template <class C, class PR>
+__device__ InnerOut ladmap_inner(Ctx<C>& cx, const DevParams& P, float lam, float mu0, float mu_max, float denom,
+                                 float tol, const uint8_t* replay, float* trace) {
+  const int ld = cx.ld, pl = cx.pl;
   const float inv_den = 1.f / denom;
   const int niter = P.fixed_inner > 0 ? P.fixed_inner : P.max_inner;
   float* __restrict__ Ap = cx.A;
@@ -128,29 +126,38 @@ __device__ InnerOut ladmap_inner(Ctx<C>& cx, const DevParams& P, float lam, floa
   o.converged = false;
   float mu = mu0;
   o.mu = mu;
+  const bool warm = P.svd_warm != 0;
+  auto vres = [&](int idx) { return Ap[idx] + Ep[idx] - Dp[idx]; };
   for (int k = 0; k < niter; ++k) {
-    // ---- A step: A_{k+1} = S_{1/mu}(M_k), M_k in S --------------------------------------
+    // ---- A step: A_{k+1} = S_{1/mu}(M_k), M_k in S ------------------------------------------
     float dA2 = 0.f;
-    SvtOut so = svt<C, true>(cx, m, n, 1.f / mu, tol, P.jacobi_max_sweeps, P.svd_warm != 0,
-                             [&](int i, int j, float a) {
-                               const int idx = j * m + i;
-                               const float d = a - Ap[idx];
-                               dA2 = fmaf(d, d, dA2);
-                               Ap[idx] = a;
-                             },
-                             P.svd_warm != 0);
+    SvtOut so = svt<C, true>(
+        cx, cx.S, 1.f / mu, tol, P.jacobi_max_sweeps, warm,
+        [&](int i0, int j, float4 a) {
+          float* ap = Ap + j * ld + i0;
+          const float4 o4 = *reinterpret_cast<const float4*>(ap);
+          float d;
+          d = a.x - o4.x; dA2 = fmaf(d, d, dA2);
+          d = a.y - o4.y; dA2 = fmaf(d, d, dA2);
+          d = a.z - o4.z; dA2 = fmaf(d, d, dA2);
+          d = a.w - o4.w; dA2 = fmaf(d, d, dA2);
+          *reinterpret_cast<float4*>(ap) = a;
+        },
+        warm);
     o.sweeps += so.sweeps;
     o.caps += so.capped ? 1 : 0;
     // ---- E step ---------------------------------------------------------------------------
     const float inv_mu = 1.f / mu;
     const float thr = lam * inv_mu;
-    float s[8];
-    kt_reduce<C>(cx, [&](int idx) { return Ap[idx] + Ep[idx] - Dp[idx]; }, s);
+    float s[8], z[9];
+    PR::reduce(cx, vres, s);
+    PR::coeffs(cx, s, z);
     float dE2 = 0.f;
-    for (int idx = threadIdx.x; idx < mn; idx += C::NT) {
+    for (PixIter pi(threadIdx.x, C::NT, ld); pi.idx < pl; pi.next(C::NT)) {
+      const int idx = pi.idx;
       const float e = Ep[idx];
       const float v = Ap[idx] + e - Dp[idx];
-      const float pv = v - k_apply<C>(cx, idx, s);
+      const float pv = v - PR::apply(cx, idx, pi.i, pi.j, z);
       const float nk = e - pv - Yp[idx] * inv_mu;
       const float en = copysignf(fmaxf(fabsf(nk) - thr, 0.f), nk);
       const float d = en - e;
@@ -161,21 +168,22 @@ __device__ InnerOut ladmap_inner(Ctx<C>& cx, const DevParams& P, float lam, floa
     block_sum_f<C, 2>(dd, cx.sc);
     const float crit2 = mu * sqrtf(fmaxf(dd[0], dd[1])) * inv_den;
     int rho_bit = crit2 < P.eps2 ? 1 : 0;
-    if (replay) rho_bit = replay[k] ? 1 : 0;
+    if (replay) rho_bit = replay[k] & 1;  // parity protocol (Z21): bit 0 = rho decision
     const float mu_next = fminf(mu_max, rho_bit ? P.rho0 * mu : mu);
     const float inv_mun = 1.f / mu_next;
     // ---- dual step + next M ----------------------------------------------------------------
-    kt_reduce<C>(cx, [&](int idx) { return Ap[idx] + Ep[idx] - Dp[idx]; }, s);
+    PR::reduce(cx, vres, s);
+    PR::coeffs(cx, s, z);
     float c1 = 0.f;
-    for (PixIter pi(threadIdx.x, C::NT, m); pi.idx < mn; pi.next(C::NT)) {
+    for (PixIter pi(threadIdx.x, C::NT, ld); pi.idx < pl; pi.next(C::NT)) {
       const int idx = pi.idx;
       const float a = Ap[idx];
       const float v = a + Ep[idx] - Dp[idx];
-      const float r = v - k_apply<C>(cx, idx, s);
+      const float r = v - PR::apply(cx, idx, pi.i, pi.j, z);
       const float y = fmaf(mu, r, Yp[idx]);
       Yp[idx] = y;
       c1 = fmaf(r, r, c1);
-      cx.S[pi.j * MD + pi.i] = a - r - y * inv_mun;
+      cx.S[idx] = a - r - y * inv_mun;
     }
     float cc[1] = {c1};
     block_sum_f<C, 1>(cc, cx.sc);
@@ -190,7 +198,8 @@ __device__ InnerOut ladmap_inner(Ctx<C>& cx, const DevParams& P, float lam, floa
     o.crit1 = crit1;
     o.crit2 = crit2;
     o.mu = mu;
-    const bool stop = crit1 < P.eps1 && crit2 < P.eps2;
+    bool stop = crit1 < P.eps1 && crit2 < P.eps2;
+    if (replay) stop = (replay[k] & 2) != 0;  // bit 1 = the replayed run's inner loop ended here
     if (stop) o.converged = true;
     if (stop && P.fixed_inner <= 0) break;
     mu = mu_next;
@@ -198,23 +207,26 @@ __device__ InnerOut ladmap_inner(Ctx<C>& cx, const DevParams& P, float lam, floa
   return o;
 }
 
-// W^TW applied in place to a plane X (X <- X - K K^T X).
-template <class C>
+// X <- W^TW X (in place)
+template <class C, class PR>
 __device__ __forceinline__ void project_plane(Ctx<C>& cx, float* X) {
-  float s[8];
-  kt_reduce<C>(cx, [&](int idx) { return X[idx]; }, s);
-  for (int idx = threadIdx.x; idx < cx.mn; idx += C::NT) X[idx] -= k_apply<C>(cx, idx, s);
+  float s[8], z[9];
+  PR::reduce(cx, [&](int idx) { return X[idx]; }, s);
+  PR::coeffs(cx, s, z);
+  for (PixIter pi(threadIdx.x, C::NT, cx.ld); pi.idx < cx.pl; pi.next(C::NT))
+    X[pi.idx] -= PR::apply(cx, pi.idx, pi.i, pi.j, z);
   __syncthreads();
 }
 
 // ||W^TW X||_F
-template <class C>
+template <class C, class PR>
 __device__ __forceinline__ float proj_norm(Ctx<C>& cx, const float* X) {
-  float s[8];
-  kt_reduce<C>(cx, [&](int idx) { return X[idx]; }, s);
+  float s[8], z[9];
+  PR::reduce(cx, [&](int idx) { return X[idx]; }, s);
+  PR::coeffs(cx, s, z);
   float acc = 0.f;
-  for (int idx = threadIdx.x; idx < cx.mn; idx += C::NT) {
-    const float r = X[idx] - k_apply<C>(cx, idx, s);
+  for (PixIter pi(threadIdx.x, C::NT, cx.ld); pi.idx < cx.pl; pi.next(C::NT)) {
+    const float r = X[pi.idx] - PR::apply(cx, pi.idx, pi.i, pi.j, z);
     acc = fmaf(r, r, acc);
   }
   float a1[1] = {acc};
@@ -223,20 +235,20 @@ __device__ __forceinline__ float proj_norm(Ctx<C>& cx, const float* X) {
 }
 
 // Prologue of an inner loop: R_0 = W^TW(A + E - D), M_0 = A - R_0 - Y/mu0 into S.
-template <class C>
+template <class C, class PR>
 __device__ __forceinline__ void write_m0(Ctx<C>& cx, float mu0) {
-  constexpr int MD = C::MAXD;
-  float s[8];
+  float s[8], z[9];
   const float* Ap = cx.A;
   const float* Ep = cx.E;
   const float* Dp = cx.D;
-  kt_reduce<C>(cx, [&](int idx) { return Ap[idx] + Ep[idx] - Dp[idx]; }, s);
+  PR::reduce(cx, [&](int idx) { return Ap[idx] + Ep[idx] - Dp[idx]; }, s);
+  PR::coeffs(cx, s, z);
   const float inv = 1.f / mu0;
-  for (PixIter pi(threadIdx.x, C::NT, cx.m); pi.idx < cx.mn; pi.next(C::NT)) {
+  for (PixIter pi(threadIdx.x, C::NT, cx.ld); pi.idx < cx.pl; pi.next(C::NT)) {
     const int idx = pi.idx;
     const float v = Ap[idx] + Ep[idx] - Dp[idx];
-    const float r = v - k_apply<C>(cx, idx, s);
-    cx.S[pi.j * MD + pi.i] = Ap[idx] - r - cx.Y[idx] * inv;
+    const float r = v - PR::apply(cx, idx, pi.i, pi.j, z);
+    cx.S[idx] = Ap[idx] - r - cx.Y[idx] * inv;
   }
   __syncthreads();
 }
@@ -244,27 +256,27 @@ __device__ __forceinline__ void write_m0(Ctx<C>& cx, float mu0) {
 template <class C>
 __device__ __forceinline__ float plane_l1(Ctx<C>& cx, const float* X) {
   float acc = 0.f;
-  for (int idx = threadIdx.x; idx < cx.mn; idx += C::NT) acc += fabsf(X[idx]);
+  for (int idx = threadIdx.x; idx < cx.pl; idx += C::NT) acc += fabsf(X[idx]);
   float a1[1] = {acc};
   block_sum_f<C, 1>(a1, cx.sc);
   return a1[0];
 }
 
-// Column-major plane -> row-major global [m][n]
+// Column-major padded plane -> row-major global [m][n]
 template <class C>
-__device__ __forceinline__ void store_plane(float* __restrict__ out, const float* X, int m, int n, bool zero) {
+__device__ __forceinline__ void store_plane(float* __restrict__ out, const float* X, int m, int n, int ld, bool zero) {
   for (int o = threadIdx.x; o < m * n; o += C::NT) {
     const int i = o / n, j = o - i * n;
-    out[o] = zero ? 0.f : X[j * m + i];
+    out[o] = zero ? 0.f : X[j * ld + i];
   }
 }
 
-// Row-major global [m][n] -> column-major plane
+// Row-major global [m][n] -> column-major padded plane (padding rows set to 0)
 template <class C>
-__device__ __forceinline__ void load_plane(float* X, const float* __restrict__ in, int m, int n) {
-  for (int o = threadIdx.x; o < m * n; o += C::NT) {
-    const int i = o / n, j = o - i * n;
-    X[j * m + i] = in[o];
+__device__ __forceinline__ void load_plane(float* X, const float* __restrict__ in, int m, int n, int ld) {
+  for (int e = threadIdx.x; e < ld * n; e += C::NT) {
+    const int j = e / ld, i = e - j * ld;
+    X[e] = (i < m) ? in[i * n + j] : 0.f;
   }
 }
 
@@ -292,8 +304,9 @@ struct SolveArgs {
 
 template <class C>
 __device__ void solve_patch(const SolveArgs& a, Ctx<C>& cx, int b) {
+  using PR = ProjImplicit;
   const DevParams& P = a.P;
-  const int m = a.m, n = a.n, p = a.p, mn = m * n;
+  const int m = a.m, n = a.n, p = a.p, ld = cx.ld, pl = cx.pl;
   const int bx[4] = {a.boxes[4 * b], a.boxes[4 * b + 1], a.boxes[4 * b + 2], a.boxes[4 * b + 3]};
   const float* img = a.images + (size_t)a.patch_image[b] * a.H * a.W;
   double tau[8];
@@ -308,7 +321,9 @@ __device__ void solve_patch(const SolveArgs& a, Ctx<C>& cx, int b) {
   const float lam = P.lambda > 0.f ? P.lambda : rsqrtf((float)max(m, n));
   const float tol = P.jacobi_tol > 0.f ? P.jacobi_tol : default_jacobi_tol(m);
   const bool warm = P.svd_warm != 0;
-  set_identity<C>(cx.V, n);
+  const int gpl = p == 8 ? 3 : 2;
+  zero_planes<C>(cx.D, (size_t)(4 + gpl) * pl);  // padding rows stay 0 from here on
+  set_identity<C>(cx.V, ld, n);
   __syncthreads();
   int status = TILT_PATCH_MAX_OUTER, stop_rule = 0, outer = 0, inner_total = 0, sweeps_total = 0,
       aux_total = 0, caps = 0, rank = 0, band = 0, svt_rank = 0;
@@ -317,16 +332,17 @@ __device__ void solve_patch(const SolveArgs& a, Ctx<C>& cx, int b) {
   bool have_state = false, have_fprev = false;
   const int n_outer = P.fixed_outer > 0 ? P.fixed_outer : P.max_outer;
   for (int it = 0; it < n_outer; ++it) {
-    // Step 1: D o tau and J_raw (fp64 per pixel, stored fp32), window-escape check
+    // Step 1: D o tau and the Jacobian factors (fp64 per pixel, stored fp32), escape check
     const WarpGeom g = make_geom(bx, tau, a.kind);
     bool esc = false;
-    for (PixIter pi(threadIdx.x, C::NT, m); pi.idx < mn; pi.next(C::NT)) {
-      double d, jr[8];
-      if (!warp_pixel(g, img, a.H, a.W, pi.i, pi.j, d, jr)) esc = true;
+    for (PixIter pi(threadIdx.x, C::NT, ld); pi.idx < pl; pi.next(C::NT)) {
+      if (pi.i >= m) continue;
+      double d, gx, gy, gz;
+      if (!warp_pixel(g, img, a.H, a.W, pi.i, pi.j, d, gx, gy, gz)) esc = true;
       cx.D[pi.idx] = (float)d;
-#pragma unroll
-      for (int q = 0; q < 8; ++q)
-        if (q < p) cx.K[q * mn + pi.idx] = (float)jr[q];
+      cx.G[pi.idx] = (float)gx;
+      cx.G[pl + pi.idx] = (float)gy;
+      if (p == 8) cx.G[2 * pl + pi.idx] = (float)gz;
     }
     if (__syncthreads_or(esc)) {
       status = TILT_PATCH_WINDOW_ESCAPE;
@@ -338,7 +354,7 @@ __device__ void solve_patch(const SolveArgs& a, Ctx<C>& cx, int b) {
       constraint_rows(tau, a.kind, m, n, qr);
       l = 3;
     }
-    const int st = orthonormalise<C>(cx, true, qr, l);
+    const int st = orthonormalise_implicit<C>(cx, qr, l);
     nd = cx.sc->nd;
     if (st != TILT_PATCH_CONVERGED) {
       status = st;
@@ -346,27 +362,27 @@ __device__ void solve_patch(const SolveArgs& a, Ctx<C>& cx, int b) {
     }
     // Step 2 warm start (Eq. warm_start; Eq. Y_new_warmstart; Z4)
     if (!have_state || !P.vws) {
-      for (int idx = threadIdx.x; idx < mn; idx += C::NT) {
+      for (int idx = threadIdx.x; idx < pl; idx += C::NT) {
         cx.A[idx] = cx.D[idx];
         cx.E[idx] = 0.f;
         cx.Y[idx] = 0.f;
       }
       __syncthreads();
     } else {
-      project_plane<C>(cx, cx.Y);
+      project_plane<C, PR>(cx, cx.Y);
     }
-    const float denom0 = proj_norm<C>(cx, cx.D);
+    const float denom0 = proj_norm<C, PR>(cx, cx.D);
     const float denom = denom0 > 0.f ? denom0 : 1.f;
     int aux = 0;
     const float s1 = sigma1_of_plane<C>(cx, cx.D, tol, P.jacobi_max_sweeps, warm, &aux);
     aux_total += aux;
     const float mu0 = s1 > 0.f ? P.mu0_scale / s1 : P.mu0_scale;
     const float mu_max = P.mu_max_ratio * mu0;
-    write_m0<C>(cx, mu0);
+    write_m0<C, PR>(cx, mu0);
     const size_t toff = ((size_t)b * P.max_outer + it) * P.max_inner;
-    const InnerOut io = ladmap_inner<C>(cx, P, lam, mu0, mu_max, denom, tol,
-                                        P.rho_replay ? P.rho_replay + toff : nullptr,
-                                        P.trace ? P.trace + 4 * toff : nullptr);
+    const InnerOut io = ladmap_inner<C, PR>(cx, P, lam, mu0, mu_max, denom, tol,
+                                            P.rho_replay ? P.rho_replay + toff : nullptr,
+                                            P.trace ? P.trace + 4 * toff : nullptr);
     have_state = true;
     inner_total += io.iters;
     sweeps_total += io.sweeps;
@@ -380,7 +396,7 @@ __device__ void solve_patch(const SolveArgs& a, Ctx<C>& cx, int b) {
     svt_rank = cx.sc->svt_rank;
     // Step 3: dtau = G^{-1} J^T (A + E - D_hat) = L^{-T} K^T (A + E - D_hat)  (Eq. Delta_tau)
     float s[8];
-    kt_reduce<C>(cx, [&](int idx) { return cx.A[idx] + cx.E[idx] - cx.D[idx]; }, s);
+    PR::reduce(cx, [&](int idx) { return cx.A[idx] + cx.E[idx] - cx.D[idx]; }, s);
     const float l1 = plane_l1<C>(cx, cx.E);
     const double* Li = cx.sc->Linv;
     double dt_inf = 0.0;
@@ -416,9 +432,9 @@ __device__ void solve_patch(const SolveArgs& a, Ctx<C>& cx, int b) {
   }
   __syncthreads();
   // outputs
-  if (a.A_out) store_plane<C>(a.A_out + (size_t)b * mn, cx.A, m, n, !have_state);
-  if (a.E_out) store_plane<C>(a.E_out + (size_t)b * mn, cx.E, m, n, !have_state);
-  if (a.Y_out) store_plane<C>(a.Y_out + (size_t)b * mn, cx.Y, m, n, !have_state);
+  if (a.A_out) store_plane<C>(a.A_out + (size_t)b * m * n, cx.A, m, n, ld, !have_state);
+  if (a.E_out) store_plane<C>(a.E_out + (size_t)b * m * n, cx.E, m, n, ld, !have_state);
+  if (a.Y_out) store_plane<C>(a.Y_out + (size_t)b * m * n, cx.Y, m, n, ld, !have_state);
   if (threadIdx.x == 0) {
     for (int q = 0; q < p; ++q) a.tau_out[b * p + q] = (float)tau[q];
     if (a.rep) {
@@ -470,7 +486,7 @@ __global__ void __launch_bounds__(C::NT, C::MINB) k_solve(SolveArgs a) {
 }
 
 // ---------------------------------------------------------------------------------------------
-// Inner loop only (Table 1 setting)
+// Inner loop only (Table 1 setting): explicit projector from a given J
 // ---------------------------------------------------------------------------------------------
 struct InnerArgs {
   const float* D;
@@ -487,45 +503,46 @@ struct InnerArgs {
 };
 
 template <class C>
-__global__ void __launch_bounds__(C::NT, C::MINB) k_inner(InnerArgs a) {
+__global__ void __launch_bounds__(C::NT, 1) k_inner(InnerArgs a) {
+  using PR = ProjExplicit;
   extern __shared__ float4 dsm4[];
   __shared__ Scal sc;
   float* ws = a.ws ? a.ws + (size_t)blockIdx.x * a.ws_stride : nullptr;
   Ctx<C> cx = make_ctx<C>(reinterpret_cast<float*>(dsm4), ws, &sc, a.m, a.n, a.p);
   const DevParams& P = a.P;
-  const int m = a.m, n = a.n, p = a.p, mn = m * n;
+  const int m = a.m, n = a.n, p = a.p, ld = cx.ld, pl = cx.pl;
   const float lam = P.lambda > 0.f ? P.lambda : rsqrtf((float)max(m, n));
   const float tol = P.jacobi_tol > 0.f ? P.jacobi_tol : default_jacobi_tol(m);
   for (int b = blockIdx.x; b < a.B; b += gridDim.x) {
-    load_plane<C>(cx.D, a.D + (size_t)b * mn, m, n);
-    for (int q = 0; q < p; ++q) load_plane<C>(cx.K + (size_t)q * mn, a.J + ((size_t)b * p + q) * mn, m, n);
+    load_plane<C>(cx.D, a.D + (size_t)b * m * n, m, n, ld);
+    for (int q = 0; q < p; ++q) load_plane<C>(cx.G + (size_t)q * pl, a.J + ((size_t)b * p + q) * m * n, m, n, ld);
     __syncthreads();
     double qr[24];
     for (int e = 0; e < 24; ++e) qr[e] = 0.0;
     if (a.Q)
       for (int r = 0; r < a.l; ++r)
         for (int q = 0; q < p; ++q) qr[r * 8 + q] = a.Q[((size_t)b * a.l + r) * p + q];
-    const int st = orthonormalise<C>(cx, false, qr, a.Q ? a.l : 0);
+    const int st = orthonormalise_explicit<C>(cx, qr, a.Q ? a.l : 0);
     tilt_report rr;
     memset(&rr, 0, sizeof(rr));
     rr.status = st;
     if (st == TILT_PATCH_CONVERGED) {
-      for (int idx = threadIdx.x; idx < mn; idx += C::NT) {
+      for (int idx = threadIdx.x; idx < pl; idx += C::NT) {
         cx.A[idx] = cx.D[idx];
         cx.E[idx] = 0.f;
         cx.Y[idx] = 0.f;
       }
-      set_identity<C>(cx.V, n);
+      set_identity<C>(cx.V, ld, n);
       __syncthreads();
-      const float denom0 = proj_norm<C>(cx, cx.D);
+      const float denom0 = proj_norm<C, PR>(cx, cx.D);
       const float denom = denom0 > 0.f ? denom0 : 1.f;
       int aux = 0;
       const float s1 = sigma1_of_plane<C>(cx, cx.D, tol, P.jacobi_max_sweeps, P.svd_warm != 0, &aux);
       const float mu0 = s1 > 0.f ? P.mu0_scale / s1 : P.mu0_scale;
-      write_m0<C>(cx, mu0);
-      const InnerOut io = ladmap_inner<C>(cx, P, lam, mu0, P.mu_max_ratio * mu0, denom, tol,
-                                          P.rho_replay ? P.rho_replay + (size_t)b * P.max_inner : nullptr,
-                                          P.trace ? P.trace + (size_t)4 * b * P.max_inner : nullptr);
+      write_m0<C, PR>(cx, mu0);
+      const InnerOut io = ladmap_inner<C, PR>(cx, P, lam, mu0, P.mu_max_ratio * mu0, denom, tol,
+                                              P.rho_replay ? P.rho_replay + (size_t)b * P.max_inner : nullptr,
+                                              P.trace ? P.trace + (size_t)4 * b * P.max_inner : nullptr);
       const float nuc = cx.sc->svt_nuc;
       rr.rank = cx.sc->svt_relrank;
       rr.rank_band = cx.sc->svt_band;
@@ -545,9 +562,9 @@ __global__ void __launch_bounds__(C::NT, C::MINB) k_inner(InnerArgs a) {
     }
     __syncthreads();
     const bool z = st != TILT_PATCH_CONVERGED;
-    store_plane<C>(a.A + (size_t)b * mn, cx.A, m, n, z);
-    store_plane<C>(a.E + (size_t)b * mn, cx.E, m, n, z);
-    if (a.Y) store_plane<C>(a.Y + (size_t)b * mn, cx.Y, m, n, z);
+    store_plane<C>(a.A + (size_t)b * m * n, cx.A, m, n, ld, z);
+    store_plane<C>(a.E + (size_t)b * m * n, cx.E, m, n, ld, z);
+    if (a.Y) store_plane<C>(a.Y + (size_t)b * m * n, cx.Y, m, n, ld, z);
     if (a.rep && threadIdx.x == 0) a.rep[b] = rr;
     __syncthreads();
   }
@@ -571,47 +588,39 @@ struct SvtArgs {
 };
 
 template <class C>
-__global__ void __launch_bounds__(C::NT, C::MINB) k_svt(SvtArgs a) {
+__global__ void __launch_bounds__(C::NT, 1) k_svt(SvtArgs a) {
   extern __shared__ float4 dsm4[];
   __shared__ Scal sc;
-  constexpr int MD = C::MAXD;
   float* ws = a.ws ? a.ws + (size_t)blockIdx.x * a.ws_stride : nullptr;
   Ctx<C> cx = make_ctx<C>(reinterpret_cast<float*>(dsm4), ws, &sc, a.m, a.n, 0);
-  const int m = a.m, n = a.n, mn = m * n;
+  const int m = a.m, n = a.n, mn = m * n, ld = cx.ld;
   for (int b = blockIdx.x; b < a.B; b += gridDim.x) {
-    zero_buf<C>(cx.S);
-    zero_buf<C>(cx.V);
-    __syncthreads();
-    for (int o = threadIdx.x; o < mn; o += C::NT) {
-      const int i = o / n, j = o - i * n;
-      cx.S[j * MD + i] = a.M[(size_t)b * mn + o];
-    }
+    load_plane<C>(cx.S, a.M + (size_t)b * mn, m, n, ld);
     if (a.V_io) {
-      for (int o = threadIdx.x; o < n * n; o += C::NT) {
-        const int i = o / n, j = o - i * n;
-        cx.V[j * MD + i] = a.V_io[(size_t)b * n * n + o];
-      }
+      load_plane<C>(cx.V, a.V_io + (size_t)b * n * n, n, n, ld);
     } else {
-      set_identity<C>(cx.V, n);
+      set_identity<C>(cx.V, ld, n);
     }
     __syncthreads();
     float* Ab = a.A + (size_t)b * mn;
-    SvtOut so = svt<C, true>(cx, m, n, a.eps[b], a.tol, a.max_sweeps, true,
-                             [&](int i, int j, float v) { Ab[i * n + j] = v; }, false);
+    SvtOut so = svt<C, true>(
+        cx, cx.S, a.eps[b], a.tol, a.max_sweeps, true,
+        [&](int i0, int j, float4 v) {
+          const float vv[4] = {v.x, v.y, v.z, v.w};
+          for (int r = 0; r < 4; ++r)
+            if (i0 + r < m) Ab[(i0 + r) * n + j] = vv[r];
+        },
+        false);
     if (a.sigma)
-      for (int j = threadIdx.x; j < n; j += C::NT) a.sigma[(size_t)b * n + j] = sqrtf(cx.nrm[j]);
-    if (a.V_io)
-      for (int o = threadIdx.x; o < n * n; o += C::NT) {
-        const int i = o / n, j = o - i * n;
-        a.V_io[(size_t)b * n * n + o] = cx.V[j * MD + i];
-      }
+      for (int j = threadIdx.x; j < n; j += C::NT) a.sigma[(size_t)b * n + j] = sqrtf(cx.ns[j].x);
+    if (a.V_io) store_plane<C>(a.V_io + (size_t)b * n * n, cx.V, n, n, ld, false);
     if (a.sweeps && threadIdx.x == 0) a.sweeps[b] = so.sweeps;
     __syncthreads();
   }
 }
 
 // ---------------------------------------------------------------------------------------------
-// Standalone projector (K2 parity): W^TW v and G^{-1} J^T v
+// Standalone projector (K2 parity): W^TW v and G^{-1} J^T v (explicit K from a given J)
 // ---------------------------------------------------------------------------------------------
 struct ProjArgs {
   const float* J;
@@ -627,26 +636,28 @@ struct ProjArgs {
 };
 
 template <class C>
-__global__ void __launch_bounds__(C::NT, C::MINB) k_project(ProjArgs a) {
+__global__ void __launch_bounds__(C::NT, 1) k_project(ProjArgs a) {
+  using PR = ProjExplicit;
   extern __shared__ float4 dsm4[];
   __shared__ Scal sc;
   float* ws = a.ws ? a.ws + (size_t)blockIdx.x * a.ws_stride : nullptr;
   Ctx<C> cx = make_ctx<C>(reinterpret_cast<float*>(dsm4), ws, &sc, a.m, a.n, a.p);
-  const int m = a.m, n = a.n, p = a.p, mn = m * n;
+  const int m = a.m, n = a.n, p = a.p, mn = m * n, ld = cx.ld, pl = cx.pl;
   for (int b = blockIdx.x; b < a.B; b += gridDim.x) {
-    for (int q = 0; q < p; ++q) load_plane<C>(cx.K + (size_t)q * mn, a.J + ((size_t)b * p + q) * mn, m, n);
-    load_plane<C>(cx.A, a.v + (size_t)b * mn, m, n);
+    for (int q = 0; q < p; ++q) load_plane<C>(cx.G + (size_t)q * pl, a.J + ((size_t)b * p + q) * mn, m, n, ld);
+    load_plane<C>(cx.A, a.v + (size_t)b * mn, m, n, ld);
     __syncthreads();
     double qr[24];
     for (int e = 0; e < 24; ++e) qr[e] = 0.0;
     if (a.Q)
       for (int r = 0; r < a.l; ++r)
         for (int q = 0; q < p; ++q) qr[r * 8 + q] = a.Q[((size_t)b * a.l + r) * p + q];
-    const int st = orthonormalise<C>(cx, false, qr, a.Q ? a.l : 0);
+    const int st = orthonormalise_explicit<C>(cx, qr, a.Q ? a.l : 0);
     if (st == TILT_PATCH_CONVERGED) {
-      float s[8];
-      kt_reduce<C>(cx, [&](int idx) { return cx.A[idx]; }, s);
-      for (int idx = threadIdx.x; idx < mn; idx += C::NT) cx.E[idx] = cx.A[idx] - k_apply<C>(cx, idx, s);
+      float s[8], z[9];
+      PR::reduce(cx, [&](int idx) { return cx.A[idx]; }, s);
+      PR::coeffs(cx, s, z);
+      for (int idx = threadIdx.x; idx < pl; idx += C::NT) cx.E[idx] = cx.A[idx] - PR::apply(cx, idx, 0, 0, z);
       if (a.dtau && threadIdx.x == 0) {
         const double* Li = cx.sc->Linv;
         for (int q = 0; q < p; ++q) {
@@ -657,7 +668,7 @@ __global__ void __launch_bounds__(C::NT, C::MINB) k_project(ProjArgs a) {
       }
       __syncthreads();
     }
-    store_plane<C>(a.Pv + (size_t)b * mn, cx.E, m, n, st != TILT_PATCH_CONVERGED);
+    store_plane<C>(a.Pv + (size_t)b * mn, cx.E, m, n, ld, st != TILT_PATCH_CONVERGED);
     if (a.status && threadIdx.x == 0) a.status[b] = st;
     __syncthreads();
   }
@@ -693,12 +704,14 @@ __global__ void __launch_bounds__(K1_NT) k_warp(WarpArgs a) {
   for (int q = 0; q < p; ++q) tau[q] = a.tau[b * p + q];
   const WarpGeom g = make_geom(bx, tau, a.kind);
   const float* img = a.images + (size_t)a.patch_image[b] * a.H * a.W;
+  const double inv_s = 1.0 / g.s;
   double acc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
   bool esc = false;
   for (int o = threadIdx.x; o < mn; o += K1_NT) {
     const int i = o / n, j = o - i * n;
-    double d, jr[8];
-    if (!warp_pixel(g, img, a.H, a.W, i, j, d, jr)) esc = true;
+    double d, gx, gy, gz, jr[8];
+    if (!warp_pixel(g, img, a.H, a.W, i, j, d, gx, gy, gz)) esc = true;
+    jraw_row(gx, gy, gz, (j - 0.5 * (n - 1)) * inv_s, (i - 0.5 * (m - 1)) * inv_s, jr);
     acc[8] = fma(d, d, acc[8]);
 #pragma unroll
     for (int q = 0; q < 8; ++q) acc[q] = fma(jr[q], d, acc[q]);
@@ -734,8 +747,9 @@ __global__ void __launch_bounds__(K1_NT) k_warp(WarpArgs a) {
   float* Jb = a.J ? a.J + (size_t)b * p * mn : nullptr;
   for (int o = threadIdx.x; o < mn; o += K1_NT) {
     const int i = o / n, j = o - i * n;
-    double d, jr[8];
-    warp_pixel(g, img, a.H, a.W, i, j, d, jr);
+    double d, gx, gy, gz, jr[8];
+    warp_pixel(g, img, a.H, a.W, i, j, d, gx, gy, gz);
+    jraw_row(gx, gy, gz, (j - 0.5 * (n - 1)) * inv_s, (i - 0.5 * (m - 1)) * inv_s, jr);
     const double dh = d * ind;
     Dh[o] = (float)dh;
     if (Jb) {
