@@ -51,9 +51,13 @@ def _gen_one(args):
     return ts.gen_patch(ts.CONFIGS[cfg_id], idx)
 
 
-def gen_shard(cfg_id: int, start: int, count: int, workers: int = 0) -> dict:
+def gen_shard(cfg_id: int, start: int, count: int, workers: int = 0, indices=None) -> dict:
     workers = workers or min(16, os.cpu_count() or 1)
-    jobs = [(cfg_id, start + i) for i in range(count)]
+    if indices is not None:
+        count = len(indices)
+        jobs = [(cfg_id, int(i)) for i in indices]
+    else:
+        jobs = [(cfg_id, start + i) for i in range(count)]
     if workers > 1 and count > 8:
         with mp.get_context("fork").Pool(workers) as pool:
             pats = pool.map(_gen_one, jobs, chunksize=16)
@@ -163,13 +167,15 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     import torch
     import torch.distributed as dist
     import paper_1205_5351_b200 as T
+    from paper_1205_5351_b200 import dist as D
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     cfg = ts.CONFIGS[CFG_ID]
     B = args.batch
     m, n, p, kind = cfg.m, cfg.n, cfg.p, cfg.kind
-    batch = gen_shard(CFG_ID, rank * B, B)
+    # rank r solves patches r, r + N, r + 2N, ... of the first N*B patches (interleaved shards)
+    batch = gen_shard(CFG_ID, 0, B, indices=D.shard_indices(B * world, world, rank))
     images = torch.as_tensor(batch["images"], device=dev)
     patch_image = torch.as_tensor(batch["patch_image"], device=dev)
     boxes = torch.as_tensor(batch["boxes"], device=dev)
@@ -237,10 +243,8 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     gather_ms = None
     if world > 1:
         t0 = time.perf_counter()
-        bufs = [torch.empty_like(out["tau"]) for _ in range(world)] if rank == 0 else None
-        dist.gather(out["tau"], bufs, dst=0)
-        rbufs = [torch.empty_like(out["rep"]) for _ in range(world)] if rank == 0 else None
-        dist.gather(out["rep"], rbufs, dst=0)
+        for key in ("tau", "rep", "A", "E"):
+            D.gather_to_root(out[key], B * world, world, rank)
         torch.cuda.synchronize()
         gather_ms = 1e3 * (time.perf_counter() - t0)
     if rank != 0:
