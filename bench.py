@@ -336,6 +336,7 @@ def k1_roofline(solver, images, patch_image, boxes, tau0, kind, m, n, p, peaks) 
 
 def e2e(solver, batch, kind, prm, args) -> dict:
     import torch
+    from paper_1205_5351_b200._abi import REPORT_BYTES as T_REPORT_BYTES
     images = np.ascontiguousarray(batch["images"])
     pinned = {k: torch.from_numpy(np.ascontiguousarray(v)).pin_memory() for k, v in batch.items()}
     B = batch["boxes"].shape[0]
@@ -355,7 +356,7 @@ def e2e(solver, batch, kind, prm, args) -> dict:
     torch.cuda.synchronize()
     t = e0.elapsed_time(e1) / 1e3
     h2d = images.nbytes + batch["patch_image"].nbytes + batch["boxes"].nbytes + B * p * 4
-    d2h = B * p * 4 + 2 * B * m * n * 4 + B * 64
+    d2h = B * p * 4 + 2 * B * m * n * 4 + B * T_REPORT_BYTES
     return {"value": conv / t, "unit": "patches/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
             "api": "tilt_solve_batch_host (host buffers, pinned)"}
 

@@ -115,6 +115,8 @@ typedef struct {
   float patch_norm;       /* ||D o tau||_F at the last outer iteration */
   float dtau_inf;         /* ||dtau||_inf of the last outer iteration */
   float mu_last;          /* mu_K of the last SVT */
+  int32_t jacobi_rotations; /* Jacobi rotations applied, summed over the LADMAP SVTs (S32-S128) */
+  int32_t reserved;
 } tilt_report;
 
 typedef struct {

@@ -62,6 +62,8 @@ class TiltReport(ctypes.Structure):
         ("patch_norm", ctypes.c_float),
         ("dtau_inf", ctypes.c_float),
         ("mu_last", ctypes.c_float),
+        ("jacobi_rotations", ctypes.c_int32),
+        ("reserved", ctypes.c_int32),
     ]
 
 

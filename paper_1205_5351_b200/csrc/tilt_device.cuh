@@ -74,6 +74,7 @@ struct Scal {
   int svt_band;
   int flag;
   int patch;
+  int rot_acc;       // Jacobi rotations of the current SVT
 };
 
 // --------------------------------------------------------------------------------------------
@@ -149,7 +150,8 @@ struct Ctx {
   float4* ns;            // (norm^2, scale, 1/scale, -) per Jacobi column
   float* hv;
   Scal* sc;
-  int m, n, p, ld, pl;   // pl = ld * n (plane size)
+  int m, n, p, ld, pl;   // planes: leading dimension ld, pl = ld * n (plane size)
+  int lds;               // SVD buffers: leading dimension MAXD (every Jacobi chunk exists)
   float ci, cj, inv_s;   // normalised frame: u = (j - cj) inv_s, v = (i - ci) inv_s
 };
 
@@ -334,7 +336,7 @@ __device__ __forceinline__ void svt_stats(Ctx<C>& cx, float eps) {
 // S <- V^T, B <- S V, B <- 1.5 I - 0.5 B, S <- V B, swap(S, V). B and S must be free.
 template <class C>
 __device__ __forceinline__ void ns_step(Ctx<C>& cx) {
-  const int n = cx.n, ld = cx.ld;
+  const int n = cx.n, ld = cx.lds;
   transpose_nn<C>(cx.S, cx.V, ld, n);
   __syncthreads();
   gemm_nn<C>(cx.B, cx.S, cx.V, ld, n, n, n);
@@ -351,6 +353,7 @@ __device__ __forceinline__ void ns_step(Ctx<C>& cx) {
 
 struct SvtOut {
   int sweeps;
+  int rotations;
   bool capped;
 };
 
@@ -360,21 +363,24 @@ template <class C, bool DO_OUT, class Out>
 __device__ SvtOut svt(Ctx<C>& cx, const float* X, float eps, float tol, int max_sweeps, bool warm, Out out,
                       bool ns_after) {
   if (!warm) {
-    set_identity<C>(cx.V, cx.ld, cx.n);
+    set_identity<C>(cx.V, cx.lds, cx.n);
     __syncthreads();
   }
-  gemm_nn<C>(cx.B, X, cx.V, cx.ld, cx.m, cx.n, cx.n);  // B = X V
+  gemm_nn<C>(cx.B, X, cx.V, cx.lds, cx.m, cx.n, cx.n);  // B = X V (X in the lds layout)
   SvtOut r;
+  r.rotations = 0;
   if constexpr (C::SVD_SMEM) {
     int capped = 0;
-    r.sweeps = jacobi_sweeps_smem<C>(cx.B, cx.V, cx.ns, cx.n, cx.ld, tol, max_sweeps, &capped);
+    if (threadIdx.x == 0) cx.sc->rot_acc = 0;  // published by the first barrier inside
+    r.sweeps = jacobi_sweeps_smem<C>(cx.B, cx.V, cx.ns, cx.n, tol, max_sweeps, &capped, &cx.sc->rot_acc);
     r.capped = capped != 0;
+    r.rotations = cx.sc->rot_acc;
   } else {
     r.sweeps = jacobi_sweeps<C>(cx, tol, max_sweeps, &r.capped);
   }
   col_pass<C, 2>(cx, eps);  // sigma_j, h_j, B <- B diag(h / ||v||^2)
   svt_stats<C>(cx, eps);
-  if constexpr (DO_OUT) gemm_bvt<C>(cx.B, cx.V, cx.ld, cx.m, cx.n, out);  // A = B diag(h) V^T
+  if constexpr (DO_OUT) gemm_bvt<C>(cx.B, cx.V, cx.lds, cx.m, cx.n, out);  // A = B diag(h) V^T
   __syncthreads();
   if (ns_after) ns_step<C>(cx);
   return r;

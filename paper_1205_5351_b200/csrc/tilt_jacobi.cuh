@@ -60,6 +60,13 @@ struct Col {
           : "+f"(v[4 * q]), "+f"(v[4 * q + 1]), "+f"(v[4 * q + 2]), "+f"(v[4 * q + 3])
           : "r"(a + 16 * q * L), "r"((int)(cm >> q & 1u)));
   }
+  __device__ __forceinline__ void sload_full(uint32_t a) {  // every chunk exists
+#pragma unroll
+    for (int q = 0; q < NCH; ++q)
+      asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
+                   : "=f"(v[4 * q]), "=f"(v[4 * q + 1]), "=f"(v[4 * q + 2]), "=f"(v[4 * q + 3])
+                   : "r"(a + 16 * q * L));
+  }
   __device__ __forceinline__ void sstore(uint32_t a, uint32_t cm) const {
 #pragma unroll
     for (int q = 0; q < NCH; ++q)
@@ -92,6 +99,12 @@ __device__ __forceinline__ float rcp_approx(float x) {
   return r;
 }
 
+__device__ __forceinline__ float rsqrt_approx(float x) {
+  float r;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
 __device__ __forceinline__ float4 lds4(uint32_t a) {
   float4 v;
   asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
@@ -118,14 +131,14 @@ struct Rot {
 __device__ __forceinline__ Rot rot_params(float4 ni, float4 nj, float gam, bool doit) {
   const float D = nj.x - ni.x, G = 2.f * gam;
   const float r2 = fmaf(D, D, G * G);
-  const float den = fabsf(D) + r2 * rsqrtf(r2);
+  const float den = fmaf(r2, rsqrt_approx(r2), fabsf(D));  // |D| + sqrt(D^2 + G^2), > 0 when doit
   float t = G * rcp_approx(den);
   t = (D < 0.f) ? -t : t;
   t = doit ? t : 0.f;
   Rot r;
   r.t = t;
   const float x2 = fmaf(t, t, 1.f);
-  r.c = rsqrtf(x2);
+  r.c = rsqrt_approx(x2);
   r.ca = t * nj.y * ni.z;  // t d_j / d_i
   r.cb = t * ni.y * nj.z;  // t d_i / d_j
   return r;
@@ -141,7 +154,7 @@ __device__ __forceinline__ Rot rot_params(float4 ni, float4 nj, float gam, bool 
 template <class C, int MODE>
 __device__ __forceinline__ void col_pass(Ctx<C>& cx, float eps) {
   constexpr int L = C::LANES, RPL = C::RPL, UPW = 32 / L;
-  const int n = cx.n, ld = cx.ld;
+  const int n = cx.n, ld = cx.lds;
   const int unit = threadIdx.x / L, lu = threadIdx.x % L;
   const int warp = threadIdx.x >> 5;
   const uint32_t cm = Col<RPL, L>::chunk_mask(lu, ld);
@@ -214,7 +227,7 @@ __device__ __forceinline__ void col_pass_smem(uint32_t sB, uint32_t sV, uint32_t
 template <class C>
 __device__ int jacobi_sweeps(Ctx<C>& cx, float tol, int max_sweeps, bool* capped) {
   constexpr int L = C::LANES, RPL = C::RPL, UPW = 32 / L;
-  const int n = cx.n, ld = cx.ld;
+  const int n = cx.n, ld = cx.lds;
   const int unit = threadIdx.x / L, lu = threadIdx.x % L;
   const int warp = threadIdx.x >> 5;
   const int sub = unit - warp * UPW;
@@ -309,12 +322,14 @@ __device__ int jacobi_sweeps(Ctx<C>& cx, float tol, int max_sweeps, bool* capped
 // (i, j <- i+1, j+1 mod q), __noinline__ so the caller's live state does not crowd its registers.
 // ---------------------------------------------------------------------------------------------
 template <class C>
-__device__ __noinline__ int jacobi_sweeps_smem(float* Bp, float* Vp, float4* nsp, int n, int ld, float tol,
-                                               int max_sweeps, int* capped) {
+__device__ __noinline__ int jacobi_sweeps_smem(float* Bp, float* Vp, float4* nsp, int n, float tol,
+                                               int max_sweeps, int* capped, int* rot_acc) {
+  int nrot = 0;  // rotations applied by this unit (counted on lane 0)
   constexpr int L = C::LANES, RPL = C::RPL;
+  constexpr int ld = C::MAXD;  // SVD buffers are MAXD rows: every chunk exists, no masks
+  constexpr uint32_t cm = (1u << Col<RPL, L>::NCH) - 1u;
   const uint32_t sB = smem_u32(Bp), sV = smem_u32(Vp), sNS = smem_u32(nsp);
   const int unit = threadIdx.x / L, lu = threadIdx.x % L;
-  const uint32_t cm = Col<RPL, L>::chunk_mask(lu, ld);
   const uint32_t lane_off = 4 * lu * 4, colb = ld * 4;
   const int Nn = n + (n & 1);
   const int q = Nn - 1;
@@ -334,8 +349,8 @@ __device__ __noinline__ int jacobi_sweeps_smem(float* Bp, float* Vp, float4* nsp
       const int ii = valid ? i : 0, jj = valid ? j : 0;
       const uint32_t ai = sB + ii * colb + lane_off, aj = sB + jj * colb + lane_off;
       Col<RPL, L> xi, xj;
-      xi.sload(ai, cm);
-      xj.sload(aj, cm);
+      xi.sload_full(ai);
+      xj.sload_full(aj);
       const float4 ni = lds4(sNS + 16 * ii), nj = lds4(sNS + 16 * jj);  // (alpha, d, 1/d, -)
       const float g = unit_sum<L>(xi.dot(xj));
       const float gam = g * ni.y * nj.y;
@@ -345,23 +360,24 @@ __device__ __noinline__ int jacobi_sweeps_smem(float* Bp, float* Vp, float4* nsp
         const Rot rp = rot_params(ni, nj, gam, doit);
         const uint32_t vi = sV + ii * colb + lane_off, vj = sV + jj * colb + lane_off;
         const uint32_t cmr = doit ? cm : 0u;
-        Col<RPL, L> yi, yj;
-        yi.sload(vi, cmr);
-        yj.sload(vj, cmr);
 #pragma unroll
         for (int e = 0; e < RPL; ++e) {
           const float o = xi.v[e];
           xi.v[e] = fmaf(-rp.ca, xj.v[e], o);
           xj.v[e] = fmaf(rp.cb, o, xj.v[e]);
         }
+        xi.sstore(ai, cmr);
+        xj.sstore(aj, cmr);
+        // V columns after B's are stored: only two columns live in registers at a time
+        Col<RPL, L> yi, yj;
+        yi.sload_full(vi);
+        yj.sload_full(vj);
 #pragma unroll
         for (int e = 0; e < RPL; ++e) {
           const float o = yi.v[e];
           yi.v[e] = fmaf(-rp.ca, yj.v[e], o);
           yj.v[e] = fmaf(rp.cb, o, yj.v[e]);
         }
-        xi.sstore(ai, cmr);
-        xj.sstore(aj, cmr);
         yi.sstore(vi, cmr);
         yj.sstore(vj, cmr);
         const float sx = rp.c * fmaf(rp.t, rp.t, 1.f);  // sqrt(1 + t^2)
@@ -369,6 +385,7 @@ __device__ __noinline__ int jacobi_sweeps_smem(float* Bp, float* Vp, float4* nsp
              doit && lu == 0);
         sts4(sNS + 16 * jj, make_float4(fmaf(rp.t, gam, nj.x), rp.c * nj.y, sx * nj.z, 0.f), doit && lu == 0);
         rot |= doit ? 1 : 0;
+        nrot += (doit && lu == 0) ? 1 : 0;
         big |= (doit && gam * gam > big2 * ab) ? 1 : 0;
       }
       __syncthreads();
@@ -384,6 +401,8 @@ __device__ __noinline__ int jacobi_sweeps_smem(float* Bp, float* Vp, float4* nsp
       break;
     }
   }
+  if (rot_acc && nrot) atomicAdd(rot_acc, nrot);
+  __syncthreads();
   *capped = any;
   return sweeps;
 }

@@ -13,7 +13,7 @@ namespace tilt {
 template <class C>
 struct Layout {
   static __host__ __device__ size_t vec_floats() { return 5 * (size_t)C::MAXD; }
-  static __host__ __device__ size_t svd_floats(int ld, int n) { return 3 * (size_t)ld * n; }
+  static __host__ __device__ size_t svd_floats(int, int n) { return 3 * (size_t)C::MAXD * n; }
   static __host__ __device__ size_t plane_floats(int ld, int n, int gplanes) { return (size_t)(4 + gplanes) * ld * n; }
   static __host__ __device__ size_t smem_bytes(int ld, int n, int gplanes) {
     size_t s = vec_floats();
@@ -39,17 +39,19 @@ __device__ __forceinline__ Ctx<C> make_ctx(float* smem, float* ws, Scal* sc, int
   cx.hv = sp + 4 * C::MAXD;
   sp += 5 * C::MAXD;
   const int blk = ld * n;
+  const int sblk = C::MAXD * n;
   float* svd;
   if constexpr (C::SVD_SMEM) {
     svd = sp;
-    sp += 3 * blk;
+    sp += 3 * sblk;
   } else {
     svd = gp;
-    gp += 3 * blk;
+    gp += 3 * sblk;
   }
   cx.B = svd;
-  cx.V = svd + blk;
-  cx.S = svd + 2 * blk;
+  cx.V = svd + sblk;
+  cx.S = svd + 2 * sblk;
+  cx.lds = C::MAXD;
   float* pl;
   if constexpr (C::PLANES_SMEM) {
     pl = sp;
@@ -86,8 +88,10 @@ __device__ __forceinline__ void zero_planes(float* X, size_t count) {
 // ---------------------------------------------------------------------------------------------
 template <class C>
 __device__ float sigma1_of_plane(Ctx<C>& cx, const float* X, float tol, int max_sweeps, bool warm, int* sweeps) {
+  for (PixIter pi(threadIdx.x, C::NT, cx.ld); pi.idx < cx.pl; pi.next(C::NT)) cx.S[pi.j * cx.lds + pi.i] = X[pi.idx];
+  __syncthreads();
   auto none = [](int, int, float4) {};
-  SvtOut so = svt<C, false>(cx, X, 0.f, tol, max_sweeps, warm, none, warm);
+  SvtOut so = svt<C, false>(cx, cx.S, 0.f, tol, max_sweeps, warm, none, warm);
   *sweeps = so.sweeps;
   return cx.sc->svt_sig1;
 }
@@ -103,7 +107,7 @@ __device__ float sigma1_of_plane(Ctx<C>& cx, const float* X, float tol, int max_
 //   rho = rho0 if crit2 < eps2 else 1, mu_{k+1} = min(mu_max, rho mu_k)
 // ---------------------------------------------------------------------------------------------
 struct InnerOut {
-  int iters, sweeps, caps;
+  int iters, sweeps, caps, rotations;
   float mu, crit1, crit2;
   bool converged;
 };
@@ -122,6 +126,7 @@ __device__ InnerOut ladmap_inner(Ctx<C>& cx, const DevParams& P, float lam, floa
   o.iters = 0;
   o.sweeps = 0;
   o.caps = 0;
+  o.rotations = 0;
   o.crit1 = o.crit2 = __int_as_float(0x7fc00000);
   o.converged = false;
   float mu = mu0;
@@ -146,6 +151,7 @@ __device__ InnerOut ladmap_inner(Ctx<C>& cx, const DevParams& P, float lam, floa
         warm);
     o.sweeps += so.sweeps;
     o.caps += so.capped ? 1 : 0;
+    o.rotations += so.rotations;
     // ---- E step ---------------------------------------------------------------------------
     const float inv_mu = 1.f / mu;
     const float thr = lam * inv_mu;
@@ -183,7 +189,7 @@ __device__ InnerOut ladmap_inner(Ctx<C>& cx, const DevParams& P, float lam, floa
       const float y = fmaf(mu, r, Yp[idx]);
       Yp[idx] = y;
       c1 = fmaf(r, r, c1);
-      cx.S[idx] = a - r - y * inv_mun;
+      cx.S[pi.j * cx.lds + pi.i] = a - r - y * inv_mun;
     }
     float cc[1] = {c1};
     block_sum_f<C, 1>(cc, cx.sc);
@@ -248,7 +254,7 @@ __device__ __forceinline__ void write_m0(Ctx<C>& cx, float mu0) {
     const int idx = pi.idx;
     const float v = Ap[idx] + Ep[idx] - Dp[idx];
     const float r = v - PR::apply(cx, idx, pi.i, pi.j, z);
-    cx.S[idx] = Ap[idx] - r - cx.Y[idx] * inv;
+    cx.S[pi.j * cx.lds + pi.i] = Ap[idx] - r - cx.Y[idx] * inv;
   }
   __syncthreads();
 }
@@ -323,10 +329,10 @@ __device__ void solve_patch(const SolveArgs& a, Ctx<C>& cx, int b) {
   const bool warm = P.svd_warm != 0;
   const int gpl = p == 8 ? 3 : 2;
   zero_planes<C>(cx.D, (size_t)(4 + gpl) * pl);  // padding rows stay 0 from here on
-  set_identity<C>(cx.V, ld, n);
+  set_identity<C>(cx.V, cx.lds, n);
   __syncthreads();
   int status = TILT_PATCH_MAX_OUTER, stop_rule = 0, outer = 0, inner_total = 0, sweeps_total = 0,
-      aux_total = 0, caps = 0, rank = 0, band = 0, svt_rank = 0;
+      aux_total = 0, caps = 0, rank = 0, band = 0, svt_rank = 0, rot_total = 0;
   const float fnan = __int_as_float(0x7fc00000);
   float f = fnan, f_prev = fnan, crit1 = fnan, crit2 = fnan, dtau_inf = fnan, mu_last = fnan, nd = fnan;
   bool have_state = false, have_fprev = false;
@@ -387,6 +393,7 @@ __device__ void solve_patch(const SolveArgs& a, Ctx<C>& cx, int b) {
     inner_total += io.iters;
     sweeps_total += io.sweeps;
     caps += io.caps;
+    rot_total += io.rotations;
     crit1 = io.crit1;
     crit2 = io.crit2;
     mu_last = io.mu;
@@ -455,6 +462,8 @@ __device__ void solve_patch(const SolveArgs& a, Ctx<C>& cx, int b) {
       r.patch_norm = nd;
       r.dtau_inf = dtau_inf;
       r.mu_last = mu_last;
+      r.jacobi_rotations = rot_total;
+      r.reserved = 0;
       if (a.rep_prev) {
         const tilt_report& pr = a.rep_prev[b];
         r.outer_iters += pr.outer_iters;
@@ -462,6 +471,7 @@ __device__ void solve_patch(const SolveArgs& a, Ctx<C>& cx, int b) {
         r.jacobi_sweeps += pr.jacobi_sweeps;
         r.aux_sweeps += pr.aux_sweeps;
         r.sweep_cap_hits += pr.sweep_cap_hits;
+        r.jacobi_rotations += pr.jacobi_rotations;
       }
       a.rep[b] = r;
     }
@@ -532,7 +542,7 @@ __global__ void __launch_bounds__(C::NT, 1) k_inner(InnerArgs a) {
         cx.E[idx] = 0.f;
         cx.Y[idx] = 0.f;
       }
-      set_identity<C>(cx.V, ld, n);
+      set_identity<C>(cx.V, cx.lds, n);
       __syncthreads();
       const float denom0 = proj_norm<C, PR>(cx, cx.D);
       const float denom = denom0 > 0.f ? denom0 : 1.f;
@@ -558,6 +568,7 @@ __global__ void __launch_bounds__(C::NT, 1) k_inner(InnerArgs a) {
       rr.crit1 = io.crit1;
       rr.crit2 = io.crit2;
       rr.mu_last = io.mu;
+      rr.jacobi_rotations = io.rotations;
       rr.patch_norm = denom0;
     }
     __syncthreads();
@@ -595,11 +606,11 @@ __global__ void __launch_bounds__(C::NT, 1) k_svt(SvtArgs a) {
   Ctx<C> cx = make_ctx<C>(reinterpret_cast<float*>(dsm4), ws, &sc, a.m, a.n, 0);
   const int m = a.m, n = a.n, mn = m * n, ld = cx.ld;
   for (int b = blockIdx.x; b < a.B; b += gridDim.x) {
-    load_plane<C>(cx.S, a.M + (size_t)b * mn, m, n, ld);
+    load_plane<C>(cx.S, a.M + (size_t)b * mn, m, n, cx.lds);
     if (a.V_io) {
-      load_plane<C>(cx.V, a.V_io + (size_t)b * n * n, n, n, ld);
+      load_plane<C>(cx.V, a.V_io + (size_t)b * n * n, n, n, cx.lds);
     } else {
-      set_identity<C>(cx.V, ld, n);
+      set_identity<C>(cx.V, cx.lds, n);
     }
     __syncthreads();
     float* Ab = a.A + (size_t)b * mn;
@@ -613,7 +624,7 @@ __global__ void __launch_bounds__(C::NT, 1) k_svt(SvtArgs a) {
         false);
     if (a.sigma)
       for (int j = threadIdx.x; j < n; j += C::NT) a.sigma[(size_t)b * n + j] = sqrtf(cx.ns[j].x);
-    if (a.V_io) store_plane<C>(a.V_io + (size_t)b * n * n, cx.V, n, n, ld, false);
+    if (a.V_io) store_plane<C>(a.V_io + (size_t)b * n * n, cx.V, n, n, cx.lds, false);
     if (a.sweeps && threadIdx.x == 0) a.sweeps[b] = so.sweeps;
     __syncthreads();
   }

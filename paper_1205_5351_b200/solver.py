@@ -14,8 +14,8 @@ import torch
 from . import _abi
 from ._abi import lib, check, default_params, TiltParams, TiltCreateOpts
 
-REPORT_DTYPE = np.dtype([(name, np.int32 if i < 10 else np.float32)
-                         for i, name in enumerate(_abi.REPORT_FIELDS)])
+REPORT_DTYPE = np.dtype([(name, np.float32 if ctype is ctypes.c_float else np.int32)
+                         for name, ctype in _abi.TiltReport._fields_])
 assert REPORT_DTYPE.itemsize == _abi.REPORT_BYTES
 
 

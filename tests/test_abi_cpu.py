@@ -27,7 +27,7 @@ def test_header_symbols_exported(pkg):
 
 def test_struct_sizes_match_header(pkg):
     from paper_1205_5351_b200 import _abi
-    assert ctypes.sizeof(_abi.TiltReport) == 16 * 4
+    assert ctypes.sizeof(_abi.TiltReport) == 18 * 4
     assert pkg.lib.tilt_abi_version() == 1
 
 

@@ -39,5 +39,7 @@ it = rep["inner_iters"].sum()
 sw = rep["jacobi_sweeps"].sum()
 m, n, p = cfg.m, cfg.n, cfg.p
 fl = it * (8 * p * m * n + 20 * m * n + 4 * m * n * n + 4 * n ** 3) + sw * n * (n - 1) / 2 * (12 * m + 6 * n)
+rot = rep["jacobi_rotations"].sum()
+pairs = sw * n * (n - 1) / 2
 print(f"batch={a.batch} inner={a.inner} outer={a.outer}: {ms:.3f} ms, {it} iters, {sw/it:.2f} sweeps/iter, "
-      f"{it/ms*1e3:.0f} iters/s, {fl/ms/1e9:.2f} TFLOP/s (model)")
+      f"{rot/max(pairs,1):.3f} rotations/pair-check, {it/ms*1e3:.0f} iters/s, {fl/ms/1e9:.2f} TFLOP/s (model)")
