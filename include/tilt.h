@@ -95,6 +95,10 @@ typedef struct {
   /* window size of the call (all boxes share it). 0: read back from boxes[0] with a stream sync;
    * > 0: taken as given (no host sync; the call is then graph-capturable). */
   int32_t win_h, win_w;
+  /* kernel family: 0 = auto (currently the CTA-per-patch kernels), 1 = CTA-per-patch kernels,
+   * 2 = warp-per-patch kernel (m <= 64 and n <= 50; TILT_E_ARG otherwise). Both compute the same
+   * method; they differ only in data layout and Jacobi ordering. */
+  int32_t kernel_path;
 } tilt_params;
 
 /* Per-patch report (device array written by tilt_solve_batch). */
@@ -115,8 +119,8 @@ typedef struct {
   float patch_norm;       /* ||D o tau||_F at the last outer iteration */
   float dtau_inf;         /* ||dtau||_inf of the last outer iteration */
   float mu_last;          /* mu_K of the last SVT */
-  int32_t jacobi_rotations; /* Jacobi rotations applied, summed over the LADMAP SVTs (S32-S128) */
-  int32_t reserved;
+  int32_t jacobi_rotations; /* Jacobi rotations applied, summed over the LADMAP SVTs */
+  int32_t kernel_path;      /* 1: CTA-per-patch kernel, 2: warp-per-patch kernel solved this patch */
 } tilt_report;
 
 typedef struct {
@@ -205,6 +209,10 @@ tilt_status tilt_inner_batch(tilt_handle* h, const float* D, const float* J, con
                              int32_t l, int32_t B, int32_t m, int32_t n, int32_t p,
                              const tilt_params* prm, float* A, float* E, float* Y,
                              tilt_report* rep);
+
+/* Kernel family used by tilt_svt_batch: 0 = auto (CTA-per-patch), 1 = CTA-per-patch,
+ * 2 = warp-per-patch (m <= 64, n <= 50) (step parity of both implementations). */
+tilt_status tilt_set_svt_path(tilt_handle* h, int32_t path);
 
 /* Number of kernel launches issued by this handle since creation (for bench accounting). */
 int64_t tilt_launch_count(const tilt_handle* h);

@@ -9,7 +9,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libtilt.so")
+# TILT_LIB: alternative build of the same library (A/B experiments of kernel variants)
+LIB_PATH = os.environ.get("TILT_LIB") or os.path.join(_HERE, "libtilt.so")
 
 TILT_OK, TILT_E_ARG, TILT_E_CUDA, TILT_E_OOM, TILT_E_UNSUPPORTED = 0, 1, 2, 3, 4
 AFFINE, HOMOGRAPHY = 0, 1
@@ -41,6 +42,7 @@ class TiltParams(ctypes.Structure):
         ("trace", ctypes.c_void_p),
         ("win_h", ctypes.c_int32),
         ("win_w", ctypes.c_int32),
+        ("kernel_path", ctypes.c_int32),
     ]
 
 
@@ -63,7 +65,7 @@ class TiltReport(ctypes.Structure):
         ("dtau_inf", ctypes.c_float),
         ("mu_last", ctypes.c_float),
         ("jacobi_rotations", ctypes.c_int32),
-        ("reserved", ctypes.c_int32),
+        ("kernel_path", ctypes.c_int32),
     ]
 
 
@@ -87,7 +89,7 @@ EXPORTS = [
     "tilt_abi_version", "tilt_status_string", "tilt_patch_status_string", "tilt_last_error",
     "tilt_default_params", "tilt_create", "tilt_destroy", "tilt_set_stream", "tilt_solve_batch",
     "tilt_solve_batch_host", "tilt_warp_batch", "tilt_svt_batch", "tilt_project_batch",
-    "tilt_inner_batch", "tilt_launch_count",
+    "tilt_inner_batch", "tilt_launch_count", "tilt_set_svt_path",
 ]
 
 _P = ctypes.c_void_p
@@ -131,6 +133,8 @@ def _load():
                                      _P, _P, _P, _P]
     lib.tilt_launch_count.restype = ctypes.c_int64
     lib.tilt_launch_count.argtypes = [_P]
+    lib.tilt_set_svt_path.restype = _I
+    lib.tilt_set_svt_path.argtypes = [_P, _I]
     return lib
 
 

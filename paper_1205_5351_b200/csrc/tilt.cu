@@ -8,6 +8,7 @@
 #include <string>
 
 #include "tilt_kernels.cuh"
+#include "tilt_rj_host.h"
 
 using namespace tilt;
 
@@ -65,6 +66,7 @@ struct tilt_handle {
   float* h_E = nullptr;
   tilt_report* h_rep = nullptr;
   int64_t launches = 0;
+  int svt_path = 0;  // tilt_svt_batch kernel family (tilt_set_svt_path): 0/1 CTA-per-patch, 2 warp-per-patch
 };
 
 namespace {
@@ -112,6 +114,7 @@ bool params_ok(const tilt_params* p) {
   if (p->fixed_inner_iters > p->max_inner || p->fixed_outer_iters > p->max_outer) return false;
   if (p->pyramid_levels < 1 || p->pyramid_levels > 2) return false;
   if (p->constraint_mode != TILT_CONSTRAINTS_NONE && p->constraint_mode != TILT_CONSTRAINTS_CENTER_AREA) return false;
+  if (p->kernel_path < 0 || p->kernel_path > 2) return false;
   return true;
 }
 
@@ -383,6 +386,14 @@ tilt_status tilt_create(tilt_handle** out, const tilt_create_opts* o) {
     const int occ = occ_need(c, h->max_m, h->max_n, gpl);
     h->ws_slots = h->num_sms * (occ > 0 ? occ : 1);
     h->ws_floats = wsf * h->ws_slots;
+  }
+  // the warp-per-patch kernel (m <= 64, n <= 50) needs its own slots; take the larger need
+  {
+    const int mm = h->max_m < 64 ? h->max_m : 64, nn = h->max_n < 50 ? h->max_n : 50;
+    const size_t rjf = tilt::rjh::ws_need(h->num_sms, mm, nn);
+    if (rjf > h->ws_floats) h->ws_floats = rjf;
+  }
+  if (h->ws_floats > 0) {
     if ((e = cudaMalloc(&h->ws, h->ws_floats * sizeof(float))) != cudaSuccess) return fail(e, "cudaMalloc(ws)");
   }
   if ((e = cudaMalloc(&h->counter, 64 * sizeof(int))) != cudaSuccess) return fail(e, "cudaMalloc(counter)");
@@ -414,6 +425,12 @@ tilt_status tilt_set_stream(tilt_handle* h, void* stream) {
 
 int64_t tilt_launch_count(const tilt_handle* h) { return h ? h->launches : 0; }
 
+tilt_status tilt_set_svt_path(tilt_handle* h, int32_t path) {
+  if (!h || path < 0 || path > 2) return TILT_E_ARG;
+  h->svt_path = path;
+  return TILT_OK;
+}
+
 static tilt_status solve_level(tilt_handle* h, const float* images, int32_t n_images, int32_t H, int32_t W,
                                const int32_t* patch_image, const int32_t* boxes, const float* tau0, int32_t B,
                                int m, int n, int32_t kind, const tilt_params* prm, float* tau_out, float* A_out,
@@ -440,6 +457,12 @@ static tilt_status solve_level(tilt_handle* h, const float* images, int32_t n_im
   a.rep = rep;
   a.rep_prev = rep_prev;
   a.counter = h->counter;
+  const bool rj_ok = tilt::rjh::fits(m, n);
+  if (prm->kernel_path == 2 && !rj_ok) {
+    g_last_error = "kernel_path = 2 (warp-per-patch) needs m <= 64 and n <= 50";
+    return TILT_E_ARG;
+  }
+  if (rj_ok && prm->kernel_path == 2) return tilt::rjh::solve(h->num_sms, h->ws, h->ws_floats, h->counter, h->stream, a, &h->launches, &g_last_error);
   return dispatch<SolveF>(size_class(m, n), h, a);
 }
 
@@ -600,6 +623,7 @@ tilt_status tilt_svt_batch(tilt_handle* h, const float* M, int32_t B, int32_t m,
   a.sweeps = sweeps;
   a.tol = default_jacobi_tol(m);
   a.max_sweeps = 20;
+  if (tilt::rjh::fits(m, n) && h->svt_path == 2) return tilt::rjh::svt(h->num_sms, h->ws, h->ws_floats, h->stream, a, &h->launches, &g_last_error);
   return dispatch<SvtF>(size_class(m, n), h, a);
 }
 

@@ -463,7 +463,7 @@ __device__ void solve_patch(const SolveArgs& a, Ctx<C>& cx, int b) {
       r.dtau_inf = dtau_inf;
       r.mu_last = mu_last;
       r.jacobi_rotations = rot_total;
-      r.reserved = 0;
+      r.kernel_path = 1;
       if (a.rep_prev) {
         const tilt_report& pr = a.rep_prev[b];
         r.outer_iters += pr.outer_iters;
@@ -690,6 +690,7 @@ __global__ void __launch_bounds__(C::NT, 1) k_project(ProjArgs a) {
 // so that a warp's taps are coalesced). Two passes: reductions (||d||, D_hat^T J_raw), then
 // recompute (taps from L1/L2) and write D_hat and the normalised J.
 // ---------------------------------------------------------------------------------------------
+#ifndef TILT_NO_FREE_KERNELS  // defined only in the translation unit that owns them (tilt.cu)
 struct WarpArgs {
   const float* images;
   int n_images, H, W;
@@ -787,5 +788,7 @@ __global__ void k_downsample(const float* __restrict__ in, float* __restrict__ o
 __global__ void k_half_boxes(const int* __restrict__ in, int* __restrict__ out, int B) {
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < 4 * B; e += gridDim.x * blockDim.x) out[e] = in[e] / 2;
 }
+
+#endif  // TILT_NO_FREE_KERNELS
 
 }  // namespace tilt

@@ -154,8 +154,10 @@ class TiltSolver:
         torch.cuda.synchronize(dev)
         return {"Dhat": dh, "J": J, "norm": nrm, "status": st}
 
-    def svt(self, M, eps, V=None):
+    def svt(self, M, eps, V=None, path: int = 0):
+        """tilt_svt_batch; path 0 = auto (CTA kernel), 1 = CTA kernel, 2 = warp-per-patch kernel."""
         dev = self.device
+        check(lib.tilt_set_svt_path(self._h, path), "tilt_set_svt_path")
         M = _dev(M, torch.float32, dev)
         B, m, n = M.shape
         eps_t = _dev(np.broadcast_to(np.asarray(eps, np.float32), (B,)).copy(), torch.float32, dev)

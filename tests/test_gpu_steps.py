@@ -71,13 +71,17 @@ def test_warp_escape_and_zero(solver):
 
 
 # ---------------------------------------------------------------------------------------------
-@pytest.mark.parametrize("m,n", [(32, 32), (50, 50), (40, 56), (56, 40), (63, 63), (100, 100), (200, 200)])
-def test_svt_parity(solver, m, n):
+SVT_SIZES = [(32, 32), (50, 50), (40, 56), (56, 40), (63, 63), (64, 50), (33, 35), (100, 100), (200, 200)]
+
+
+@pytest.mark.parametrize("m,n,path", [(m, n, p) for (m, n) in SVT_SIZES for p in (1, 2) if p == 1 or (m <= 64 and n <= 50)])
+def test_svt_parity(solver, m, n, path):
+    """path 1: CTA-per-patch kernel, path 2: warp-per-patch kernel (m <= 64, n <= 50)."""
     B = 4
     Ms = np.stack([ts.lowrank_sparse(m, n, 3 + k, k) for k in range(B)])
     sig1 = np.array([np.linalg.svd(x, compute_uv=False)[0] for x in Ms])
     eps = (sig1 * np.array([0.01, 0.05, 0.2, 1e-4])).astype(np.float32)
-    out = solver.svt(Ms.astype(np.float32), eps)
+    out = solver.svt(Ms.astype(np.float32), eps, path=path)
     A = out["A"].double().cpu().numpy()
     for k in range(B):
         ref, s = O.svt(Ms[k].astype(np.float32).astype(np.float64), float(eps[k]))

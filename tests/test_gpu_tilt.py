@@ -52,18 +52,21 @@ def _replay_tensor(traces_per_patch, max_outer, max_inner, stops=False):
     return torch.as_tensor(arr, device="cuda")
 
 
+@pytest.mark.parametrize("path", [1, 2])
 @pytest.mark.parametrize("cfg_id,K", [(1, 20), (1, 50), (2, 20), (2, 50)])
-def test_fixed_count_parity(solver, T, cfg_id, K):
+def test_fixed_count_parity(solver, T, cfg_id, K, path):
+    """path 1: CTA-per-patch kernel, path 2: warp-per-patch kernel (tilt_params.kernel_path)."""
     cfg = ts.CONFIGS[cfg_id]
     B = 4
     b = ts.gen_batch(cfg, 0, B)
     prm_o = O.Params(fixed_inner_iters=K, fixed_outer_iters=1, max_inner=K, max_outer=1)
     refs = [O.tilt(b["images"][k], b["boxes"][k], b["tau0"][k], cfg.kind, prm_o) for k in range(B)]
     rr = _replay_tensor([r["traces"] for r in refs], 1, K)
-    prm = T.default_params(fixed_inner_iters=K, fixed_outer_iters=1, max_inner=K, max_outer=1)
+    prm = T.default_params(fixed_inner_iters=K, fixed_outer_iters=1, max_inner=K, max_outer=1, kernel_path=path)
     prm.rho_replay = rr.data_ptr()
     out = solver.solve(b["images"], b["patch_image"], b["boxes"], b["tau0"], cfg.kind, prm, want_Y=True)
     rep = T.reports_to_numpy(out["rep"])
+    assert np.all(rep["kernel_path"] == path)
     for k in range(B):
         a = out["A"][k].double().cpu().numpy()
         e = out["E"][k].double().cpu().numpy()
@@ -75,7 +78,7 @@ def test_fixed_count_parity(solver, T, cfg_id, K):
         assert rep["inner_iters"][k] == K and rep["outer_iters"][k] == 1
 
 
-def _convergence_case(solver, T, cfg, idx_list, replay=True, **gen):
+def _convergence_case(solver, T, cfg, idx_list, replay=True, path=0, **gen):
     """Oracle free-running; the GPU replays its outer count and (replay=True) its rho decisions and
     inner-loop ends (parity protocol 3 of SURVEY.md §8(c): the outer problem is flat along the aspect
     direction, so only a replayed path is comparable to 1e-3)."""
@@ -83,7 +86,7 @@ def _convergence_case(solver, T, cfg, idx_list, replay=True, **gen):
     refs = [O.tilt(b["images"][k], b["boxes"][k], b["tau0"][k], cfg.kind) for k in range(len(idx_list))]
     results = []
     for k, r in enumerate(refs):
-        prm = T.default_params(fixed_outer_iters=max(1, r["outer_iters"]))
+        prm = T.default_params(fixed_outer_iters=max(1, r["outer_iters"]), kernel_path=path)
         if replay:
             rr = _replay_tensor([r["traces"]], prm.max_outer, prm.max_inner, stops=True)
             prm.rho_replay = rr.data_ptr()
@@ -105,11 +108,12 @@ def _disagreements(res):
     return bad
 
 
+@pytest.mark.parametrize("path", [1, 2])
 @pytest.mark.parametrize("cfg_id", [1, 2])
-def test_convergence_parity(solver, T, cfg_id):
+def test_convergence_parity(solver, T, cfg_id, path):
     """tau within 1e-3 max-abs, rank equal, objective within 1e-3 (BASELINE north_star), replayed path."""
     cfg = ts.CONFIGS[cfg_id]
-    res = _convergence_case(solver, T, cfg, list(range(8 if cfg_id == 1 else 3)))
+    res = _convergence_case(solver, T, cfg, list(range(8 if cfg_id == 1 else 3)), path=path)
     bad = _disagreements(res)
     for r, rep, _ in res:
         assert rep["inner_iters"] == r["inner_iters"] and rep["outer_iters"] == r["outer_iters"]
@@ -145,7 +149,7 @@ def test_full_size_config2(solver, T):
     # sampled patches vs the oracle (outer count replayed)
     for k in (0, 517):
         r = O.tilt(b["images"][k], b["boxes"][k], b["tau0"][k], cfg.kind)
-        prm = T.default_params(fixed_outer_iters=max(1, r["outer_iters"]))
+        prm = T.default_params(fixed_outer_iters=max(1, r["outer_iters"]), kernel_path=path)
         rr = _replay_tensor([r["traces"]], prm.max_outer, prm.max_inner, stops=True)
         prm.rho_replay = rr.data_ptr()
         o1 = solver.solve(b["images"][k:k + 1], [0], b["boxes"][k:k + 1], b["tau0"][k:k + 1], cfg.kind, prm)
