@@ -99,6 +99,9 @@ typedef struct {
    * 2 = warp-per-patch kernel (m <= 64 and n <= 50; TILT_E_ARG otherwise). Both compute the same
    * method; they differ only in data layout and Jacobi ordering. */
   int32_t kernel_path;
+  /* Newton-Schulz re-orthonormalisation of the carried V (reading Z14) after every ns_period-th
+   * LADMAP SVT of an inner loop (and after the last one); <= 1: after every SVT. */
+  int32_t ns_period;
 } tilt_params;
 
 /* Per-patch report (device array written by tilt_solve_batch). */
@@ -178,12 +181,14 @@ tilt_status tilt_solve_batch_host(tilt_handle* h, const float* images, int32_t n
 
 /* K1: Alg. 1 Step 1 for B patches at the given tau: D_hat = D o tau / ||D o tau||_F and
  * J = d/dtau (D o tau / ||D o tau||_F) (quotient rule), bilinear sampling with the exact
- * interpolant derivative (Z2). Outputs: Dhat [B][m][n], J [B][p][m][n] (may be NULL),
- * norm [B] = ||D o tau||_F (may be NULL), status [B] int32 (tilt_patch_status; may be NULL). */
+ * interpolant derivative (Z2). win_h, win_w: window size of the call (all boxes share it); <= 0 ->
+ * read from boxes[0] with a stream sync (> 0: no host sync, graph-capturable). Outputs: Dhat
+ * [B][m][n], J [B][p][m][n] (may be NULL), norm [B] = ||D o tau||_F (may be NULL), status [B]
+ * int32 (tilt_patch_status; may be NULL). */
 tilt_status tilt_warp_batch(tilt_handle* h, const float* images, int32_t n_images, int32_t H,
                             int32_t W, const int32_t* patch_image, const int32_t* boxes,
-                            const float* tau, int32_t B, int32_t kind, float* Dhat, float* J,
-                            float* norm, int32_t* status);
+                            const float* tau, int32_t B, int32_t kind, int32_t win_h, int32_t win_w,
+                            float* Dhat, float* J, float* norm, int32_t* status);
 
 /* K3 core: singular value thresholding S_eps(M) (Eqs. A_1, S_operator) of B matrices
  * [B][m][n] with per-matrix eps [B], by warm one-sided Jacobi. V_io [B][n][n] row-major: input

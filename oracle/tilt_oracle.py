@@ -7,7 +7,8 @@ TEST INFRASTRUCTURE ONLY. Only ``tests/``, ``__graft_entry__.smoke()`` and ``ben
 Every function follows the paper step by step in its notation; citations are ``P:<line>`` of
 ``/root/reference/PAPER.md`` with the section / equation label. Where the paper is silent or
 garbled the reading taken is named (R*/Z*/E*), listed in DESIGN.md "Readings of the paper".
-Library primitives used as single steps: ``numpy.linalg.svd`` (the SVD in Eq. S_operator),
+Library primitives used as single steps: ``numpy.linalg.svd`` (the SVD in Eq. S_operator; the
+oracle's own one-sided Jacobi ``jacobi_svd`` is the alternative, Params.svd = "jacobi"),
 ``numpy.linalg.cholesky`` / ``solve`` (the p x p Gram system of Eq. Jperpv). No blocking, fusion or
 reordering beyond what the equations state.
 
@@ -54,6 +55,7 @@ class Params:
     vws: bool = True            # variable warm start (Eq. warm_start)
     fixed_inner_iters: int = 0  # >0: run exactly K inner iterations (test mode)
     fixed_outer_iters: int = 0  # >0: run exactly F outer iterations (test mode)
+    svd: str = "lapack"         # SVD inside S_eps: "lapack" (library step) or "jacobi" (own, jacobi_svd)
 
 
 # ----------------------------------------------------------------------------------------------
@@ -66,12 +68,80 @@ def shrink(x, eps):
     return np.sign(x) * np.maximum(np.abs(x) - eps, 0.0)
 
 
-def svt(w, eps):
+def jacobi_svd(w, tol=1e-14, max_sweeps=60, v0=None):
+    """The oracle's own SVD: one-sided (Hestenes) Jacobi in fp64 (SURVEY.md §8(c) oracle step 5).
+
+    B = W V with V orthogonal (identity, or the warm start v0); every sweep visits each column pair
+    (i, j) once (round-robin parallel ordering: the n/2 disjoint pairs of a round are rotated
+    together), rotating the pair so that b_i . b_j = 0 with the smaller-angle tangent
+    t = sgn(zeta)/(|zeta| + sqrt(1 + zeta^2)), zeta = (beta - alpha)/(2 gamma); a pair is skipped
+    when |gamma| <= tol sqrt(alpha beta). Stops after a sweep without rotation (<= max_sweeps).
+    Returns (U, sigma, V, sweeps): W = U diag(sigma) V^T, sigma descending; columns of U for
+    sigma = 0 are 0 (they multiply zero in every use below).
+    """
+    b = np.array(w, dtype=np.float64, copy=True)
+    m, n = b.shape
+    v = np.eye(n) if v0 is None else np.array(v0, dtype=np.float64, copy=True)
+    if v0 is not None:
+        b = b @ v
+    nn = n + (n & 1)
+    q = nn - 1
+    # columns below this squared norm are zero to working precision (the n - rank columns of a
+    # rank-deficient W converge to rounding noise, which must not keep the sweeps going)
+    small = (n * np.finfo(np.float64).eps * max(np.linalg.norm(b), np.finfo(np.float64).tiny)) ** 2
+    sweeps = 0
+    for sweeps in range(1, max_sweeps + 1):
+        rotated = False
+        for r in range(q):
+            k = np.arange(nn // 2)
+            i = np.where(k == 0, q, (r + k) % q)
+            j = np.where(k == 0, r % q, (r - k) % q)
+            keep = (i < n) & (j < n)
+            i, j = i[keep], j[keep]
+            bi, bj = b[:, i], b[:, j]
+            alpha = np.einsum("ij,ij->j", bi, bi)
+            beta = np.einsum("ij,ij->j", bj, bj)
+            gamma = np.einsum("ij,ij->j", bi, bj)
+            act = (np.abs(gamma) > tol * np.sqrt(alpha * beta)) & (alpha > small) & (beta > small)
+            if not np.any(act):
+                continue
+            rotated = True
+            i, j, alpha, beta, gamma = i[act], j[act], alpha[act], beta[act], gamma[act]
+            zeta = (beta - alpha) / (2.0 * gamma)
+            t = np.sign(zeta) / (np.abs(zeta) + np.hypot(1.0, zeta))
+            t[zeta == 0.0] = 1.0
+            c = 1.0 / np.sqrt(1.0 + t * t)
+            s = c * t
+            bi, bj = b[:, i].copy(), b[:, j].copy()
+            b[:, i] = c * bi - s * bj
+            b[:, j] = s * bi + c * bj
+            vi, vj = v[:, i].copy(), v[:, j].copy()
+            v[:, i] = c * vi - s * vj
+            v[:, j] = s * vi + c * vj
+        if not rotated:
+            break
+    sigma = np.sqrt(np.einsum("ij,ij->j", b, b))
+    order = np.argsort(-sigma, kind="stable")
+    sigma, b, v = sigma[order], b[:, order], v[:, order]
+    u = np.divide(b, sigma, out=np.zeros_like(b), where=sigma > 0)
+    return u, sigma, v, sweeps
+
+
+SVD_METHOD = {"lapack": None, "jacobi": jacobi_svd}
+
+
+def svt(w, eps, method="lapack"):
     """Singular value shrinkage S_eps(W) = U T_eps(Sigma) V^T  (Eqs. A_1, S_operator).
 
-    Returns (S_eps(W), sigma(W)) with sigma the singular values of W (descending).
+    The SVD is the library routine (method="lapack", a single library step) or the oracle's own
+    one-sided Jacobi (method="jacobi", ``jacobi_svd``); both give the same S_eps(W) (the prox of
+    eps ||.||_*, is single valued). Returns (S_eps(W), sigma(W)) with sigma descending.
     """
-    u, sig, vt = np.linalg.svd(np.asarray(w, dtype=np.float64), full_matrices=False)
+    w = np.asarray(w, dtype=np.float64)
+    if method == "jacobi":
+        u, sig, v, _ = jacobi_svd(w)
+        return (u * shrink(sig, eps)) @ v.T, sig
+    u, sig, vt = np.linalg.svd(w, full_matrices=False)
     return (u * shrink(sig, eps)) @ vt, sig
 
 
@@ -289,7 +359,7 @@ class InnerResult:
 
 
 def ladmap(dh, proj, lam, mu0, mu_max, rho0, eps1, eps2, max_inner, a0, e0, y0,
-           fixed_iters=0, rho_replay=None):
+           fixed_iters=0, rho_replay=None, svd="lapack"):
     """LADMAP for min ||A||_* + lam ||E||_1  s.t.  W^T W (A + E) = W^T W D  (Eq. reformulated_TILT2).
 
     Iteration (Eq. newvars2, with errata E1 (+ sign of the dual step, as Eq. Y)
@@ -320,7 +390,7 @@ def ladmap(dh, proj, lam, mu0, mu_max, rho0, eps1, eps2, max_inner, a0, e0, y0,
     k = 0
     for k in range(n_iter):
         m_k = a - y / mu - r
-        a1, sig = svt(m_k, 1.0 / mu)
+        a1, sig = svt(m_k, 1.0 / mu, svd)
         n_k = e - y / mu - proj.apply(a1 + e - dh)
         e1 = shrink(n_k, lam / mu)
         r = proj.apply(a1 + e1 - dh)
@@ -406,7 +476,7 @@ def tilt(image, box, tau0, kind, prm: Params = Params(), rho_replay=None):
         mu0 = prm.mu0_scale / sigma1
         replay = rho_replay[it] if rho_replay is not None and it < len(rho_replay) else None
         res = ladmap(dh, proj, lam, mu0, prm.mu_max_ratio * mu0, prm.rho0, prm.eps1, prm.eps2,
-                     prm.max_inner, a, e, y, fixed_iters=prm.fixed_inner_iters, rho_replay=replay)
+                     prm.max_inner, a, e, y, fixed_iters=prm.fixed_inner_iters, rho_replay=replay, svd=prm.svd)
         a, e, y = res.A, res.E, res.Y
         inner_iters += res.iters
         outer_traces.append(res.trace)

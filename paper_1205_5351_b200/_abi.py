@@ -43,6 +43,7 @@ class TiltParams(ctypes.Structure):
         ("win_h", ctypes.c_int32),
         ("win_w", ctypes.c_int32),
         ("kernel_path", ctypes.c_int32),
+        ("ns_period", ctypes.c_int32),
     ]
 
 
@@ -123,7 +124,7 @@ def _load():
     lib.tilt_solve_batch_host.argtypes = [_P, _P, _I, _I, _I, _P, _P, _P, _I, _I,
                                           ctypes.POINTER(TiltParams), _P, _P, _P, _P]
     lib.tilt_warp_batch.restype = _I
-    lib.tilt_warp_batch.argtypes = [_P, _P, _I, _I, _I, _P, _P, _P, _I, _I, _P, _P, _P, _P]
+    lib.tilt_warp_batch.argtypes = [_P, _P, _I, _I, _I, _P, _P, _P, _I, _I, _I, _I, _P, _P, _P, _P]
     lib.tilt_svt_batch.restype = _I
     lib.tilt_svt_batch.argtypes = [_P, _P, _I, _I, _I, _P, _P, _P, _P, _P]
     lib.tilt_project_batch.restype = _I

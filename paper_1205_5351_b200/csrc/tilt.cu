@@ -97,6 +97,7 @@ DevParams to_dev(const tilt_params* prm) {
   P.jacobi_max_sweeps = prm->jacobi_max_sweeps;
   P.fixed_inner = prm->fixed_inner_iters;
   P.fixed_outer = prm->fixed_outer_iters;
+  P.ns_period = prm->ns_period > 1 ? prm->ns_period : 1;
   P.rho_replay = prm->rho_replay;
   P.trace = prm->trace;
   return P;
@@ -571,16 +572,18 @@ tilt_status tilt_solve_batch_host(tilt_handle* h, const float* images, int32_t n
 
 tilt_status tilt_warp_batch(tilt_handle* h, const float* images, int32_t n_images, int32_t H, int32_t W,
                             const int32_t* patch_image, const int32_t* boxes, const float* tau, int32_t B, int32_t kind,
-                            float* Dhat, float* J, float* norm, int32_t* status) {
+                            int32_t win_h, int32_t win_w, float* Dhat, float* J, float* norm, int32_t* status) {
   if (!h || B < 0) return TILT_E_ARG;
   if (B == 0) return TILT_OK;
   if (!images || !patch_image || !boxes || !tau || !Dhat) return TILT_E_ARG;
   if (kind != TILT_AFFINE && kind != TILT_HOMOGRAPHY) return TILT_E_ARG;
   TILT_CUDA(cudaSetDevice(h->device));
-  int m = 0, n = 0;
-  tilt_status s = first_box(h, boxes, &m, &n);
-  if (s != TILT_OK) return s;
-  if (m < 2 || n < 2) return TILT_E_ARG;
+  int m = win_h, n = win_w;
+  if (m <= 0 || n <= 0) {
+    tilt_status s = first_box(h, boxes, &m, &n);
+    if (s != TILT_OK) return s;
+  }
+  if (m < 2 || n < 2 || (size_t)m * n * sizeof(float4) > 227 * 1024) return TILT_E_ARG;
   WarpArgs a;
   a.images = images;
   a.n_images = n_images;
@@ -598,7 +601,9 @@ tilt_status tilt_warp_batch(tilt_handle* h, const float* images, int32_t n_image
   a.J = J;
   a.norm = norm;
   a.status = status;
-  k_warp<<<B, K1_NT, 0, h->stream>>>(a);
+  const size_t k1_smem = (size_t)m * n * sizeof(float4);  // (d, gx, gy, gz) per window pixel
+  if (k1_smem > 48 * 1024) TILT_CUDA(cudaFuncSetAttribute((const void*)k_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k1_smem));
+  k_warp<<<B, K1_NT, k1_smem, h->stream>>>(a);
   h->launches++;
   TILT_CUDA(cudaGetLastError());
   return TILT_OK;

@@ -53,6 +53,7 @@ struct DevParams {
   float jacobi_tol;
   int jacobi_max_sweeps;
   int fixed_inner, fixed_outer;
+  int ns_period;
   const uint8_t* rho_replay;
   float* trace;
 };

@@ -148,7 +148,7 @@ __device__ InnerOut ladmap_inner(Ctx<C>& cx, const DevParams& P, float lam, floa
           d = a.w - o4.w; dA2 = fmaf(d, d, dA2);
           *reinterpret_cast<float4*>(ap) = a;
         },
-        warm);
+        warm && (k % P.ns_period == P.ns_period - 1 || k + 1 == niter));
     o.sweeps += so.sweeps;
     o.caps += so.capped ? 1 : 0;
     o.rotations += so.rotations;
@@ -686,9 +686,14 @@ __global__ void __launch_bounds__(C::NT, 1) k_project(ProjArgs a) {
 }
 
 // ---------------------------------------------------------------------------------------------
-// K1 standalone: Alg. 1 Step 1 over all patches (HBM-bound; one CTA per patch, row-major pixels
-// so that a warp's taps are coalesced). Two passes: reductions (||d||, D_hat^T J_raw), then
-// recompute (taps from L1/L2) and write D_hat and the normalised J.
+// K1 standalone: Alg. 1 Step 1 over all patches (HBM-bound). One CTA per patch.
+//   pass 1: per pixel (fp64 coordinates, 4 bilinear taps) -> d, gx, gy, gz stored fp32 in shared
+//           memory (the same fp32 values the fused solve kernel keeps in its planes), fp64 sums of
+//           ||d||^2 and J_raw^T d; the tap loads of K1_ILP pixels are issued before their math;
+//   pass 2: D_hat = d/||d|| and J = (J_raw - D_hat c^T)/||d|| (quotient rule) from shared memory,
+//           written as coalesced row-major planes.
+// Traffic per patch: the window's 4-tap footprint (~(m+1)(n+1) pixels) read, (1+p) m n floats
+// written.
 // ---------------------------------------------------------------------------------------------
 #ifndef TILT_NO_FREE_KERNELS  // defined only in the translation unit that owns them (tilt.cu)
 struct WarpArgs {
@@ -705,8 +710,36 @@ struct WarpArgs {
 };
 
 constexpr int K1_NT = 256;
+constexpr int K1_ILP = 4;
 
-__global__ void __launch_bounds__(K1_NT) k_warp(WarpArgs a) {
+// Geometry of one window pixel: source coordinate, cell and fractions (reading Z2, Z15, Z16)
+struct Tap {
+  int off;            // yi * W + xi
+  float fx, fy, w, xn, yn;  // fractions from the fp64 source coordinate, then rounded to fp32
+  bool ok;
+};
+
+__device__ __forceinline__ Tap tap_geom(const WarpGeom& g, double inv_s, int H, int W, int i, int j) {
+  Tap t;
+  const double du = j - 0.5 * (g.n - 1);
+  const double dv = i - 0.5 * (g.m - 1);
+  const double w = 1.0 + (g.h31 * du + g.h32 * dv) * inv_s;
+  const double iw = g.kind == TILT_HOMOGRAPHY ? 1.0 / w : 1.0;
+  const double X = g.cx + (g.h11 * du + g.h12 * dv + g.s * g.h13) * iw;
+  const double Y = g.cy + (g.h21 * du + g.h22 * dv + g.s * g.h23) * iw;
+  const double X0 = floor(X), Y0 = floor(Y);
+  t.ok = X0 >= 0.0 && X0 + 1.0 <= W - 1 && Y0 >= 0.0 && Y0 + 1.0 <= H - 1;
+  t.fx = (float)(X - X0);
+  t.fy = (float)(Y - Y0);
+  t.w = (float)w;
+  t.off = t.ok ? (int)Y0 * W + (int)X0 : 0;
+  t.xn = (float)((X - g.cx) * inv_s);
+  t.yn = (float)((Y - g.cy) * inv_s);
+  return t;
+}
+
+__global__ void __launch_bounds__(K1_NT, 3) k_warp(WarpArgs a) {
+  extern __shared__ float4 k1s[];  // per pixel (d, gx, gy, gz)
   __shared__ double red[K1_NT / 32][9];
   __shared__ double tot[9];
   const int b = blockIdx.x;
@@ -719,14 +752,50 @@ __global__ void __launch_bounds__(K1_NT) k_warp(WarpArgs a) {
   const double inv_s = 1.0 / g.s;
   double acc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
   bool esc = false;
-  for (int o = threadIdx.x; o < mn; o += K1_NT) {
-    const int i = o / n, j = o - i * n;
-    double d, gx, gy, gz, jr[8];
-    if (!warp_pixel(g, img, a.H, a.W, i, j, d, gx, gy, gz)) esc = true;
-    jraw_row(gx, gy, gz, (j - 0.5 * (n - 1)) * inv_s, (i - 0.5 * (m - 1)) * inv_s, jr);
-    acc[8] = fma(d, d, acc[8]);
+  PixIter it(threadIdx.x, K1_NT, n);  // row-major (j fastest): it.i is the column j, it.j the row i
+  for (int o0 = threadIdx.x; o0 < mn; o0 += K1_NT * K1_ILP) {
+    Tap t[K1_ILP];
+    float v[K1_ILP][4];
+    int pi[K1_ILP], pj[K1_ILP];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) acc[q] = fma(jr[q], d, acc[q]);
+    for (int u = 0; u < K1_ILP; ++u) {  // geometry and all tap loads first
+      const int o = o0 + u * K1_NT;
+      pi[u] = it.j;
+      pj[u] = it.i;
+      it.next(K1_NT);
+      const int i = pi[u], j = pj[u];
+      t[u] = tap_geom(g, inv_s, a.H, a.W, o < mn ? i : 0, o < mn ? j : 0);
+      const bool live = o < mn && t[u].ok;
+      esc |= (o < mn) && !t[u].ok;
+      const float* r0 = img + t[u].off;
+      v[u][0] = live ? __ldg(r0) : 0.f;
+      v[u][1] = live ? __ldg(r0 + 1) : 0.f;
+      v[u][2] = live ? __ldg(r0 + a.W) : 0.f;
+      v[u][3] = live ? __ldg(r0 + a.W + 1) : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < K1_ILP; ++u) {
+      const int o = o0 + u * K1_NT;
+      if (o >= mn) break;
+      const int i = pi[u], j = pj[u];
+      const float fx = t[u].fx, fy = t[u].fy;
+      const float i00 = v[u][0], i01 = v[u][1], i10 = v[u][2], i11 = v[u][3];
+      const float top = fmaf(fx, i01 - i00, i00), bot = fmaf(fx, i11 - i10, i10);
+      const float d = fmaf(fy, bot - top, top);
+      const float dX = fmaf(fy, (i11 - i10) - (i01 - i00), i01 - i00);
+      const float dY = bot - top;
+      const float sw = (float)g.s / t[u].w;
+      const float gx = sw * dX, gy = sw * dY;
+      const float gz = -fmaf(gx, t[u].xn, gy * t[u].yn);
+      const float4 px = make_float4(d, gx, gy, gz);
+      k1s[o] = px;
+      double jr[8];
+      jraw_row(px.y, px.z, px.w, (j - 0.5 * (n - 1)) * inv_s, (i - 0.5 * (m - 1)) * inv_s, jr);
+      const double dd = px.x;
+      acc[8] = fma(dd, dd, acc[8]);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) acc[q] = fma(jr[q], dd, acc[q]);
+    }
   }
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
 #pragma unroll
@@ -751,23 +820,25 @@ __global__ void __launch_bounds__(K1_NT) k_warp(WarpArgs a) {
     if (a.norm) a.norm[b] = (float)nd;
     if (a.status) a.status[b] = st;
   }
-  const double ind = st == TILT_PATCH_CONVERGED ? 1.0 / nd : 0.0;
-  double c[8];
+  const double indd = st == TILT_PATCH_CONVERGED ? 1.0 / nd : 0.0;
+  const float ind = (float)indd;
+  float c[8];
 #pragma unroll
-  for (int q = 0; q < 8; ++q) c[q] = tot[q] * ind;
+  for (int q = 0; q < 8; ++q) c[q] = (float)(tot[q] * indd);  // D_hat^T J_raw
   float* Dh = a.Dhat + (size_t)b * mn;
   float* Jb = a.J ? a.J + (size_t)b * p * mn : nullptr;
-  for (int o = threadIdx.x; o < mn; o += K1_NT) {
-    const int i = o / n, j = o - i * n;
-    double d, gx, gy, gz, jr[8];
-    warp_pixel(g, img, a.H, a.W, i, j, d, gx, gy, gz);
-    jraw_row(gx, gy, gz, (j - 0.5 * (n - 1)) * inv_s, (i - 0.5 * (m - 1)) * inv_s, jr);
-    const double dh = d * ind;
-    Dh[o] = (float)dh;
+  const float inv_sf = (float)inv_s, ci = 0.5f * (m - 1), cj = 0.5f * (n - 1);
+  for (PixIter it2(threadIdx.x, K1_NT, n); it2.idx < mn; it2.next(K1_NT)) {
+    const int o = it2.idx, i = it2.j, j = it2.i;
+    const float4 px = k1s[o];
+    const float dh = px.x * ind;
+    Dh[o] = dh;
     if (Jb) {
+      const float u = ((float)j - cj) * inv_sf, vv = ((float)i - ci) * inv_sf;
+      const float jr[8] = {px.y * u, px.y * vv, px.z * u, px.z * vv, px.y, px.z, px.w * u, px.w * vv};
 #pragma unroll
       for (int q = 0; q < 8; ++q)
-        if (q < p) Jb[(size_t)q * mn + o] = (float)((jr[q] - dh * c[q]) * ind);
+        if (q < p) Jb[(size_t)q * mn + o] = fmaf(-dh, c[q], jr[q]) * ind;
     }
   }
 }

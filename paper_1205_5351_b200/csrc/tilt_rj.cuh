@@ -132,7 +132,9 @@ struct RJ {
   static constexpr int OFF_CP = OFF_LP + 64;
   static constexpr int OFF_LINV = (OFF_CP + 8 + 3) & ~3;
   static constexpr int OFF_SC = OFF_LINV + 128;  // per-call scalar scratch (16 words)
-  static constexpr int SMF = OFF_SC + 16;
+  static constexpr int LOGRING = 8;              // rounds of the rotation log staged in shared memory
+  static constexpr int OFF_RING = OFF_SC + 16;   // LOGRING x 32 float2 (cp.async staging of the log)
+  static constexpr int SMF = OFF_RING + LOGRING * 64;
   static constexpr int NPLANES = 8;       // D, A, E, Y, GX, GY, GZ, B (= M V)
   static_assert(NC % 2 == 0 && NC <= 52, "register budget: 4 NC + ~40 registers per lane");
   static_assert(Q % RR == 0, "the ring length must be a multiple of the body length");
@@ -521,19 +523,45 @@ __device__ __forceinline__ void sweep_b(u64 (&X)[NC], float2* Pw, float2* logp, 
   }
 }
 
-// Replay of a logged sweep on V (registers)
+__device__ __forceinline__ void cp_async8(void* smem_dst, const void* gmem_src) {
+  const uint32_t d = (uint32_t)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(gmem_src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// Replay of a logged sweep on V (registers). The log (global, written by sweep_b) is staged into a
+// shared ring of LOGRING rounds by cp.async, LOGRING - 1 rounds ahead of its use (each lane copies
+// its own float2 of a round), so the replay never waits on L2.
 template <int NC>
-__device__ __forceinline__ void sweep_v(u64 (&V)[NC], const float2* logp) {
+__device__ __forceinline__ void sweep_v(u64 (&V)[NC], const float2* logp, float* sm, int lane) {
   using R = RJ<NC>;
+  constexpr int NR = R::Q;  // rounds per sweep
+  constexpr int AHEAD = R::LOGRING - 1;
+  float2* ring = reinterpret_cast<float2*>(sm + R::OFF_RING);
+#pragma unroll
+  for (int r = 0; r < AHEAD; ++r) {
+    if (r < NR) cp_async8(ring + r * 32 + lane, logp + r * 32 + lane);
+    cp_async_commit();
+  }
 #pragma unroll 1
   for (int body = 0; body < R::NB; ++body) {
 #pragma unroll 1
     for (int r = 0; r < R::RR; ++r) {
-      const float4* P4 = reinterpret_cast<const float4*>(logp + (body * R::RR + r) * 32);
-      round_rot_dispatch<NC>(r, V, [&](int q) { return __ldcg(P4 + q); });
+      const int g = body * R::RR + r;
+      const int ahead = g + AHEAD;
+      if (ahead < NR) cp_async8(ring + (ahead % R::LOGRING) * 32 + lane, logp + ahead * 32 + lane);
+      cp_async_commit();
+      cp_async_wait<AHEAD>();  // round g has landed (this lane's part)
+      __syncwarp();            // ... and every other lane's part
+      const float4* P4 = reinterpret_cast<const float4*>(ring + (g % R::LOGRING) * 32);
+      round_rot_dispatch<NC>(r, V, [&](int q) { return P4[q]; });
+      __syncwarp();  // the slot is refilled LOGRING - 1 rounds later
     }
     ring_shift<NC>(V);
   }
+  cp_async_wait<0>();
 }
 
 // Singular value thresholding S_eps (Eqs. A_1, S_operator) of M, given B = M V in the
@@ -577,7 +605,7 @@ __device__ __noinline__ SvtRes svt_rj(float* Bp, float* Ap, float* sm, float2* l
     {
       u64 V[NC];
       load_vrows<NC>(sm, lane, V);
-      sweep_v<NC>(V, logp);
+      sweep_v<NC>(V, logp, sm, lane);
       scale_by_wv<NC, 1>(sm, V);
       vn = pair_norms<NC>(V, lane);
       store_vrows<NC>(sm, lane, V);
@@ -1027,7 +1055,7 @@ __device__ void solve_patch_rj(const SolveArgs& a, const W<NC>& w, int b) {
       sweeps_total += sst.sweeps;
       caps += sst.capped;
       rot_total += sst.rotations;
-      if (warm) ns_step<NC>(w.sm, w.Ts());
+      if (warm && (k % P.ns_period == P.ns_period - 1 || k + 1 == niter)) ns_step<NC>(w.sm, w.Ts());
       // E step: N_k = E_k - W^TW(A_{k+1} + E_k - D) - Y/mu, E_{k+1} = T_{lam/mu}(N_k)
       const float inv_mu = 1.f / mu;
       const float thr = lam * inv_mu;

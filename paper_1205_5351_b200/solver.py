@@ -150,7 +150,7 @@ class TiltSolver:
         n_images, H, W = images.shape
         self._bind_stream()
         check(lib.tilt_warp_batch(self._h, _ptr(images), n_images, H, W, _ptr(patch_image), _ptr(boxes_t),
-                                  _ptr(tau_t), B, kind, _ptr(dh), _ptr(J), _ptr(nrm), _ptr(st)), "tilt_warp_batch")
+                                  _ptr(tau_t), B, kind, m, n, _ptr(dh), _ptr(J), _ptr(nrm), _ptr(st)), "tilt_warp_batch")
         torch.cuda.synchronize(dev)
         return {"Dhat": dh, "J": J, "norm": nrm, "status": st}
 

@@ -52,17 +52,19 @@ def _replay_tensor(traces_per_patch, max_outer, max_inner, stops=False):
     return torch.as_tensor(arr, device="cuda")
 
 
-@pytest.mark.parametrize("path", [1, 2])
+@pytest.mark.parametrize("path,ns", [(1, 1), (2, 1), (1, 4)])
 @pytest.mark.parametrize("cfg_id,K", [(1, 20), (1, 50), (2, 20), (2, 50)])
-def test_fixed_count_parity(solver, T, cfg_id, K, path):
-    """path 1: CTA-per-patch kernel, path 2: warp-per-patch kernel (tilt_params.kernel_path)."""
+def test_fixed_count_parity(solver, T, cfg_id, K, path, ns):
+    """path 1: CTA-per-patch kernel, path 2: warp-per-patch kernel (tilt_params.kernel_path);
+    ns: Newton-Schulz period of the carried V (tilt_params.ns_period)."""
     cfg = ts.CONFIGS[cfg_id]
     B = 4
     b = ts.gen_batch(cfg, 0, B)
     prm_o = O.Params(fixed_inner_iters=K, fixed_outer_iters=1, max_inner=K, max_outer=1)
     refs = [O.tilt(b["images"][k], b["boxes"][k], b["tau0"][k], cfg.kind, prm_o) for k in range(B)]
     rr = _replay_tensor([r["traces"] for r in refs], 1, K)
-    prm = T.default_params(fixed_inner_iters=K, fixed_outer_iters=1, max_inner=K, max_outer=1, kernel_path=path)
+    prm = T.default_params(fixed_inner_iters=K, fixed_outer_iters=1, max_inner=K, max_outer=1, kernel_path=path,
+                           ns_period=ns)
     prm.rho_replay = rr.data_ptr()
     out = solver.solve(b["images"], b["patch_image"], b["boxes"], b["tau0"], cfg.kind, prm, want_Y=True)
     rep = T.reports_to_numpy(out["rep"])
@@ -76,6 +78,24 @@ def test_fixed_count_parity(solver, T, cfg_id, K, path):
         tau = out["tau"][k].double().cpu().numpy()
         assert np.max(np.abs(tau - refs[k]["tau"])) < 1e-3
         assert rep["inner_iters"][k] == K and rep["outer_iters"][k] == 1
+
+
+def test_fixed_count_parity_own_jacobi_oracle(solver, T):
+    """Fixed-count parity against the oracle running its own one-sided Jacobi SVD (Params.svd)."""
+    cfg = ts.CONFIGS[1]
+    K, B = 20, 2
+    b = ts.gen_batch(cfg, 0, B)
+    prm_o = O.Params(fixed_inner_iters=K, fixed_outer_iters=1, max_inner=K, max_outer=1, svd="jacobi")
+    refs = [O.tilt(b["images"][k], b["boxes"][k], b["tau0"][k], cfg.kind, prm_o) for k in range(B)]
+    rr = _replay_tensor([r["traces"] for r in refs], 1, K)
+    prm = T.default_params(fixed_inner_iters=K, fixed_outer_iters=1, max_inner=K, max_outer=1)
+    prm.rho_replay = rr.data_ptr()
+    out = solver.solve(b["images"], b["patch_image"], b["boxes"], b["tau0"], cfg.kind, prm)
+    for k in range(B):
+        a = out["A"][k].double().cpu().numpy()
+        e = out["E"][k].double().cpu().numpy()
+        assert np.linalg.norm(a - refs[k]["A"]) < 1e-4 * np.linalg.norm(refs[k]["A"])
+        assert np.linalg.norm(e - refs[k]["E"]) < 1e-4 * np.linalg.norm(refs[k]["E"])
 
 
 def _convergence_case(solver, T, cfg, idx_list, replay=True, path=0, **gen):

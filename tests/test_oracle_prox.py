@@ -97,3 +97,74 @@ def test_objective_closed_forms():
     e = np.zeros((4, 4))
     e[0, 0], e[1, 2], e[3, 3] = 1, -1, 1
     assert O.objective(np.zeros((4, 4)), e, 0.5) == pytest.approx(1.5)
+
+
+# ---------------------------------------------------------------------------------------------
+# The oracle's own one-sided Jacobi SVD (SURVEY.md §8(c) oracle step 5, P3)
+# ---------------------------------------------------------------------------------------------
+def _tiny_cases():
+    rng = np.random.default_rng(7)
+    cases = [np.eye(3), np.array([[2.0]]), np.zeros((3, 2)), np.diag([3.0, 3.0, 1.0])]  # repeated sigma
+    for (m, n) in [(1, 4), (4, 1), (2, 2), (3, 5), (5, 3), (8, 8)]:
+        cases.append(rng.normal(size=(m, n)))
+    u = rng.normal(size=(6, 2))
+    cases.append(u @ rng.normal(size=(2, 7)))  # rank 2 of 6 x 7
+    q, _ = np.linalg.qr(rng.normal(size=(5, 5)))
+    cases.append(q @ np.diag([2.0, 2.0, 2.0, 1e-9, 0.0]) @ q.T)  # repeated + near-zero + zero
+    return cases
+
+
+@pytest.mark.parametrize("k", range(12))
+def test_jacobi_svd_reconstruction_orthogonality(k):
+    w = _tiny_cases()[k]
+    u, s, v, sweeps = O.jacobi_svd(w)
+    scale = max(np.linalg.norm(w), 1.0)
+    assert np.linalg.norm(u * s @ v.T - w) <= 1e-12 * scale
+    assert np.linalg.norm(v.T @ v - np.eye(w.shape[1])) <= 1e-12
+    keep = s > 1e-9 * max(s.max(), 1e-300)
+    uk = u[:, keep]
+    assert np.linalg.norm(uk.T @ uk - np.eye(int(keep.sum()))) <= 1e-10
+    assert np.all(np.diff(s) <= 0) and np.all(s >= 0) and sweeps <= 60
+
+
+def test_jacobi_svd_identity_and_eigen():
+    # I_3 -> sigma = (1, 1, 1) with no rotation
+    _, s, _, sweeps = O.jacobi_svd(np.eye(3))
+    np.testing.assert_array_equal(s, [1.0, 1.0, 1.0])
+    assert sweeps == 1
+    # sigma^2 against an independent symmetric eigen-solver of M^T M (not the library SVD)
+    rng = np.random.default_rng(3)
+    for (m, n) in [(9, 6), (6, 9), (12, 12)]:
+        w = rng.normal(size=(m, n))
+        s = O.jacobi_svd(w)[1]
+        ev = np.sort(np.linalg.eigvalsh(w.T @ w))[::-1][:min(m, n)]
+        np.testing.assert_allclose(s[:min(m, n)] ** 2, ev, rtol=1e-9, atol=1e-10)
+
+
+def test_jacobi_svt_equals_library_svt_and_warm_start():
+    rng = np.random.default_rng(4)
+    w = rng.normal(size=(20, 16)) @ np.diag(np.linspace(3, 0.01, 16))
+    for eps in (0.0, 0.05, 0.7, 5.0):
+        a_j, s_j = O.svt(w, eps, "jacobi")
+        a_l, s_l = O.svt(w, eps, "lapack")
+        np.testing.assert_allclose(a_j, a_l, atol=1e-12 * np.linalg.norm(w))
+        np.testing.assert_allclose(s_j, s_l, atol=1e-12 * s_l[0])
+    # warm start from the right vectors of a nearby matrix: same SVD, fewer sweeps
+    _, _, v, cold = O.jacobi_svd(w)
+    w2 = w + 1e-4 * rng.normal(size=w.shape)
+    u2, s2, v2, warm = O.jacobi_svd(w2, v0=v)
+    assert warm < O.jacobi_svd(w2)[3]
+    np.testing.assert_allclose(u2 * s2 @ v2.T, w2, atol=1e-12 * np.linalg.norm(w2))
+
+
+def test_ladmap_same_with_own_jacobi_svd():
+    """A fixed count of LADMAP iterations with the oracle's Jacobi SVD equals the library-SVD run."""
+    import tilt_synth as ts
+    inst = ts.table1_instance(10, 6, 0)
+    proj = O.Projector(inst["J"])
+    mu0 = 1.25 / np.linalg.svd(inst["D"], compute_uv=False)[0]
+    z = np.zeros_like(inst["D"])
+    runs = [O.ladmap(inst["D"], proj, inst["lam"], mu0, 1e6 * mu0, 2.0, 1e-6, 0.1, 15, inst["D"].copy(), z, z,
+                     fixed_iters=15, svd=m) for m in ("lapack", "jacobi")]
+    np.testing.assert_allclose(runs[1].A, runs[0].A, atol=1e-10)
+    np.testing.assert_allclose(runs[1].E, runs[0].E, atol=1e-10)

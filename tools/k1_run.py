@@ -1,0 +1,10 @@
+import sys, os
+sys.path.insert(0, os.getcwd())
+import bench, json, numpy as np, torch
+import paper_1205_5351_b200 as T, tilt_synth as ts
+cfg = ts.CONFIGS[2]
+b = bench.gen_shard(2, 0, 1024)
+images = torch.as_tensor(b["images"], device="cuda"); pi = torch.as_tensor(b["patch_image"], device="cuda")
+boxes = torch.as_tensor(b["boxes"], device="cuda"); tau0 = torch.as_tensor(b["tau0"], device="cuda")
+s = T.TiltSolver(0, max_batch=1024, max_m=50, max_n=50, max_p=8, max_image_elems=int(images.numel()))
+print(json.dumps(bench.k1_roofline(s, images, pi, boxes, tau0, cfg.kind, 50, 50, 8, bench._peaks())))

@@ -22,12 +22,13 @@ ap.add_argument("--outer", type=int, default=1)
 ap.add_argument("--cfg", type=int, default=2)
 ap.add_argument("--reps", type=int, default=2)
 ap.add_argument("--path", type=int, default=0, help="tilt_params.kernel_path (0 auto, 1 CTA, 2 warp)")
+ap.add_argument("--ns", type=int, default=1, help="tilt_params.ns_period")
 a = ap.parse_args()
 cfg = ts.CONFIGS[a.cfg]
 b = ts.gen_batch(cfg, 0, a.batch)
 s = T.TiltSolver(0, max_batch=a.batch, max_m=cfg.m, max_n=cfg.n, max_p=cfg.p, max_image_elems=b["images"].size)
 prm = T.default_params(fixed_inner_iters=a.inner, fixed_outer_iters=a.outer, max_inner=max(a.inner, 1),
-                       max_outer=max(a.outer, 1), win_h=cfg.m, win_w=cfg.n, kernel_path=a.path)
+                       max_outer=max(a.outer, 1), win_h=cfg.m, win_w=cfg.n, kernel_path=a.path, ns_period=a.ns)
 ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 for r in range(a.reps):
     ev0.record()
@@ -42,5 +43,5 @@ m, n, p = cfg.m, cfg.n, cfg.p
 fl = it * (8 * p * m * n + 20 * m * n + 4 * m * n * n + 4 * n ** 3) + sw * n * (n - 1) / 2 * (12 * m + 6 * n)
 rot = rep["jacobi_rotations"].sum()
 pairs = sw * n * (n - 1) / 2
-print(f"path={a.path} cfg={a.cfg} batch={a.batch} inner={a.inner} outer={a.outer}: {ms:.3f} ms, {it} iters, {sw/it:.2f} sweeps/iter, "
+print(f"path={a.path} ns={a.ns} cfg={a.cfg} batch={a.batch} inner={a.inner} outer={a.outer}: {ms:.3f} ms, {it} iters, {sw/it:.2f} sweeps/iter, "
       f"{rot/max(pairs,1):.3f} rotations/pair-check, {it/ms*1e3:.0f} iters/s, {fl/ms/1e9:.2f} TFLOP/s (model)")
