@@ -169,7 +169,7 @@ def test_full_size_config2(solver, T):
     # sampled patches vs the oracle (outer count replayed)
     for k in (0, 517):
         r = O.tilt(b["images"][k], b["boxes"][k], b["tau0"][k], cfg.kind)
-        prm = T.default_params(fixed_outer_iters=max(1, r["outer_iters"]), kernel_path=path)
+        prm = T.default_params(fixed_outer_iters=max(1, r["outer_iters"]))
         rr = _replay_tensor([r["traces"]], prm.max_outer, prm.max_inner, stops=True)
         prm.rho_replay = rr.data_ptr()
         o1 = solver.solve(b["images"][k:k + 1], [0], b["boxes"][k:k + 1], b["tau0"][k:k + 1], cfg.kind, prm)
