@@ -335,8 +335,13 @@ def k1_roofline(solver, images, patch_image, boxes, tau0, kind, m, n, p, peaks) 
     byts = B * 4.0 * ((m + 1) * (n + 1) + m * n * (1 + p))
     achieved = byts / t / 1e9
     peak = float(peaks.get("hbm_gbs", 6650.0))
+    traffic = None
+    try:
+        traffic = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json"))).get("k_warp_dram_bytes_per_launch")
+    except Exception:
+        pass
     return {"bound": "hbm", "kernel": "k_warp", "achieved": achieved, "peak": peak, "unit": "GB/s",
-            "frac": achieved / peak, "traffic": None, "bytes_per_launch": byts, "us_per_launch": 1e6 * t,
+            "frac": achieved / peak, "traffic": traffic, "bytes_per_launch": byts, "us_per_launch": 1e6 * t,
             "note": "standalone K1 over the bench batch at tau0; L2 flushed before each timed launch (median of "
                     f"{reps})"}
 
