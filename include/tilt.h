@@ -100,8 +100,18 @@ typedef struct {
    * method; they differ only in data layout and Jacobi ordering. */
   int32_t kernel_path;
   /* Newton-Schulz re-orthonormalisation of the carried V (reading Z14) after every ns_period-th
-   * LADMAP SVT of an inner loop (and after the last one); <= 1: after every SVT. */
+   * LADMAP SVT of an inner loop (and after the last one); <= 1: after every SVT. Default 4 (the
+   * column scales are renormalised exactly every SVT; the slow orthogonality drift is corrected
+   * every 4th; fixed-count parity is tested at 1 and 4). */
   int32_t ns_period;
+  /* inner solver: 0 = LADMAP (the paper's), 1 = the ADM baseline of Zhang et al. as
+   * restated in P:241-264 (three variables, mu_{k+1} = adm_rho mu_k unbounded, cold start every outer
+   * iteration, dtau from the ADM). CTA kernels only. */
+  int32_t inner_solver;
+  float adm_rho;          /* ADM penalty growth (default 1.25) */
+  float adm_tol;          /* ADM stop: ||D + J dtau - A - E||_F / ||D||_F < adm_tol (default 1e-6: the
+                             fp32 residual floor is ~1e-7, as for eps1; the fp64 oracle reproduces
+                             Table 1's ADM counts at 1e-7) */
 } tilt_params;
 
 /* Per-patch report (device array written by tilt_solve_batch). */

@@ -56,6 +56,10 @@ class Params:
     fixed_inner_iters: int = 0  # >0: run exactly K inner iterations (test mode)
     fixed_outer_iters: int = 0  # >0: run exactly F outer iterations (test mode)
     svd: str = "lapack"         # SVD inside S_eps: "lapack" (library step) or "jacobi" (own, jacobi_svd)
+    inner: str = "ladmap"       # inner solver: "ladmap" (the paper's) or "adm" (the baseline of P:241-264)
+    adm_rho: float = 1.25       # ADM penalty growth mu_{k+1} = rho mu_k, unbounded (reading Z24)
+    adm_tol: float = 1e-6       # ADM stop: ||D + J dtau - A - E||_F / ||D||_F < adm_tol (reading Z24;
+                                # 1e-7 reproduces Table 1's ADM counts in fp64, 1e-6 is fp32-resolvable)
 
 
 # ----------------------------------------------------------------------------------------------
@@ -413,6 +417,57 @@ def ladmap(dh, proj, lam, mu0, mu_max, rho0, eps1, eps2, max_inner, a0, e0, y0,
 
 
 # ----------------------------------------------------------------------------------------------
+# ADM baseline inner loop (Zhang et al., as restated in P:241-264)
+# ----------------------------------------------------------------------------------------------
+
+@dataclass
+class AdmResult:
+    A: np.ndarray
+    E: np.ndarray
+    Y: np.ndarray
+    dtau: np.ndarray
+    iters: int
+    mu: float               # mu_k of the last iteration's updates
+    sigma_m: np.ndarray     # singular values of the last SVT argument
+    resid: float            # ||D + J dtau - A - E||_F / ||D||_F at exit
+    converged: bool = False
+
+
+def adm(dh, proj, lam, mu0, rho, tol, max_inner, fixed_iters=0):
+    """Gauss-Seidel ADM on the augmented Lagrangian of Eq. TILT_3:
+        A_{k+1}   = argmin_A L = S_{1/mu_k}(D + J dtau_k - E_k + Y_k/mu_k)        (Eq. update_A, cf. Eq. A_1)
+        E_{k+1}   = argmin_E L = T_{lam/mu_k}(D + J dtau_k - A_{k+1} + Y_k/mu_k)  (Eq. update_E, cf. Eq. E_1)
+        dtau_{k+1} = argmin_dtau L = G^{-1} J^T (A_{k+1} + E_{k+1} - D - Y_k/mu_k) (Eq. update_detla_Tau;
+                     with the constraint rows Q the stacked least squares of P:671-684: G = J^TJ + Q^TQ)
+        Y_{k+1}   = Y_k + mu_k (D + J dtau_{k+1} - A_{k+1} - E_{k+1})
+        mu_{k+1}  = rho mu_k  (unbounded)
+    initialised A_0 = D, E_0 = 0, Y_0 = 0, dtau_0 = 0. Stops when the constraint
+    residual ||D + J dtau - A - E||_F/||D||_F < tol (reading Z24) unless ``fixed_iters`` > 0.
+    """
+    a, e, y = dh.copy(), np.zeros_like(dh), np.zeros_like(dh)
+    dtau = np.zeros(proj.jm.shape[1])
+    jdt = np.zeros_like(dh)
+    nd = float(np.linalg.norm(dh)) or 1.0
+    mu = mu0
+    n_iter = fixed_iters if fixed_iters > 0 else max_inner
+    sig = None
+    resid = float("nan")
+    for k in range(n_iter):
+        a, sig = svt(dh + jdt - e + y / mu, 1.0 / mu)
+        e = shrink(dh + jdt - a + y / mu, lam / mu)
+        dtau = proj.delta_tau(a + e - dh - y / mu)
+        jdt = (proj.jm @ dtau).reshape(dh.shape)
+        r = dh + jdt - a - e
+        y = y + mu * r
+        resid = float(np.linalg.norm(r)) / nd
+        mu_used = mu
+        mu = rho * mu
+        if resid < tol and fixed_iters <= 0:
+            return AdmResult(a, e, y, dtau, k + 1, mu_used, sig, resid, True)
+    return AdmResult(a, e, y, dtau, n_iter, mu / rho, sig, resid, resid < tol)
+
+
+# ----------------------------------------------------------------------------------------------
 # Algorithm 1 (P:527-574): TILT via LADMAP + VWS
 # ----------------------------------------------------------------------------------------------
 
@@ -468,19 +523,27 @@ def tilt(image, box, tau0, kind, prm: Params = Params(), rho_replay=None):
         except Projector.SingularGram:
             status = SINGULAR_GRAM
             break
-        if a is None or not prm.vws:
-            a, e, y = dh.copy(), np.zeros_like(dh), np.zeros_like(dh)
-        else:
-            y = proj.apply(y)                      # Eq. Y_new_warmstart
         sigma1 = float(np.linalg.svd(dh, compute_uv=False)[0])
         mu0 = prm.mu0_scale / sigma1
-        replay = rho_replay[it] if rho_replay is not None and it < len(rho_replay) else None
-        res = ladmap(dh, proj, lam, mu0, prm.mu_max_ratio * mu0, prm.rho0, prm.eps1, prm.eps2,
-                     prm.max_inner, a, e, y, fixed_iters=prm.fixed_inner_iters, rho_replay=replay, svd=prm.svd)
-        a, e, y = res.A, res.E, res.Y
-        inner_iters += res.iters
-        outer_traces.append(res.trace)
-        dtau = proj.delta_tau(a + e - dh)          # Step 3
+        if prm.inner == "adm":
+            # the original method: cold start every outer iteration, dtau from the ADM
+            res = adm(dh, proj, lam, mu0, prm.adm_rho, prm.adm_tol, prm.max_inner, fixed_iters=prm.fixed_inner_iters)
+            a, e, y = res.A, res.E, res.Y
+            inner_iters += res.iters
+            outer_traces.append([])
+            dtau = res.dtau
+        else:
+            if a is None or not prm.vws:
+                a, e, y = dh.copy(), np.zeros_like(dh), np.zeros_like(dh)
+            else:
+                y = proj.apply(y)                      # Eq. Y_new_warmstart
+            replay = rho_replay[it] if rho_replay is not None and it < len(rho_replay) else None
+            res = ladmap(dh, proj, lam, mu0, prm.mu_max_ratio * mu0, prm.rho0, prm.eps1, prm.eps2,
+                         prm.max_inner, a, e, y, fixed_iters=prm.fixed_inner_iters, rho_replay=replay, svd=prm.svd)
+            a, e, y = res.A, res.E, res.Y
+            inner_iters += res.iters
+            outer_traces.append(res.trace)
+            dtau = proj.delta_tau(a + e - dh)          # Step 3
         tau = tau + dtau                           # Step 4
         dtau_inf = float(np.max(np.abs(dtau)))
         f = float(shrink(res.sigma_m, 1.0 / res.mu).sum()) + lam * float(np.abs(e).sum())
@@ -506,7 +569,8 @@ def tilt(image, box, tau0, kind, prm: Params = Params(), rho_replay=None):
         "status": status, "stop_rule": stop_rule, "tau": tau, "A": a, "E": e, "Y": y,
         "outer_iters": it_done, "inner_iters": inner_iters, "objective": f,
         "rank": rank, "rank_band": band, "svt_rank": int(np.sum(res.sigma_m > 1.0 / res.mu)) if res else 0,
-        "crit1": res.crit1 if res else float("nan"), "crit2": res.crit2 if res else float("nan"),
+        "crit1": (res.resid if isinstance(res, AdmResult) else res.crit1) if res else float("nan"),
+        "crit2": (float("nan") if isinstance(res, AdmResult) else res.crit2) if res else float("nan"),
         "patch_norm": nd, "dtau_inf": dtau_inf, "traces": outer_traces, "lam": lam,
     }
 

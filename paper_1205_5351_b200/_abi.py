@@ -44,6 +44,9 @@ class TiltParams(ctypes.Structure):
         ("win_w", ctypes.c_int32),
         ("kernel_path", ctypes.c_int32),
         ("ns_period", ctypes.c_int32),
+        ("inner_solver", ctypes.c_int32),
+        ("adm_rho", ctypes.c_float),
+        ("adm_tol", ctypes.c_float),
     ]
 
 

@@ -98,6 +98,9 @@ DevParams to_dev(const tilt_params* prm) {
   P.fixed_inner = prm->fixed_inner_iters;
   P.fixed_outer = prm->fixed_outer_iters;
   P.ns_period = prm->ns_period > 1 ? prm->ns_period : 1;
+  P.inner_solver = prm->inner_solver;
+  P.adm_rho = prm->adm_rho;
+  P.adm_tol = prm->adm_tol;
   P.rho_replay = prm->rho_replay;
   P.trace = prm->trace;
   return P;
@@ -116,6 +119,9 @@ bool params_ok(const tilt_params* p) {
   if (p->pyramid_levels < 1 || p->pyramid_levels > 2) return false;
   if (p->constraint_mode != TILT_CONSTRAINTS_NONE && p->constraint_mode != TILT_CONSTRAINTS_CENTER_AREA) return false;
   if (p->kernel_path < 0 || p->kernel_path > 2) return false;
+  if (p->inner_solver < 0 || p->inner_solver > 1) return false;
+  if (p->inner_solver == 1 && p->kernel_path == 2) return false;  // the warp-per-patch kernel runs LADMAP only
+  if (!std::isfinite(p->adm_rho) || !std::isfinite(p->adm_tol) || p->adm_rho < 1.f || p->adm_tol <= 0.f) return false;
   return true;
 }
 
@@ -335,6 +341,10 @@ tilt_status tilt_default_params(tilt_params* prm) {
   prm->pyramid_levels = 1;
   prm->jacobi_tol = 0.f;
   prm->jacobi_max_sweeps = 20;
+  prm->ns_period = 4;
+  prm->inner_solver = 0;
+  prm->adm_rho = 1.25f;
+  prm->adm_tol = 1e-6f;
   return TILT_OK;
 }
 
@@ -463,7 +473,7 @@ static tilt_status solve_level(tilt_handle* h, const float* images, int32_t n_im
     g_last_error = "kernel_path = 2 (warp-per-patch) needs m <= 64 and n <= 50";
     return TILT_E_ARG;
   }
-  if (rj_ok && prm->kernel_path == 2) return tilt::rjh::solve(h->num_sms, h->ws, h->ws_floats, h->counter, h->stream, a, &h->launches, &g_last_error);
+  if (rj_ok && prm->kernel_path == 2 && prm->inner_solver == 0) return tilt::rjh::solve(h->num_sms, h->ws, h->ws_floats, h->counter, h->stream, a, &h->launches, &g_last_error);
   return dispatch<SolveF>(size_class(m, n), h, a);
 }
 

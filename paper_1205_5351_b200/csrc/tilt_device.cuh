@@ -54,6 +54,8 @@ struct DevParams {
   int jacobi_max_sweeps;
   int fixed_inner, fixed_outer;
   int ns_period;
+  int inner_solver;      // 0 LADMAP (the paper's), 1 ADM baseline
+  float adm_rho, adm_tol;
   const uint8_t* rho_replay;
   float* trace;
 };
@@ -146,6 +148,7 @@ __device__ __forceinline__ void block_sum_d(double (&v)[KV], Scal* sc) {
 template <class C>
 struct Ctx {
   float *D, *A, *E, *Y;  // planes (col-major, ld)
+  float* T;              // J dtau (ADM baseline)
   float *G;              // implicit projector: GX, GY, GZ planes; explicit: K (p planes)
   float *B, *V, *S;      // SVD buffers (col-major, ld)
   float4* ns;            // (norm^2, scale, 1/scale, -) per Jacobi column

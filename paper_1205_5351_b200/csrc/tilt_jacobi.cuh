@@ -370,8 +370,8 @@ __device__ __noinline__ int jacobi_sweeps_smem(float* Bp, float* Vp, float4* nsp
         xj.sstore(aj, cmr);
         // V columns after B's are stored: only two columns live in registers at a time
         Col<RPL, L> yi, yj;
-        yi.sload_full(vi);
-        yj.sload_full(vj);
+        yi.sload(vi, cmr);  // only units that rotate read (and write) their V columns
+        yj.sload(vj, cmr);
 #pragma unroll
         for (int e = 0; e < RPL; ++e) {
           const float o = yi.v[e];

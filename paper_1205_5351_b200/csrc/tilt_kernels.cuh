@@ -14,7 +14,7 @@ template <class C>
 struct Layout {
   static __host__ __device__ size_t vec_floats() { return 5 * (size_t)C::MAXD; }
   static __host__ __device__ size_t svd_floats(int, int n) { return 3 * (size_t)C::MAXD * n; }
-  static __host__ __device__ size_t plane_floats(int ld, int n, int gplanes) { return (size_t)(4 + gplanes) * ld * n; }
+  static __host__ __device__ size_t plane_floats(int ld, int n, int gplanes) { return (size_t)(5 + gplanes) * ld * n; }
   static __host__ __device__ size_t smem_bytes(int ld, int n, int gplanes) {
     size_t s = vec_floats();
     if (C::SVD_SMEM) s += svd_floats(ld, n);
@@ -62,7 +62,8 @@ __device__ __forceinline__ Ctx<C> make_ctx(float* smem, float* ws, Scal* sc, int
   cx.A = pl + blk;
   cx.E = pl + 2 * blk;
   cx.Y = pl + 3 * blk;
-  cx.G = pl + 4 * blk;
+  cx.T = pl + 4 * blk;  // J dtau of the ADM baseline
+  cx.G = pl + 5 * blk;
   cx.sc = sc;
   cx.m = m;
   cx.n = n;
@@ -213,6 +214,98 @@ __device__ InnerOut ladmap_inner(Ctx<C>& cx, const DevParams& P, float lam, floa
   return o;
 }
 
+// ---------------------------------------------------------------------------------------------
+// ADM baseline inner loop (Zhang et al.), Gauss-Seidel on the
+// augmented Lagrangian of Eq. TILT_3 with the penalty mu_{k+1} = rho mu_k (unbounded):
+//   A_{k+1} = S_{1/mu}(D + J dtau_k - E_k + Y_k/mu)
+//   E_{k+1} = T_{lam/mu}(D + J dtau_k - A_{k+1} + Y_k/mu)
+//   dtau_{k+1} = G^{-1} J^T v, v = A_{k+1} + E_{k+1} - D - Y_k/mu   (J dtau = K K^T v)
+//   Y_{k+1} = Y_k + mu (D + J dtau_{k+1} - A_{k+1} - E_{k+1})
+// stop when ||D + J dtau - A - E||_F / ||D||_F < adm_tol (reading Z24). Cold start A = D,
+// E = Y = 0, J dtau = 0. Returns K^T v of the last dtau step in s_last.
+// ---------------------------------------------------------------------------------------------
+template <class C, class PR>
+__device__ InnerOut adm_inner(Ctx<C>& cx, const DevParams& P, float lam, float mu0, float tol, float (&s_last)[8]) {
+  const int ld = cx.ld, pl = cx.pl;
+  const int niter = P.fixed_inner > 0 ? P.fixed_inner : P.max_inner;
+  float* __restrict__ Ap = cx.A;
+  float* __restrict__ Ep = cx.E;
+  float* __restrict__ Yp = cx.Y;
+  float* __restrict__ Tp = cx.T;
+  const float* __restrict__ Dp = cx.D;
+  for (int idx = threadIdx.x; idx < pl; idx += C::NT) {
+    Ap[idx] = Dp[idx];
+    Ep[idx] = 0.f;
+    Yp[idx] = 0.f;
+    Tp[idx] = 0.f;
+  }
+  float nd2 = 0.f;
+  for (int idx = threadIdx.x; idx < pl; idx += C::NT) nd2 = fmaf(Dp[idx], Dp[idx], nd2);
+  float nn[1] = {nd2};
+  block_sum_f<C, 1>(nn, cx.sc);
+  const float inv_nd = nn[0] > 0.f ? rsqrtf(nn[0]) : 1.f;
+  InnerOut o;
+  o.iters = o.sweeps = o.caps = o.rotations = 0;
+  o.crit1 = o.crit2 = __int_as_float(0x7fc00000);
+  o.converged = false;
+  float mu = mu0;
+  o.mu = mu;
+  const bool warm = P.svd_warm != 0;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) s_last[q] = 0.f;
+  for (int k = 0; k < niter; ++k) {
+    const float inv_mu = 1.f / mu;
+    // A step: S <- D + J dtau - E + Y/mu, A = S_{1/mu}(S)
+    for (PixIter pi(threadIdx.x, C::NT, ld); pi.idx < pl; pi.next(C::NT)) {
+      const int idx = pi.idx;
+      cx.S[pi.j * cx.lds + pi.i] = fmaf(Yp[idx], inv_mu, Dp[idx] + Tp[idx] - Ep[idx]);
+    }
+    __syncthreads();
+    SvtOut so = svt<C, true>(
+        cx, cx.S, inv_mu, tol, P.jacobi_max_sweeps, warm,
+        [&](int i0, int j, float4 a) { *reinterpret_cast<float4*>(Ap + j * ld + i0) = a; },
+        warm && (k % P.ns_period == P.ns_period - 1 || k + 1 == niter));
+    o.sweeps += so.sweeps;
+    o.caps += so.capped ? 1 : 0;
+    o.rotations += so.rotations;
+    // E step
+    const float thr = lam * inv_mu;
+    for (int idx = threadIdx.x; idx < pl; idx += C::NT) {
+      const float x = fmaf(Yp[idx], inv_mu, Dp[idx] + Tp[idx] - Ap[idx]);
+      Ep[idx] = copysignf(fmaxf(fabsf(x) - thr, 0.f), x);
+    }
+    __syncthreads();
+    // dtau step: J dtau = K K^T v
+    float s[8], z[9];
+    auto vf = [&](int idx) { return fmaf(-Yp[idx], inv_mu, Ap[idx] + Ep[idx] - Dp[idx]); };
+    PR::reduce(cx, vf, s);
+    PR::coeffs(cx, s, z);
+    float r2 = 0.f;
+    for (PixIter pi(threadIdx.x, C::NT, ld); pi.idx < pl; pi.next(C::NT)) {
+      const int idx = pi.idx;
+      const float jdt = PR::apply(cx, idx, pi.i, pi.j, z);
+      Tp[idx] = jdt;
+      const float r = Dp[idx] + jdt - Ap[idx] - Ep[idx];
+      Yp[idx] = fmaf(mu, r, Yp[idx]);
+      r2 = fmaf(r, r, r2);
+    }
+    float rr[1] = {r2};
+    block_sum_f<C, 1>(rr, cx.sc);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) s_last[q] = s[q];
+    const float resid = sqrtf(rr[0]) * inv_nd;
+    o.iters = k + 1;
+    o.crit1 = resid;
+    o.mu = mu;
+    mu *= P.adm_rho;
+    if (resid < P.adm_tol) {
+      o.converged = true;
+      if (P.fixed_inner <= 0) break;
+    }
+  }
+  return o;
+}
+
 // X <- W^TW X (in place)
 template <class C, class PR>
 __device__ __forceinline__ void project_plane(Ctx<C>& cx, float* X) {
@@ -328,7 +421,7 @@ __device__ void solve_patch(const SolveArgs& a, Ctx<C>& cx, int b) {
   const float tol = P.jacobi_tol > 0.f ? P.jacobi_tol : default_jacobi_tol(m);
   const bool warm = P.svd_warm != 0;
   const int gpl = p == 8 ? 3 : 2;
-  zero_planes<C>(cx.D, (size_t)(4 + gpl) * pl);  // padding rows stay 0 from here on
+  zero_planes<C>(cx.D, (size_t)(5 + gpl) * pl);  // padding rows stay 0 from here on
   set_identity<C>(cx.V, cx.lds, n);
   __syncthreads();
   int status = TILT_PATCH_MAX_OUTER, stop_rule = 0, outer = 0, inner_total = 0, sweeps_total = 0,
@@ -384,11 +477,16 @@ __device__ void solve_patch(const SolveArgs& a, Ctx<C>& cx, int b) {
     aux_total += aux;
     const float mu0 = s1 > 0.f ? P.mu0_scale / s1 : P.mu0_scale;
     const float mu_max = P.mu_max_ratio * mu0;
-    write_m0<C, PR>(cx, mu0);
     const size_t toff = ((size_t)b * P.max_outer + it) * P.max_inner;
-    const InnerOut io = ladmap_inner<C, PR>(cx, P, lam, mu0, mu_max, denom, tol,
-                                            P.rho_replay ? P.rho_replay + toff : nullptr,
-                                            P.trace ? P.trace + 4 * toff : nullptr);
+    float s_adm[8];
+    InnerOut io;
+    if (P.inner_solver == 1) {
+      io = adm_inner<C, PR>(cx, P, lam, mu0, tol, s_adm);
+    } else {
+      write_m0<C, PR>(cx, mu0);
+      io = ladmap_inner<C, PR>(cx, P, lam, mu0, mu_max, denom, tol, P.rho_replay ? P.rho_replay + toff : nullptr,
+                               P.trace ? P.trace + 4 * toff : nullptr);
+    }
     have_state = true;
     inner_total += io.iters;
     sweeps_total += io.sweeps;
@@ -403,7 +501,12 @@ __device__ void solve_patch(const SolveArgs& a, Ctx<C>& cx, int b) {
     svt_rank = cx.sc->svt_rank;
     // Step 3: dtau = G^{-1} J^T (A + E - D_hat) = L^{-T} K^T (A + E - D_hat)  (Eq. Delta_tau)
     float s[8];
-    PR::reduce(cx, [&](int idx) { return cx.A[idx] + cx.E[idx] - cx.D[idx]; }, s);
+    if (P.inner_solver == 1) {  // the ADM's own dtau (Eq. update_detla_Tau)
+#pragma unroll
+      for (int q = 0; q < 8; ++q) s[q] = s_adm[q];
+    } else {
+      PR::reduce(cx, [&](int idx) { return cx.A[idx] + cx.E[idx] - cx.D[idx]; }, s);
+    }
     const float l1 = plane_l1<C>(cx, cx.E);
     const double* Li = cx.sc->Linv;
     double dt_inf = 0.0;
@@ -549,10 +652,16 @@ __global__ void __launch_bounds__(C::NT, 1) k_inner(InnerArgs a) {
       int aux = 0;
       const float s1 = sigma1_of_plane<C>(cx, cx.D, tol, P.jacobi_max_sweeps, P.svd_warm != 0, &aux);
       const float mu0 = s1 > 0.f ? P.mu0_scale / s1 : P.mu0_scale;
-      write_m0<C, PR>(cx, mu0);
-      const InnerOut io = ladmap_inner<C, PR>(cx, P, lam, mu0, P.mu_max_ratio * mu0, denom, tol,
-                                              P.rho_replay ? P.rho_replay + (size_t)b * P.max_inner : nullptr,
-                                              P.trace ? P.trace + (size_t)4 * b * P.max_inner : nullptr);
+      InnerOut io;
+      float s_adm[8];
+      if (P.inner_solver == 1) {
+        io = adm_inner<C, PR>(cx, P, lam, mu0, tol, s_adm);
+      } else {
+        write_m0<C, PR>(cx, mu0);
+        io = ladmap_inner<C, PR>(cx, P, lam, mu0, P.mu_max_ratio * mu0, denom, tol,
+                                 P.rho_replay ? P.rho_replay + (size_t)b * P.max_inner : nullptr,
+                                 P.trace ? P.trace + (size_t)4 * b * P.max_inner : nullptr);
+      }
       const float nuc = cx.sc->svt_nuc;
       rr.rank = cx.sc->svt_relrank;
       rr.rank_band = cx.sc->svt_band;

@@ -266,6 +266,77 @@ __device__ __forceinline__ u64 proj_apply(const W<NC>& w, int j, const float (&z
   return fmas2(w.ld(w.D(), j), -z[8], r);
 }
 
+// Projector factors of one column (lane rows), loaded once and shared by apply + accumulate
+struct ColG {
+  u64 gx, gy, gz, d;
+  float u;
+};
+
+template <int NC>
+__device__ __forceinline__ ColG load_g(const W<NC>& w, const float* __restrict__ GX, const float* __restrict__ GY,
+                                       const float* __restrict__ GZ, const float* __restrict__ Dp, int j) {
+  ColG c;
+  c.gx = w.ld(GX, j);
+  c.gy = w.ld(GY, j);
+  c.gz = w.p == 8 ? w.ld(GZ, j) : 0ull;
+  c.d = w.ld(Dp, j);
+  c.u = w.ucol(j);
+  return c;
+}
+
+// (K z) at a column from its factors (as proj_apply)
+template <int NC>
+__device__ __forceinline__ u64 apply_g(const W<NC>& w, const ColG& c, const float (&z)[9]) {
+  const float s1 = fmaf(z[0], c.u, z[4]), s2 = fmaf(z[2], c.u, z[5]), s3 = z[6] * c.u;
+  u64 r = mul2(c.gx, fmas2(w.vv, z[1], pk(s1, s1)));
+  r = fma2(c.gy, fmas2(w.vv, z[3], pk(s2, s2)), r);
+  r = fma2(c.gz, fmas2(w.vv, z[7], pk(s3, s3)), r);  // gz = 0 for affine
+  return fmas2(c.d, -z[8], r);
+}
+
+// accumulate the 9 projector sums of a column value (as proj_s)
+__device__ __forceinline__ void accum_g(const ColG& c, u64 vv, u64 val, u64 (&a)[9]) {
+  const u64 ga = mul2(c.gx, val), gb = mul2(c.gy, val), gc = mul2(c.gz, val);
+  a[0] = fmas2(ga, c.u, a[0]);
+  a[1] = fma2(ga, vv, a[1]);
+  a[2] = fmas2(gb, c.u, a[2]);
+  a[3] = fma2(gb, vv, a[3]);
+  a[4] = add2(a[4], ga);
+  a[5] = add2(a[5], gb);
+  a[6] = fmas2(gc, c.u, a[6]);
+  a[7] = fma2(gc, vv, a[7]);
+  a[8] = fma2(c.d, val, a[8]);
+}
+
+// warp-reduce the sums and form z (as proj_z)
+template <int NC>
+__device__ __forceinline__ void finish_z(const W<NC>& w, const u64 (&a)[9], float (&z)[9]) {
+  float r[9];
+#pragma unroll
+  for (int k = 0; k < 9; ++k) r[k] = wsum(hsum(a[k]));
+  const float* Lp = w.Lp();
+  const float* cp = w.cp();
+  float s[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    float acc = -cp[q] * r[8];
+#pragma unroll
+    for (int b = 0; b <= q; ++b) acc = fmaf(Lp[q * 8 + b], r[b], acc);
+    s[q] = acc;
+  }
+#pragma unroll
+  for (int b = 0; b < 8; ++b) {
+    float acc = 0.f;
+#pragma unroll
+    for (int q = b; q < 8; ++q) acc = fmaf(Lp[q * 8 + b], s[q], acc);
+    z[b] = acc;
+  }
+  float ww = 0.f;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) ww = fmaf(cp[q], s[q], ww);
+  z[8] = ww;
+}
+
 // ---------------------------------------------------------------------------------------------
 // Warm one-sided Jacobi, circle (round-robin) ordering, deferred V.
 // A sweep first rotates only B (X, lane rows in registers): column pairs of a round are static
@@ -1056,21 +1127,28 @@ __device__ void solve_patch_rj(const SolveArgs& a, const W<NC>& w, int b) {
       caps += sst.capped;
       rot_total += sst.rotations;
       if (warm && (k % P.ns_period == P.ns_period - 1 || k + 1 == niter)) ns_step<NC>(w.sm, w.Ts());
-      // E step: N_k = E_k - W^TW(A_{k+1} + E_k - D) - Y/mu, E_{k+1} = T_{lam/mu}(N_k)
+      // E step: N_k = E_k - W^TW(A_{k+1} + E_k - D) - Y/mu, E_{k+1} = T_{lam/mu}(N_k); the same
+      // pass accumulates the projector sums of A_{k+1} + E_{k+1} - D for the dual step
       const float inv_mu = 1.f / mu;
       const float thr = lam * inv_mu;
+      const float *__restrict__ GXp = w.GX(), *__restrict__ GYp = w.GY(), *__restrict__ GZp = w.GZ();
       proj_z<NC>(w, [&](int j) { return sub2(add2(w.ld(Ap, j), w.ld(Ep, j)), w.ld(Dp, j)); }, z);
       float dE2 = 0.f;
-#pragma unroll 2
+      u64 acc[9];
+#pragma unroll
+      for (int q = 0; q < 9; ++q) acc[q] = 0ull;
+#pragma unroll 4
       for (int j = 0; j < n; ++j) {
-        const u64 e = w.ld(Ep, j);
-        const u64 v = sub2(add2(w.ld(Ap, j), e), w.ld(Dp, j));
-        const u64 pv = sub2(v, proj_apply<NC>(w, j, z));
-        const u64 nk = fmas2(w.ld(Yp, j), -inv_mu, sub2(e, pv));
+        const ColG cg = load_g<NC>(w, GXp, GYp, GZp, Dp, j);
+        const u64 e = w.ld(Ep, j), av = w.ld(Ap, j), yv = w.ld(Yp, j);
+        const u64 v = sub2(add2(av, e), cg.d);
+        const u64 pv = sub2(v, apply_g<NC>(w, cg, z));
+        const u64 nk = fmas2(yv, -inv_mu, sub2(e, pv));
         const u64 en = shrink2(nk, thr);
         const u64 d = sub2(en, e);
         dE2 += hsum(mul2(d, d));
         w.st(Ep, j, en);
+        accum_g(cg, w.vv, sub2(add2(av, en), cg.d), acc);
       }
       dE2 = wsum(dE2);
       const float c2 = mu * sqrtf(fmaxf(sst.dA2, dE2)) * inv_den;
@@ -1079,7 +1157,7 @@ __device__ void solve_patch_rj(const SolveArgs& a, const W<NC>& w, int b) {
       const float mu_next = fminf(mu_max, rho_bit ? P.rho0 * mu : mu);
       const float inv_mun = 1.f / mu_next;
       // dual step (Y += mu R, erratum E1) + next M = A - R - Y/mu_next, B = M V
-      proj_z<NC>(w, [&](int j) { return sub2(add2(w.ld(Ap, j), w.ld(Ep, j)), w.ld(Dp, j)); }, z);
+      finish_z<NC>(w, acc, z);
       float c1 = 0.f;
       build_b<NC>(w, w.Bm(), [&](int kk, u64& m0, u64& m1) {
         u64 mk[2];
@@ -1090,9 +1168,10 @@ __device__ void solve_patch_rj(const SolveArgs& a, const W<NC>& w, int b) {
             mk[h] = 0ull;
             continue;
           }
+          const ColG cg = load_g<NC>(w, GXp, GYp, GZp, Dp, j);
           const u64 av = w.ld(Ap, j);
-          const u64 v = sub2(add2(av, w.ld(Ep, j)), w.ld(Dp, j));
-          const u64 r = sub2(v, proj_apply<NC>(w, j, z));
+          const u64 v = sub2(add2(av, w.ld(Ep, j)), cg.d);
+          const u64 r = sub2(v, apply_g<NC>(w, cg, z));
           const u64 y = fmas2(r, mu, w.ld(Yp, j));
           w.st(Yp, j, y);
           c1 += hsum(mul2(r, r));
