@@ -90,3 +90,21 @@ def test_tilt_with_adm_inner_fixed_count(solver, T):
         assert np.linalg.norm(a - refs[k]["A"]) < 1e-4 * np.linalg.norm(refs[k]["A"])
         assert np.linalg.norm(e - refs[k]["E"]) < 1e-4 * np.linalg.norm(refs[k]["E"])
         assert np.max(np.abs(out["tau"][k].double().cpu().numpy() - refs[k]["tau"])) < 1e-4
+
+
+def test_range_of_convergence_grid_batched(solver, T):
+    """Fig. 2's grid as one batched solve per inner solver; small deformations are
+    rectified by both, and sampled cells agree with the fp64 oracle (tau within 2e-3)."""
+    from tilt_synth.metrics import rectified
+    g = ts.convergence_grid(32, 8)
+    nt, ns = len(g["thetas"]), len(g["skews"])
+    for sid in (0, 1):
+        out = solver.solve(g["images"], g["patch_image"], g["boxes"], g["tau0"], T.AFFINE,
+                           T.default_params(inner_solver=sid))
+        tau = out["tau"].double().cpu().numpy()
+        ok = np.array([rectified(tau[k], g["tau_g"][k]) for k in range(nt * ns)]).reshape(nt, ns)
+        assert ok[:3, :5].all(), ok[:3, :5]  # theta <= 6 deg, t <= 0.2
+        for k in (6, 70, 144):
+            r = O.tilt(g["images"][k], g["boxes"][k], g["tau0"][k], O.AFFINE,
+                       O.Params(inner="adm" if sid else "ladmap"))
+            assert np.max(np.abs(r["tau"] - tau[k])) < 2e-3, (sid, k)

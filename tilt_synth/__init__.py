@@ -222,3 +222,33 @@ def lowrank_sparse(m: int, n: int, rank: int, seed: int, frac: float = 0.05) -> 
     x.reshape(-1)[sel] += rng.normal(0, 3.0, size=k)
     x += 1e-3 * rng.normal(size=(m, n))
     return x / np.linalg.norm(x)
+
+
+def checkerboard_case(theta: float, skew: float, m: int = 32, square_px: int = 8, supersample: int = 4) -> dict:
+    """Fig. 2's range-of-convergence input: a standard 0/1 checker-board
+    (squares of ``square_px`` window pixels) deformed by y = A(theta, t) x, A(theta, t) =
+    R(theta) [[1, t], [0, 1]], on a 2m x 2m canvas with the central m x m window; no corruption.
+    The checker-board is T(u, v) = (1 + s(u) s(v)) / 2 with s a +-1 square wave (rank 2)."""
+    big = m
+    length = 8 * big
+    wave = np.where((np.arange(length) // square_px) % 2 == 0, 1.0, -1.0)
+    ones = np.ones(length)
+    h_g = planted_transform(theta, skew)
+    x0 = y0 = m // 2
+    canvas = render_texture([ones, wave], [ones, wave], h_g, m, m, (x0, y0), (2 * m, 2 * m), supersample)
+    return {"canvas": canvas.astype(np.float32), "box": np.array([x0, y0, m, m], dtype=np.int32),
+            "tau0": identity_tau(AFFINE), "tau_g": tau_from_h(h_g, AFFINE), "theta": theta, "skew": skew}
+
+
+def convergence_grid(m: int = 32, square_px: int = 8) -> dict:
+    """The Fig. 2 grid: theta in [0, pi/6] step pi/60, t in [0, 1] step 0.05."""
+    thetas = [k * math.pi / 60 for k in range(11)]
+    skews = [round(0.05 * k, 2) for k in range(21)]
+    cases = [checkerboard_case(th, t, m, square_px) for th in thetas for t in skews]
+    return {"thetas": thetas, "skews": skews,
+            "images": np.stack([c["canvas"] for c in cases]),
+            "patch_image": np.arange(len(cases), dtype=np.int32),
+            "boxes": np.stack([c["box"] for c in cases]),
+            "tau0": np.stack([c["tau0"] for c in cases]),
+            "tau_g": np.stack([c["tau_g"] for c in cases])}
+
