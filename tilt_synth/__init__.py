@@ -252,3 +252,26 @@ def convergence_grid(m: int = 32, square_px: int = 8) -> dict:
             "tau0": np.stack([c["tau0"] for c in cases]),
             "tau_g": np.stack([c["tau_g"] for c in cases])}
 
+
+
+def corruption_case(idx: int, frac: float, m: int = 32, theta_deg: float = 10.0, rank: int = 3) -> dict:
+    """Fig. 4's robustness input (synthetic stand-in for the missing
+    low-rank-texture set): texture ``idx`` (seed [6, idx]: rank-``rank`` piecewise-constant, as the
+    configs), rotated by ``theta_deg`` (the paper's 10 degrees), then exactly round(frac * 4 m^2)
+    canvas pixels replaced by U[0, 1] (seed [6, idx, round(1000 frac)], reading Z23)."""
+    rng = np.random.default_rng([6, idx])
+    length = 8 * m
+    seg_lo, seg_hi = math.ceil(m / 16), math.ceil(m / 6)
+    a = [_piecewise_constant(rng, length, seg_lo, seg_hi) for _ in range(rank)]
+    b = [_piecewise_constant(rng, length, seg_lo, seg_hi) for _ in range(rank)]
+    h_g = planted_transform(math.radians(theta_deg), 0.0)
+    x0 = y0 = m // 2
+    canvas = render_texture(a, b, h_g, m, m, (x0, y0), (2 * m, 2 * m))
+    npx = 4 * m * m
+    k = int(round(frac * npx))
+    if k > 0:
+        r2 = np.random.default_rng([6, idx, int(round(1000 * frac))])
+        sel = r2.choice(npx, size=k, replace=False)
+        canvas.reshape(-1)[sel] = r2.uniform(0.0, 1.0, size=k)
+    return {"canvas": canvas.astype(np.float32), "box": np.array([x0, y0, m, m], dtype=np.int32),
+            "tau0": identity_tau(AFFINE), "tau_g": tau_from_h(h_g, AFFINE)}
