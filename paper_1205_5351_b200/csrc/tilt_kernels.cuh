@@ -859,7 +859,8 @@ __global__ void __launch_bounds__(K1_NT, 3) k_warp(WarpArgs a) {
   const WarpGeom g = make_geom(bx, tau, a.kind);
   const float* img = a.images + (size_t)a.patch_image[b] * a.H * a.W;
   const double inv_s = 1.0 / g.s;
-  double acc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  const float inv_sf = (float)inv_s, cif = 0.5f * (m - 1), cjf = 0.5f * (n - 1);
+  float facc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
   bool esc = false;
   PixIter it(threadIdx.x, K1_NT, n);  // row-major (j fastest): it.i is the column j, it.j the row i
   for (int o0 = threadIdx.x; o0 < mn; o0 += K1_NT * K1_ILP) {
@@ -898,18 +899,24 @@ __global__ void __launch_bounds__(K1_NT, 3) k_warp(WarpArgs a) {
       const float gz = -fmaf(gx, t[u].xn, gy * t[u].yn);
       const float4 px = make_float4(d, gx, gy, gz);
       k1s[o] = px;
-      double jr[8];
-      jraw_row(px.y, px.z, px.w, (j - 0.5 * (n - 1)) * inv_s, (i - 0.5 * (m - 1)) * inv_s, jr);
-      const double dd = px.x;
-      acc[8] = fma(dd, dd, acc[8]);
-#pragma unroll
-      for (int q = 0; q < 8; ++q) acc[q] = fma(jr[q], dd, acc[q]);
+      // per-thread partial sums in fp32 (~10 pixels each), combined across threads in fp64
+      const float uu = ((float)j - cjf) * inv_sf, vv = ((float)i - cif) * inv_sf;
+      const float gxd = gx * d, gyd = gy * d, gzd = gz * d;
+      facc[0] = fmaf(gxd, uu, facc[0]);
+      facc[1] = fmaf(gxd, vv, facc[1]);
+      facc[2] = fmaf(gyd, uu, facc[2]);
+      facc[3] = fmaf(gyd, vv, facc[3]);
+      facc[4] += gxd;
+      facc[5] += gyd;
+      facc[6] = fmaf(gzd, uu, facc[6]);
+      facc[7] = fmaf(gzd, vv, facc[7]);
+      facc[8] = fmaf(d, d, facc[8]);
     }
   }
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
 #pragma unroll
   for (int k = 0; k < 9; ++k) {
-    double x = acc[k];
+    double x = facc[k];
 #pragma unroll
     for (int off = 16; off; off >>= 1) x += __shfl_xor_sync(FULL, x, off);
     if (lane == 0) red[w][k] = x;
@@ -936,7 +943,7 @@ __global__ void __launch_bounds__(K1_NT, 3) k_warp(WarpArgs a) {
   for (int q = 0; q < 8; ++q) c[q] = (float)(tot[q] * indd);  // D_hat^T J_raw
   float* Dh = a.Dhat + (size_t)b * mn;
   float* Jb = a.J ? a.J + (size_t)b * p * mn : nullptr;
-  const float inv_sf = (float)inv_s, ci = 0.5f * (m - 1), cj = 0.5f * (n - 1);
+  const float ci = cif, cj = cjf;
   for (PixIter it2(threadIdx.x, K1_NT, n); it2.idx < mn; it2.next(K1_NT)) {
     const int o = it2.idx, i = it2.j, j = it2.i;
     const float4 px = k1s[o];
