@@ -26,7 +26,7 @@ constexpr unsigned FULL = 0xffffffffu;
 // Configuration
 // --------------------------------------------------------------------------------------------
 
-template <int LANES_, int RPL_, int NWARPS_, bool PLANES_SMEM_, bool SVD_SMEM_, int MINB_>
+template <int LANES_, int RPL_, int NWARPS_, bool PLANES_SMEM_, bool SVD_SMEM_, int MINB_, bool B_SMEM_ = SVD_SMEM_>
 struct Cfg {
   static constexpr int LANES = LANES_;   // lanes per Jacobi pair unit (16: half warp, 32: warp)
   static constexpr int RPL = RPL_;       // rows per lane (a column holds up to MAXD rows)
@@ -36,6 +36,7 @@ struct Cfg {
   static constexpr int UNITS = NT / LANES_;
   static constexpr bool PLANES_SMEM = PLANES_SMEM_;
   static constexpr bool SVD_SMEM = SVD_SMEM_;
+  static constexpr bool B_SMEM = B_SMEM_;  // B = M V in shared memory even when V, S are not
   static constexpr int MINB = MINB_;
 };
 
@@ -45,7 +46,10 @@ struct Cfg {
 using CfgS32 = Cfg<8, 4, 8, true, true, 4>;
 using CfgS64 = Cfg<8, 8, 8, false, true, 4>;
 using CfgS128 = Cfg<16, 8, 32, false, true, 1>;
-using CfgS256 = Cfg<32, 8, 32, false, false, 1>;
+// S256: B (256 x n floats, 205 KB at n = 200) in shared memory; V and S in the L2-resident slot
+using CfgS256 = Cfg<32, 8, 32, false, false, 1, true>;
+// S256 with n > 216 (B does not fit in shared memory): everything in the slot
+using CfgS256G = Cfg<32, 8, 32, false, false, 1, false>;
 
 struct DevParams {
   float lambda, mu0_scale, mu_max_ratio, rho0, eps1, eps2, obj_tol, tau_tol;

@@ -18,12 +18,13 @@ struct Layout {
   static __host__ __device__ size_t smem_bytes(int ld, int n, int gplanes) {
     size_t s = vec_floats();
     if (C::SVD_SMEM) s += svd_floats(ld, n);
+    else if (C::B_SMEM) s += (size_t)C::MAXD * n;
     if (C::PLANES_SMEM) s += plane_floats(ld, n, gplanes);
     return s * sizeof(float);
   }
   static __host__ __device__ size_t ws_floats(int ld, int n, int gplanes) {
     size_t s = 0;
-    if (!C::SVD_SMEM) s += svd_floats(ld, n);
+    if (!C::SVD_SMEM) s += svd_floats(ld, n) - (C::B_SMEM ? (size_t)C::MAXD * n : 0);
     if (!C::PLANES_SMEM) s += plane_floats(ld, n, gplanes);
     return (s + 31) & ~size_t(31);
   }
@@ -40,17 +41,23 @@ __device__ __forceinline__ Ctx<C> make_ctx(float* smem, float* ws, Scal* sc, int
   sp += 5 * C::MAXD;
   const int blk = ld * n;
   const int sblk = C::MAXD * n;
-  float* svd;
   if constexpr (C::SVD_SMEM) {
-    svd = sp;
+    cx.B = sp;
+    cx.V = sp + sblk;
+    cx.S = sp + 2 * sblk;
     sp += 3 * sblk;
+  } else if constexpr (C::B_SMEM) {
+    cx.B = sp;
+    sp += sblk;
+    cx.V = gp;
+    cx.S = gp + sblk;
+    gp += 2 * sblk;
   } else {
-    svd = gp;
+    cx.B = gp;
+    cx.V = gp + sblk;
+    cx.S = gp + 2 * sblk;
     gp += 3 * sblk;
   }
-  cx.B = svd;
-  cx.V = svd + sblk;
-  cx.S = svd + 2 * sblk;
   cx.lds = C::MAXD;
   float* pl;
   if constexpr (C::PLANES_SMEM) {
