@@ -112,6 +112,10 @@ typedef struct {
   float adm_tol;          /* ADM stop: ||D + J dtau - A - E||_F / ||D||_F < adm_tol (default 1e-6: the
                              fp32 residual floor is ~1e-7, as for eps1; the fp64 oracle reproduces
                              Table 1's ADM counts at 1e-7) */
+  /* persistent-grid size of the CTA-per-patch solve: at most this many patches in flight per SM
+   * (0: the occupancy limit). Fewer in-flight patches run faster each, which shortens the tail of
+   * a batch whose per-patch work varies widely. */
+  int32_t ctas_per_sm;
 } tilt_params;
 
 /* Per-patch report (device array written by tilt_solve_batch). */

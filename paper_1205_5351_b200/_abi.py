@@ -47,6 +47,7 @@ class TiltParams(ctypes.Structure):
         ("inner_solver", ctypes.c_int32),
         ("adm_rho", ctypes.c_float),
         ("adm_tol", ctypes.c_float),
+        ("ctas_per_sm", ctypes.c_int32),
     ]
 
 

@@ -120,6 +120,7 @@ bool params_ok(const tilt_params* p) {
   if (p->constraint_mode != TILT_CONSTRAINTS_NONE && p->constraint_mode != TILT_CONSTRAINTS_CENTER_AREA) return false;
   if (p->kernel_path < 0 || p->kernel_path > 2) return false;
   if (p->inner_solver < 0 || p->inner_solver > 1) return false;
+  if (p->ctas_per_sm < 0) return false;
   if (p->inner_solver == 1 && p->kernel_path == 2) return false;  // the warp-per-patch kernel runs LADMAP only
   if (!std::isfinite(p->adm_rho) || !std::isfinite(p->adm_tol) || p->adm_rho < 1.f || p->adm_tol <= 0.f) return false;
   return true;
@@ -144,7 +145,7 @@ struct Launch {
   }
 
   // grid size (persistent): num_sms * occupancy, capped by B and by the workspace slots
-  static tilt_status grid(tilt_handle* h, const void* fn, Geo geo, int B, int* g) {
+  static tilt_status grid(tilt_handle* h, const void* fn, Geo geo, int B, int* g, int cap_per_sm = 0) {
     const size_t sm = smem(geo);
     tilt_status s = prep(fn, sm);
     if (s != TILT_OK) return s;
@@ -153,7 +154,7 @@ struct Launch {
       g_last_error = "kernel does not fit on an SM (shared memory / registers)";
       return TILT_E_UNSUPPORTED;
     }
-    int gsz = h->num_sms * occ;
+    int gsz = h->num_sms * (cap_per_sm > 0 && cap_per_sm < occ ? cap_per_sm : occ);
     if (gsz > B) gsz = B;
     const size_t w = wsf(geo);
     if (w > 0) {
@@ -178,7 +179,7 @@ struct Launch {
     const Geo geo = geo_of<C>(a.m, a.n, a.p == 8 ? 3 : 2);
     const void* fn = (const void*)k_solve<C>;
     int g = 0;
-    tilt_status s = grid(h, fn, geo, a.B, &g);
+    tilt_status s = grid(h, fn, geo, a.B, &g, a.ctas_per_sm);
     if (s != TILT_OK) return s;
     set_ws(h, a, geo);
     TILT_CUDA(cudaMemsetAsync(a.counter, 0, sizeof(int), h->stream));
@@ -471,6 +472,7 @@ static tilt_status solve_level(tilt_handle* h, const float* images, int32_t n_im
   a.rep = rep;
   a.rep_prev = rep_prev;
   a.counter = h->counter;
+  a.ctas_per_sm = prm->ctas_per_sm;
   const bool rj_ok = tilt::rjh::fits(m, n);
   if (prm->kernel_path == 2 && !rj_ok) {
     g_last_error = "kernel_path = 2 (warp-per-patch) needs m <= 64 and n <= 50";

@@ -406,6 +406,7 @@ struct SolveArgs {
   int* counter;
   float* ws;
   size_t ws_stride;
+  int ctas_per_sm;  // host-side launch cap (0: occupancy limit)
 };
 
 template <class C>
