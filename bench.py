@@ -71,12 +71,14 @@ def gen_shard(cfg_id: int, start: int, count: int, workers: int = 0, indices=Non
     }
 
 
-def flops_per_launch(rep, m, n, p) -> float:
+def flops_per_launch(rep, m, n, p, ns_period: int = 4) -> float:
     """Algorithmic FLOPs (SURVEY.md §8(d) model) from the device counters of one launch:
-    per LADMAP iteration 8pmn + 20mn + 4mn^2 + 4n^3, per Jacobi sweep n(n-1)/2 (12m + 6n)."""
+    per LADMAP iteration 8pmn + 20mn + 4mn^2 + 4n^3/ns_period (the Newton-Schulz step on V runs
+    after every ns_period-th SVT, tilt_params.ns_period), per Jacobi sweep n(n-1)/2 (12m + 6n)."""
     it = float(np.sum(rep["inner_iters"]))
     sw = float(np.sum(rep["jacobi_sweeps"]))
-    return it * (8 * p * m * n + 20 * m * n + 4 * m * n * n + 4 * n ** 3) + sw * n * (n - 1) / 2 * (12 * m + 6 * n)
+    return it * (8 * p * m * n + 20 * m * n + 4 * m * n * n + 4 * n ** 3 / max(1, ns_period)) + \
+        sw * n * (n - 1) / 2 * (12 * m + 6 * n)
 
 
 class ClockSampler:
@@ -227,7 +229,7 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     rep = T.reports_to_numpy(out["rep"])
     conv = int(np.sum(rep["status"] == T.CONVERGED))
     inner = int(np.sum(rep["inner_iters"]))
-    flops = flops_per_launch(rep, m, n, p)
+    flops = flops_per_launch(rep, m, n, p, int(prm.ns_period))
     stats = torch.tensor([elapsed, float(conv), float(inner), flops, float(np.mean(kern_ms))], dtype=torch.float64,
                          device=dev)
     if world > 1:
@@ -273,7 +275,8 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
         "mean_jacobi_sweeps_per_svt": float(np.sum(rep["jacobi_sweeps"]) / max(1, np.sum(rep["inner_iters"]))),
         "roofline": {"bound": "alu", "kernel": "k_solve", "achieved": achieved, "peak": FP32_PEAK_TFLOPS,
                      "unit": "TFLOP/s", "frac": achieved / FP32_PEAK_TFLOPS, "traffic": traffic,
-                     "peak_note": "FP32 FMA: 148 SMs x 128 lanes x 2 x 1.965 GHz (sm_max_mhz of MEASURED_PEAKS.json)",
+                     "peak_note": "FP32 FMA: 148 SMs x 128 lanes x 2 x 1.965 GHz (sm_max_mhz of MEASURED_PEAKS.json); "
+                                  "achieved = SURVEY §8(d) model flops from the device counters / event time",
                      "flops_per_launch": flops},
         "gpu_launches": int(launches),
         "clocks": clk,

@@ -45,6 +45,6 @@ for cid in [int(c) for c in a.configs.split(",")]:
     row = {"config": cid, "batch": B, "window": f"{m}x{n}", "p": p, "pyramid": cfg.pyramid_levels, "seconds": t,
            "converged_patches_per_s": conv / t, "converged_fraction": conv / B, "inner_iters_per_s": it / t,
            "mean_inner_iters": it / B, "sweeps_per_svt": float(np.sum(rep["jacobi_sweeps"]) / max(it, 1)),
-           "model_tflops": bench.flops_per_launch(rep, m, n, p) / t / 1e12}
+           "model_tflops": bench.flops_per_launch(rep, m, n, p, int(prm.ns_period)) / t / 1e12}
     print(json.dumps(row), flush=True)
     s.close()

@@ -40,7 +40,7 @@ ms = ev0.elapsed_time(ev1)
 it = rep["inner_iters"].sum()
 sw = rep["jacobi_sweeps"].sum()
 m, n, p = cfg.m, cfg.n, cfg.p
-fl = it * (8 * p * m * n + 20 * m * n + 4 * m * n * n + 4 * n ** 3) + sw * n * (n - 1) / 2 * (12 * m + 6 * n)
+fl = it * (8 * p * m * n + 20 * m * n + 4 * m * n * n + 4 * n ** 3 / max(1, a.ns)) + sw * n * (n - 1) / 2 * (12 * m + 6 * n)
 rot = rep["jacobi_rotations"].sum()
 pairs = sw * n * (n - 1) / 2
 print(f"path={a.path} ns={a.ns} cfg={a.cfg} batch={a.batch} inner={a.inner} outer={a.outer}: {ms:.3f} ms, {it} iters, {sw/it:.2f} sweeps/iter, "
