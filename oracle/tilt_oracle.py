@@ -345,6 +345,86 @@ class Projector:
 
 
 # ----------------------------------------------------------------------------------------------
+# SVD with warm start (Algorithm 2; Appendix A)
+# ----------------------------------------------------------------------------------------------
+
+def svd_warm_start(m_k, u, sig, v):
+    """One Taylor step of Algorithm 2 along the Cayley curve of Eq. curve_to_search.
+
+    (u, sig, v): the (approximate) SVD of M_{k-1}, u m x n column-orthonormal, sig the diagonal
+    of Sigma (entries may be negative), v n x n orthogonal; m >= n. Steps:
+      W = U Sigma V^T;  P_U = W M^T - M W^T,  P_V = W^T M - M^T W,  P_Sigma = diag(Sigma - U^T M V)
+        (Eqs. projected_gradient1-3, P:1424-1428)
+      h(0) = M - W,  h'(0) = P_U W + U P_Sigma V^T - W P_V,  Z = h'(0) + U P_Sigma V^T,
+      h''(0) = -P_U Z + Z P_V
+      f'(0) = <h(0), h'(0)>,  f''(0) = ||h'(0)||^2 + <h(0), h''(0)>,  t* = -f'(0)/f''(0)  (Eq. ft)
+      U(t*) = (I + t*/2 P_U)^{-1}(I - t*/2 P_U) U,  Sigma(t*) = Sigma - t* P_Sigma,
+      V(t*) = (I + t*/2 P_V)^{-1}(I - t*/2 P_V) V  (Eq. curve_to_search)
+    Returns (U(t*), Sigma(t*), V(t*), t*); t* = 0 when f''(0) <= 0 (no descent model).
+    """
+    m_k = np.asarray(m_k, dtype=np.float64)
+    w = (u * sig) @ v.T
+    p_u = w @ m_k.T - m_k @ w.T
+    p_v = w.T @ m_k - m_k.T @ w
+    p_s = sig - np.einsum("ij,ij->j", u, m_k @ v)
+    h0 = m_k - w
+    ups = (u * p_s) @ v.T
+    h1 = p_u @ w + ups - w @ p_v
+    z = h1 + ups
+    h2 = -p_u @ z + z @ p_v
+    f1 = float(np.sum(h0 * h1))
+    f2 = float(np.sum(h1 * h1) + np.sum(h0 * h2))
+    t = -f1 / f2 if f2 > 0.0 else 0.0
+    im, in_ = np.eye(p_u.shape[0]), np.eye(p_v.shape[0])
+    u_t = np.linalg.solve(im + 0.5 * t * p_u, (im - 0.5 * t * p_u) @ u)
+    v_t = np.linalg.solve(in_ + 0.5 * t * p_v, (in_ - 0.5 * t * p_v) @ v)
+    return u_t, sig - t * p_s, v_t, t
+
+
+def cayley_objective(m_k, u, sig, v, t):
+    """f(t) = 1/2 ||M - U(t) Sigma(t) V(t)^T||_F^2 on the curve of Eq. curve_to_search (Eq. solve_t);
+    test helper for the derivative formulas of Appendix A."""
+    w = (u * sig) @ v.T
+    p_u = w @ m_k.T - m_k @ w.T
+    p_v = w.T @ m_k - m_k.T @ w
+    p_s = sig - np.einsum("ij,ij->j", u, m_k @ v)
+    im, in_ = np.eye(p_u.shape[0]), np.eye(p_v.shape[0])
+    u_t = np.linalg.solve(im + 0.5 * t * p_u, (im - 0.5 * t * p_u) @ u)
+    v_t = np.linalg.solve(in_ + 0.5 * t * p_v, (in_ - 0.5 * t * p_v) @ v)
+    r = m_k - (u_t * (sig - t * p_s)) @ v_t.T
+    return 0.5 * float(np.sum(r * r))
+
+
+class SvdWarm:
+    """The SVD warm start of LADMAP+SVDWS (Algorithm 2): keeps the previous (approximate) SVD and
+    M_{k-1}; S_eps(M_k) uses one ``svd_warm_start`` step when ||M_k - M_{k-1}||_F < eps_svd, else a
+    full SVD ("Else do full svd"). m < n is handled on the transpose (S_eps(M^T) = S_eps(M)^T)."""
+
+    def __init__(self, eps_svd):
+        self.eps_svd = eps_svd
+        self.prev = None
+        self.m_prev = None
+        self.warm_steps = 0
+        self.full_svds = 0
+
+    def svt(self, m_k, eps):
+        m_k = np.asarray(m_k, dtype=np.float64)
+        tr = m_k.shape[0] < m_k.shape[1]
+        x = m_k.T if tr else m_k
+        if self.prev is not None and np.linalg.norm(x - self.m_prev) < self.eps_svd:
+            u, sig, v, _ = svd_warm_start(x, *self.prev)
+            self.warm_steps += 1
+        else:
+            u, sig, vt = np.linalg.svd(x, full_matrices=False)
+            v = vt.T
+            self.full_svds += 1
+        self.prev = (u, sig, v)
+        self.m_prev = x.copy()
+        a = (u * shrink(sig, eps)) @ v.T
+        return (a.T if tr else a), np.sort(np.abs(sig))[::-1]
+
+
+# ----------------------------------------------------------------------------------------------
 # LADMAP inner loop (P:437-468 Eqs. A, E, Y, mu, rho; P:489-497 Cond1/2; P:708-749 Eq. newvars2)
 # ----------------------------------------------------------------------------------------------
 
@@ -394,7 +474,7 @@ def ladmap(dh, proj, lam, mu0, mu_max, rho0, eps1, eps2, max_inner, a0, e0, y0,
     k = 0
     for k in range(n_iter):
         m_k = a - y / mu - r
-        a1, sig = svt(m_k, 1.0 / mu, svd)
+        a1, sig = svd.svt(m_k, 1.0 / mu) if isinstance(svd, SvdWarm) else svt(m_k, 1.0 / mu, svd)
         n_k = e - y / mu - proj.apply(a1 + e - dh)
         e1 = shrink(n_k, lam / mu)
         r = proj.apply(a1 + e1 - dh)
