@@ -98,8 +98,9 @@ def test_range_of_convergence_grid_batched(solver, T):
     from tilt_synth.metrics import rectified
     g = ts.convergence_grid(32, 8)
     nt, ns = len(g["thetas"]), len(g["skews"])
+    grid_solver = T.TiltSolver(0, max_batch=nt * ns, max_m=32, max_n=32, max_p=6)
     for sid in (0, 1):
-        out = solver.solve(g["images"], g["patch_image"], g["boxes"], g["tau0"], T.AFFINE,
+        out = grid_solver.solve(g["images"], g["patch_image"], g["boxes"], g["tau0"], T.AFFINE,
                            T.default_params(inner_solver=sid))
         tau = out["tau"].double().cpu().numpy()
         ok = np.array([rectified(tau[k], g["tau_g"][k]) for k in range(nt * ns)]).reshape(nt, ns)
@@ -108,3 +109,4 @@ def test_range_of_convergence_grid_batched(solver, T):
             r = O.tilt(g["images"][k], g["boxes"][k], g["tau0"][k], O.AFFINE,
                        O.Params(inner="adm" if sid else "ladmap"))
             assert np.max(np.abs(r["tau"] - tau[k])) < 2e-3, (sid, k)
+    grid_solver.close()
