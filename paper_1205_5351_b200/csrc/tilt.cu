@@ -8,6 +8,7 @@
 #include <string>
 
 #include "tilt_kernels.cuh"
+#include "tilt_large_host.h"
 #include "tilt_rj_host.h"
 
 using namespace tilt;
@@ -66,10 +67,21 @@ struct tilt_handle {
   float* h_E = nullptr;
   tilt_report* h_rep = nullptr;
   int64_t launches = 0;
-  int svt_path = 0;  // tilt_svt_batch kernel family (tilt_set_svt_path): 0/1 CTA-per-patch, 2 warp-per-patch
+  int svt_path = 0;  // tilt_svt_batch kernel family (tilt_set_svt_path): 0/1 CTA-per-patch, 2 warp-per-patch,
+                     // 3 multi-CTA
+  tilt::lp::Ctx lp;  // multi-CTA path for large windows (workspace on first use)
 };
 
 namespace {
+
+tilt::lp::Ctx& lp_ctx(tilt_handle* h) {
+  h->lp.device = h->device;
+  h->lp.num_sms = h->num_sms;
+  h->lp.stream = h->stream;
+  h->lp.launches = &h->launches;
+  h->lp.err = &g_last_error;
+  return h->lp;
+}
 
 template <class C>
 int occupancy_for(const void* fn, size_t smem) {
@@ -118,7 +130,8 @@ bool params_ok(const tilt_params* p) {
   if (p->fixed_inner_iters > p->max_inner || p->fixed_outer_iters > p->max_outer) return false;
   if (p->pyramid_levels < 1 || p->pyramid_levels > 2) return false;
   if (p->constraint_mode != TILT_CONSTRAINTS_NONE && p->constraint_mode != TILT_CONSTRAINTS_CENTER_AREA) return false;
-  if (p->kernel_path < 0 || p->kernel_path > 2) return false;
+  if (p->kernel_path < 0 || p->kernel_path > 3) return false;
+  if (p->inner_solver == 1 && p->kernel_path == 3) return false;  // the multi-CTA path runs LADMAP only
   if (p->inner_solver < 0 || p->inner_solver > 1) return false;
   if (p->ctas_per_sm < 0) return false;
   if (p->inner_solver == 1 && p->kernel_path == 2) return false;  // the warp-per-patch kernel runs LADMAP only
@@ -359,6 +372,7 @@ tilt_status tilt_destroy(tilt_handle* h) {
                   h->h_boxes, h->h_tau0, h->h_tau, h->h_A, h->h_E, h->h_rep};
   for (void* p : ptrs)
     if (p) cudaFree(p);
+  tilt::lp::release(h->lp);
   delete h;
   return TILT_OK;
 }
@@ -366,7 +380,8 @@ tilt_status tilt_destroy(tilt_handle* h) {
 tilt_status tilt_create(tilt_handle** out, const tilt_create_opts* o) {
   if (!out || !o) return TILT_E_ARG;
   *out = nullptr;
-  if (o->max_batch < 0 || o->max_m < 1 || o->max_n < 1 || o->max_m > 256 || o->max_n > 256) return TILT_E_ARG;
+  if (o->max_batch < 0 || o->max_m < 1 || o->max_n < 1 || o->max_m > tilt::lp::MAX_DIM || o->max_n > tilt::lp::MAX_DIM)
+    return TILT_E_ARG;
   if (o->max_p != 6 && o->max_p != 8) return TILT_E_ARG;
   tilt_handle* h = new tilt_handle();
   h->device = o->device;
@@ -393,12 +408,14 @@ tilt_status tilt_create(tilt_handle** out, const tilt_create_opts* o) {
     tilt_destroy(h);
     return err == cudaErrorMemoryAllocation ? TILT_E_OOM : TILT_E_CUDA;
   };
-  const SizeClass c = size_class(h->max_m, h->max_n);
+  // CTA-per-patch workspace for windows up to 256 x 256 (larger windows: the multi-CTA path)
+  const int cm = h->max_m < 256 ? h->max_m : 256, cn = h->max_n < 256 ? h->max_n : 256;
+  const SizeClass c = size_class(cm, cn);
   const int mn = h->max_m * h->max_n;
   const int gpl = h->max_p > 3 ? h->max_p : 3;
-  const size_t wsf = ws_need(c, h->max_m, h->max_n, gpl);
+  const size_t wsf = ws_need(c, cm, cn, gpl);
   if (wsf > 0) {
-    const int occ = occ_need(c, h->max_m, h->max_n, gpl);
+    const int occ = occ_need(c, cm, cn, gpl);
     h->ws_slots = h->num_sms * (occ > 0 ? occ : 1);
     h->ws_floats = wsf * h->ws_slots;
   }
@@ -441,7 +458,7 @@ tilt_status tilt_set_stream(tilt_handle* h, void* stream) {
 int64_t tilt_launch_count(const tilt_handle* h) { return h ? h->launches : 0; }
 
 tilt_status tilt_set_svt_path(tilt_handle* h, int32_t path) {
-  if (!h || path < 0 || path > 2) return TILT_E_ARG;
+  if (!h || path < 0 || path > 3) return TILT_E_ARG;
   h->svt_path = path;
   return TILT_OK;
 }
@@ -473,6 +490,10 @@ static tilt_status solve_level(tilt_handle* h, const float* images, int32_t n_im
   a.rep_prev = rep_prev;
   a.counter = h->counter;
   a.ctas_per_sm = prm->ctas_per_sm;
+  if (prm->kernel_path == 3 || m > 256 || n > 256) {
+    g_last_error = "tilt_solve_batch: windows up to 256 x 256 (the multi-CTA path serves tilt_inner_batch / tilt_svt_batch)";
+    return TILT_E_ARG;
+  }
   const bool rj_ok = tilt::rjh::fits(m, n);
   if (prm->kernel_path == 2 && !rj_ok) {
     g_last_error = "kernel_path = 2 (warp-per-patch) needs m <= 64 and n <= 50";
@@ -643,6 +664,8 @@ tilt_status tilt_svt_batch(tilt_handle* h, const float* M, int32_t B, int32_t m,
   a.sweeps = sweeps;
   a.tol = default_jacobi_tol(m);
   a.max_sweeps = 20;
+  if (h->svt_path == 3 || m > 256 || n > 256)
+    return tilt::lp::svt(lp_ctx(h), M, B, m, n, eps, V_io, A, sigma, sweeps, a.tol, a.max_sweeps);
   if (tilt::rjh::fits(m, n) && h->svt_path == 2) return tilt::rjh::svt(h->num_sms, h->ws, h->ws_floats, h->stream, a, &h->launches, &g_last_error);
   return dispatch<SvtF>(size_class(m, n), h, a);
 }
@@ -693,6 +716,10 @@ tilt_status tilt_inner_batch(tilt_handle* h, const float* D, const float* J, con
   a.E = E;
   a.Y = Y;
   a.rep = rep;
+  if (prm->kernel_path == 3 || m > 256 || n > 256) {
+    if (prm->inner_solver != 0) return TILT_E_ARG;
+    return tilt::lp::inner(lp_ctx(h), D, J, Q, Q ? l : 0, B, m, n, p, a.P, A, E, Y, rep);
+  }
   return dispatch<InnerF>(size_class(m, n), h, a);
 }
 

@@ -1,0 +1,1166 @@
+// tilt_large.cu — the multi-CTA path for large windows (m, n <= 1024; SURVEY.md §8(f) NEXT-4:
+// Table 1's 300x300 ... 1000x1000 sizes). The same LADMAP inner loop as
+// tilt_kernels.cuh (P:437-501 with errata E1, E2; readings Z3, Z6, Z7, Z14, Z19, Z21) and the same
+// warm one-sided Jacobi SVT, with the work of one problem spread over the
+// whole GPU instead of one CTA:
+//   * planes (column-major, ld = m rounded to 4) live in a per-problem HBM/L2 slot;
+//   * elementwise passes and the projector reductions K^T v run over all CTAs (fp64 atomics);
+//   * B = M V, A = B diag(h) V^T and the Newton-Schulz step are cuBLAS SGEMMs (FP32, no TF32);
+//   * the Jacobi sweep is block-cyclic: columns in blocks of BW = 16; one round rotates every
+//     cross pair of a block pair (one CTA per block pair; both blocks' columns staged in shared
+//     memory, 16 warps, one column pair per warp, fast scaled rotations as tilt_jacobi.cuh) and
+//     accumulates the 32 x 32 transformation W, then V <- V W for the pair's 32 columns. A sweep is
+//     one intra-block round plus the circle method over blocks, so every column pair is visited
+//     once per sweep as in the CTA kernels; the stop rule is theirs.
+// The host drives the iteration (one stream; one host read of an active-problem counter per Jacobi
+// sweep and per LADMAP iteration).
+#define TILT_NO_FREE_KERNELS
+#include <cublas_v2.h>
+
+#include <cstdio>
+#include <cstring>
+
+#include "tilt_kernels.cuh"
+#include "tilt_large_host.h"
+
+namespace tilt {
+namespace lp {
+namespace {
+
+constexpr int BW = 16;    // Jacobi block width (columns)
+constexpr int RNT = 512;  // threads of a Jacobi round (16 warps)
+constexpr int ENT = 256;  // threads of the elementwise / reduction kernels
+constexpr int EPT = 8;    // elements per thread of the elementwise kernels
+constexpr int NACC = 40;
+
+// fp64 accumulator slots (G: setup only; the others per LADMAP iteration)
+enum : int {
+  ACC_G = 0,    // 36 (packed upper triangle of J^T J)
+  ACC_S1 = 0,   // 8: K^T v, then 1: ||A+ - A||^2
+  ACC_DA = 8,
+  ACC_S2 = 9,   // 8: K^T v2, then 1: ||E+ - E||^2
+  ACC_DE = 17,
+  ACC_C1 = 18,  // ||R||^2
+  ACC_R = 19,   // ||W^TW D||^2
+  ACC_L1 = 20   // ||E||_1
+};
+
+struct St {
+  double acc[NACC];
+  double Linv[64];
+  float mu, mu_next, mu0, mu_max, denom, denom0, lam, eps;
+  float crit1, crit2, nuc, sig1;
+  int svt_rank, relrank, band;
+  int iters, done, status, conv;
+  int svt_done, big_any, rot_any, sw_cur, cap_cur, rot_cur;
+  int sweeps, caps, rotations, aux_sweeps;
+  double fro2;  // ||B||_F^2 at the start of the current SVT (negligible-column threshold)
+};
+
+struct Lay {
+  int m, n, p, ldm, ldn;
+  size_t plane, vplane;
+  size_t oD, oA, oAn, oE, oY, oS, oB, oK, oV, oV2, oT, oSig, oVv, oSt, stride;
+};
+
+inline size_t up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+Lay make_lay(int m, int n, int p) {
+  Lay L;
+  L.m = m;
+  L.n = n;
+  L.p = p;
+  L.ldm = (int)up(m, 4);
+  L.ldn = (int)up(n, 4);
+  L.plane = up((size_t)L.ldm * n, 64);
+  L.vplane = up((size_t)L.ldn * n, 64);
+  size_t o = 0;
+  L.oD = o; o += L.plane;
+  L.oA = o; o += L.plane;
+  L.oAn = o; o += L.plane;
+  L.oE = o; o += L.plane;
+  L.oY = o; o += L.plane;
+  L.oS = o; o += L.plane;
+  L.oB = o; o += L.plane;
+  L.oK = o; o += (size_t)p * L.plane;
+  L.oV = o; o += L.vplane;
+  L.oV2 = o; o += L.vplane;
+  L.oT = o; o += L.vplane;
+  L.oSig = o; o += up(n, 64);
+  L.oVv = o; o += up(n, 64);
+  L.oSt = o; o += up(sizeof(St) / 4 + 1, 64);
+  L.stride = o;
+  return L;
+}
+
+struct Args {
+  float* ws;
+  Lay L;
+  int B;
+  DevParams P;
+  size_t oV;       // current V buffer (swapped by the Newton-Schulz step)
+  float tol, big2;
+  float tiny2;     // a column with ||b||^2 <= tiny2 ||B||_F^2 is numerically zero: never rotated
+  int max_sweeps;
+  int NB, NBp;     // Jacobi blocks
+  int niter;
+  int* counter;
+};
+
+__device__ __forceinline__ float* slot(const Args& a, int b) { return a.ws + (size_t)b * a.L.stride; }
+__device__ __forceinline__ St* state(const Args& a, int b) { return reinterpret_cast<St*>(slot(a, b) + a.L.oSt); }
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// block sum of NV per-thread partials, added (fp64 atomics) into dst[0..NV)
+template <int NV>
+__device__ __forceinline__ void block_add(float (&v)[NV], double* dst) {
+  __shared__ float red[NV][ENT / 32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    const float s = warp_sum(v[k]);
+    if (lane == 0) red[k][wid] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x < NV) {
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < ENT / 32; ++w) s += red[threadIdx.x][w];
+    atomicAdd(dst + threadIdx.x, s);
+  }
+}
+
+// element loop of an elementwise kernel: CTA blockIdx.x covers ENT*EPT consecutive plane entries
+__device__ __forceinline__ size_t elems_end(size_t pl) {
+  const size_t e = (size_t)(blockIdx.x + 1) * ENT * EPT;
+  return e < pl ? e : pl;
+}
+#define FOR_ELEMS(pl) \
+  for (size_t idx = (size_t)blockIdx.x * ENT * EPT + threadIdx.x, end_ = elems_end(pl); idx < end_; idx += ENT)
+
+__device__ __forceinline__ void load_s(const double* acc, int p, float (&s)[8]) {
+#pragma unroll
+  for (int q = 0; q < 8; ++q) s[q] = q < p ? (float)acc[q] : 0.f;
+}
+
+__device__ __forceinline__ float kdot(const float* K, size_t pl, size_t idx, int p, const float (&s)[8]) {
+  float r = 0.f;
+#pragma unroll
+  for (int q = 0; q < 8; ++q)
+    if (q < p) r = fmaf(K[q * pl + idx], s[q], r);
+  return r;
+}
+
+// ---------------------------------------------------------------------------------------------
+// Layout conversion: row-major [m][n] <-> column-major plane (ld), 32 x 32 tiles
+// ---------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_to_plane(const float* __restrict__ src, int nper, Args a, size_t off) {
+  __shared__ float t[32][33];
+  const Lay& L = a.L;
+  const int z = blockIdx.z, b = z / nper, q = z % nper;
+  const float* s = src + ((size_t)b * nper + q) * L.m * L.n;
+  float* d = slot(a, b) + off + (size_t)q * L.plane;
+  const int i0 = blockIdx.y * 32, j0 = blockIdx.x * 32;
+  for (int r = threadIdx.y; r < 32; r += 8) {
+    const int i = i0 + r, j = j0 + threadIdx.x;
+    t[r][threadIdx.x] = (i < L.m && j < L.n) ? s[(size_t)i * L.n + j] : 0.f;
+  }
+  __syncthreads();
+  for (int c = threadIdx.y; c < 32; c += 8) {
+    const int j = j0 + c, i = i0 + threadIdx.x;
+    if (i < L.m && j < L.n) d[(size_t)j * L.ldm + i] = t[threadIdx.x][c];
+  }
+}
+
+// plane -> row-major [m][n] (zeros for problems whose Gram failed when zero_bad)
+__global__ void __launch_bounds__(256) k_from_plane(float* __restrict__ dst, Args a, size_t off, int rows, int cols,
+                                                    int ld, int zero_bad) {
+  __shared__ float t[32][33];
+  const int b = blockIdx.z;
+  const float* s = slot(a, b) + off;
+  const bool z = zero_bad && state(a, b)->status == TILT_PATCH_SINGULAR_GRAM;
+  float* d = dst + (size_t)b * rows * cols;
+  const int i0 = blockIdx.y * 32, j0 = blockIdx.x * 32;
+  for (int c = threadIdx.y; c < 32; c += 8) {
+    const int j = j0 + c, i = i0 + threadIdx.x;
+    t[c][threadIdx.x] = (i < rows && j < cols && !z) ? s[(size_t)j * ld + i] : 0.f;
+  }
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += 8) {
+    const int i = i0 + r, j = j0 + threadIdx.x;
+    if (i < rows && j < cols) d[(size_t)i * cols + j] = t[threadIdx.x][r];
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// Projector setup: G = J^T J (fp64), L^{-1} from chol(G + Q^T Q), K = J L^{-T} (Eq. Jperpv
+// P:601-606, Eq. WTW_property), as orthonormalise_explicit in tilt_device.cuh
+// ---------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(ENT) k_gram(Args a) {
+  const int b = blockIdx.y;
+  const Lay& L = a.L;
+  const float* K = slot(a, b) + L.oK;
+  double g[36];
+#pragma unroll
+  for (int e = 0; e < 36; ++e) g[e] = 0.0;
+  FOR_ELEMS(L.plane) {
+    float j[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) j[q] = q < L.p ? K[q * L.plane + idx] : 0.f;
+    int e = 0;
+#pragma unroll
+    for (int x = 0; x < 8; ++x)
+#pragma unroll
+      for (int y = x; y < 8; ++y) {
+        g[e] = fma((double)j[x], (double)j[y], g[e]);
+        ++e;
+      }
+  }
+  __shared__ double red[ENT / 32];
+  St* st = state(a, b);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int e = 0; e < 36; ++e) {
+    double v = g[e];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) red[wid] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double s = 0.0;
+      for (int w = 0; w < ENT / 32; ++w) s += red[w];
+      atomicAdd(&st->acc[ACC_G + e], s);
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void k_chol(Args a, const float* __restrict__ Q, int l) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= a.B) return;
+  St* st = state(a, b);
+  double qr[24];
+  for (int e = 0; e < 24; ++e) qr[e] = 0.0;
+  if (Q)
+    for (int r = 0; r < l; ++r)
+      for (int q = 0; q < a.L.p; ++q) qr[r * 8 + q] = Q[((size_t)b * l + r) * a.L.p + q];
+  const bool ok = chol_inverse(st->acc + ACC_G, qr, Q ? l : 0, a.L.p, st->Linv);
+  st->status = ok ? TILT_PATCH_CONVERGED : TILT_PATCH_SINGULAR_GRAM;
+  st->done = ok ? 0 : 1;
+  for (int e = 0; e < NACC; ++e) st->acc[e] = 0.0;
+}
+
+__global__ void __launch_bounds__(ENT) k_apply_linv(Args a) {
+  const int b = blockIdx.y;
+  St* st = state(a, b);
+  if (st->status != TILT_PATCH_CONVERGED) return;
+  const Lay& L = a.L;
+  float* K = slot(a, b) + L.oK;
+  const double* Li = st->Linv;
+  FOR_ELEMS(L.plane) {
+    double j[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) j[q] = q < L.p ? (double)K[q * L.plane + idx] : 0.0;
+#pragma unroll
+    for (int x = 0; x < 8; ++x) {
+      if (x < L.p) {
+        double s = 0.0;
+#pragma unroll
+        for (int y = 0; y <= x; ++y) s = fma(Li[x * 8 + y], j[y], s);
+        K[x * L.plane + idx] = (float)s;
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// Projector reductions and the elementwise LADMAP steps (ladmap_inner in tilt_kernels.cuh)
+// ---------------------------------------------------------------------------------------------
+// MODE 0: v = D; 1: v = A + E - D; 2: v = A+ + E - D and ||A+ - A||^2. -> acc[ACC_S1..]
+template <int MODE>
+__global__ void __launch_bounds__(ENT) k_kt(Args a) {
+  const int b = blockIdx.y;
+  St* st = state(a, b);
+  if (st->done) return;
+  const Lay& L = a.L;
+  const float* w = slot(a, b);
+  const float* D = w + L.oD;
+  const float* A = w + L.oA;
+  const float* An = w + L.oAn;
+  const float* E = w + L.oE;
+  const float* K = w + L.oK;
+  float s[9];
+#pragma unroll
+  for (int q = 0; q < 9; ++q) s[q] = 0.f;
+  FOR_ELEMS(L.plane) {
+    float v;
+    if (MODE == 0) {
+      v = D[idx];
+    } else if (MODE == 1) {
+      v = A[idx] + E[idx] - D[idx];
+    } else {
+      const float an = An[idx];
+      v = an + E[idx] - D[idx];
+      const float d = an - A[idx];
+      s[8] = fmaf(d, d, s[8]);
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (q < L.p) s[q] = fmaf(K[q * L.plane + idx], v, s[q]);
+  }
+  block_add<9>(s, st->acc + ACC_S1);
+}
+
+// ||W^TW D||^2 (the Cond1/Cond2 denominator, Z11)
+__global__ void __launch_bounds__(ENT) k_denom(Args a) {
+  const int b = blockIdx.y;
+  St* st = state(a, b);
+  if (st->done) return;
+  const Lay& L = a.L;
+  const float* w = slot(a, b);
+  float s[8];
+  load_s(st->acc + ACC_S1, L.p, s);
+  float r2[1] = {0.f};
+  FOR_ELEMS(L.plane) {
+    const float r = w[L.oD + idx] - kdot(w + L.oK, L.plane, idx, L.p, s);
+    r2[0] = fmaf(r, r, r2[0]);
+  }
+  block_add<1>(r2, st->acc + ACC_R);
+}
+
+// M_0 = A - W^TW(A + E - D) - Y/mu_0 into S (write_m0)
+__global__ void __launch_bounds__(ENT) k_m0(Args a) {
+  const int b = blockIdx.y;
+  St* st = state(a, b);
+  if (st->done) return;
+  const Lay& L = a.L;
+  float* w = slot(a, b);
+  float s[8];
+  load_s(st->acc + ACC_S1, L.p, s);
+  const float inv = 1.f / st->mu;
+  FOR_ELEMS(L.plane) {
+    const float av = w[L.oA + idx];
+    const float v = av + w[L.oE + idx] - w[L.oD + idx];
+    const float r = v - kdot(w + L.oK, L.plane, idx, L.p, s);
+    w[L.oS + idx] = av - r - w[L.oY + idx] * inv;
+  }
+}
+
+// E step (Eq. E with erratum E2): N = E - W^TW(A+ + E - D) - Y/mu, E+ = T_{lam/mu}(N); then the
+// first half of the dual step: K^T (A+ + E+ - D) -> acc[ACC_S2..], ||E+ - E||^2
+__global__ void __launch_bounds__(ENT) k_estep(Args a) {
+  const int b = blockIdx.y;
+  St* st = state(a, b);
+  if (st->done) return;
+  const Lay& L = a.L;
+  float* w = slot(a, b);
+  const float* K = w + L.oK;
+  float s[8];
+  load_s(st->acc + ACC_S1, L.p, s);
+  const float inv_mu = 1.f / st->mu;
+  const float thr = st->lam * inv_mu;
+  float o[9];
+#pragma unroll
+  for (int q = 0; q < 9; ++q) o[q] = 0.f;
+  FOR_ELEMS(L.plane) {
+    const float an = w[L.oAn + idx], e = w[L.oE + idx], dv = w[L.oD + idx];
+    const float pv = (an + e - dv) - kdot(K, L.plane, idx, L.p, s);
+    const float nk = e - pv - w[L.oY + idx] * inv_mu;
+    const float en = copysignf(fmaxf(fabsf(nk) - thr, 0.f), nk);
+    const float d = en - e;
+    o[8] = fmaf(d, d, o[8]);
+    w[L.oE + idx] = en;
+    const float v2 = an + en - dv;
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (q < L.p) o[q] = fmaf(K[q * L.plane + idx], v2, o[q]);
+  }
+  block_add<9>(o, st->acc + ACC_S2);
+}
+
+// dual step (Eq. Y, erratum E1) and the next M: R = W^TW(A+ + E+ - D), Y += mu R,
+// S = A+ - R - Y/mu_{k+1}, A = A+, ||R||^2
+__global__ void __launch_bounds__(ENT) k_ystep(Args a) {
+  const int b = blockIdx.y;
+  St* st = state(a, b);
+  if (st->done) return;
+  const Lay& L = a.L;
+  float* w = slot(a, b);
+  float s[8];
+  load_s(st->acc + ACC_S2, L.p, s);
+  const float mu = st->mu, inv_mun = 1.f / st->mu_next;
+  float c1[1] = {0.f};
+  FOR_ELEMS(L.plane) {
+    const float an = w[L.oAn + idx];
+    const float r = (an + w[L.oE + idx] - w[L.oD + idx]) - kdot(w + L.oK, L.plane, idx, L.p, s);
+    const float y = fmaf(mu, r, w[L.oY + idx]);
+    w[L.oY + idx] = y;
+    c1[0] = fmaf(r, r, c1[0]);
+    w[L.oS + idx] = an - r - y * inv_mun;
+    w[L.oA + idx] = an;
+  }
+  block_add<1>(c1, st->acc + ACC_C1);
+}
+
+__global__ void __launch_bounds__(ENT) k_l1(Args a) {
+  const int b = blockIdx.y;
+  St* st = state(a, b);
+  if (st->status != TILT_PATCH_CONVERGED) return;
+  const float* E = slot(a, b) + a.L.oE;
+  float s[1] = {0.f};
+  FOR_ELEMS(a.L.plane) s[0] += fabsf(E[idx]);
+  block_add<1>(s, st->acc + ACC_L1);
+}
+
+// ||B||_F^2 of the current SVT (B = M V)
+__global__ void __launch_bounds__(ENT) k_fro(Args a) {
+  const int b = blockIdx.y;
+  St* st = state(a, b);
+  if (st->svt_done) return;
+  const float* X = slot(a, b) + a.L.oB;
+  float s[1] = {0.f};
+  FOR_ELEMS(a.L.plane) s[0] = fmaf(X[idx], X[idx], s[0]);
+  block_add<1>(s, &st->fro2);
+}
+
+__global__ void __launch_bounds__(ENT) k_copy_plane(Args a, size_t dst, size_t src) {
+  const int b = blockIdx.y;
+  if (state(a, b)->done) return;
+  float* w = slot(a, b);
+  FOR_ELEMS(a.L.plane) w[dst + idx] = w[src + idx];
+}
+
+// V <- I (n x n, ld = ldn)
+__global__ void __launch_bounds__(ENT) k_identity(Args a, size_t off) {
+  const int b = blockIdx.y;
+  if (state(a, b)->done) return;
+  float* V = slot(a, b) + off;
+  const int ldn = a.L.ldn, n = a.L.n;
+  FOR_ELEMS(a.L.vplane) {
+    const int j = (int)(idx / ldn), i = (int)(idx % ldn);
+    V[idx] = (i == j && j < n) ? 1.f : 0.f;
+  }
+}
+
+// T <- 1.5 I - 0.5 T (Newton-Schulz, Z14)
+__global__ void __launch_bounds__(ENT) k_ns_mid(Args a) {
+  const int b = blockIdx.y;
+  if (state(a, b)->done) return;
+  float* T = slot(a, b) + a.L.oT;
+  const int ldn = a.L.ldn;
+  FOR_ELEMS(a.L.vplane) {
+    const int j = (int)(idx / ldn), i = (int)(idx % ldn);
+    T[idx] = (i == j ? 1.5f : 0.f) - 0.5f * T[idx];
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// Per-problem scalar steps (one thread per problem)
+// ---------------------------------------------------------------------------------------------
+__global__ void k_init(Args a) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= a.B) return;
+  St* st = state(a, b);
+  const int m = a.L.m, n = a.L.n;
+  st->lam = a.P.lambda > 0.f ? a.P.lambda : rsqrtf((float)max(m, n));
+  st->iters = st->sweeps = st->caps = st->rotations = st->aux_sweeps = 0;
+  st->conv = 0;
+  st->crit1 = st->crit2 = __int_as_float(0x7fc00000);
+  st->nuc = 0.f;
+  st->svt_rank = st->relrank = st->band = 0;
+}
+
+__global__ void k_sc_denom(Args a) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= a.B) return;
+  St* st = state(a, b);
+  if (st->done) return;
+  const float d0 = (float)sqrt(st->acc[ACC_R]);
+  st->denom0 = d0;
+  st->denom = d0 > 0.f ? d0 : 1.f;
+  for (int e = 0; e < NACC; ++e) st->acc[e] = 0.0;
+}
+
+// mu_0 = mu0_scale / sigma_1(D) (Z3) after the sigma_1 SVD; mu_max = ratio mu_0 (Z6)
+__global__ void k_sc_mu0(Args a) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= a.B) return;
+  St* st = state(a, b);
+  if (st->done) return;
+  const float s1 = st->sig1;
+  st->mu0 = s1 > 0.f ? a.P.mu0_scale / s1 : a.P.mu0_scale;
+  st->mu = st->mu0;
+  st->mu_max = a.P.mu_max_ratio * st->mu0;
+  st->aux_sweeps = st->sw_cur;
+  for (int e = 0; e < NACC; ++e) st->acc[e] = 0.0;
+}
+
+// Cond2 and the penalty update (Eqs. rho, mu; replay Z21)
+__global__ void k_sc1(Args a, int k) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= a.B) return;
+  St* st = state(a, b);
+  if (st->done) return;
+  const float dA = (float)st->acc[ACC_DA], dE = (float)st->acc[ACC_DE];
+  const float crit2 = st->mu * sqrtf(fmaxf(dA, dE)) / st->denom;
+  int rho_bit = crit2 < a.P.eps2 ? 1 : 0;
+  if (a.P.rho_replay) rho_bit = a.P.rho_replay[(size_t)b * a.P.max_inner + k] & 1;
+  st->mu_next = fminf(st->mu_max, rho_bit ? a.P.rho0 * st->mu : st->mu);
+  st->crit2 = crit2;
+  if (a.P.trace) a.P.trace[4 * ((size_t)b * a.P.max_inner + k) + 3] = (float)rho_bit;
+}
+
+// Cond1, the stop rule (strict), mu <- mu_{k+1}
+__global__ void k_sc2(Args a, int k) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= a.B) return;
+  St* st = state(a, b);
+  if (st->done) return;
+  const float crit1 = (float)sqrt(st->acc[ACC_C1]) / st->denom;
+  if (a.P.trace) {
+    float* t = a.P.trace + 4 * ((size_t)b * a.P.max_inner + k);
+    t[0] = st->mu;
+    t[1] = crit1;
+    t[2] = st->crit2;
+  }
+  st->crit1 = crit1;
+  st->iters = k + 1;
+  bool stop = crit1 < a.P.eps1 && st->crit2 < a.P.eps2;
+  if (a.P.rho_replay) stop = (a.P.rho_replay[(size_t)b * a.P.max_inner + k] & 2) != 0;
+  if (stop) st->conv = 1;
+  const float mu_used = st->mu;
+  st->mu = st->mu_next;
+  for (int e = 0; e < NACC; ++e) st->acc[e] = 0.0;
+  if ((stop && a.P.fixed_inner <= 0) || k + 1 >= a.niter) {
+    st->done = 1;
+    st->mu = mu_used;  // report mu_K of the last SVT
+  } else {
+    atomicAdd(a.counter, 1);
+  }
+}
+
+__global__ void k_report(Args a, tilt_report* rep) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= a.B) return;
+  St* st = state(a, b);
+  tilt_report r;
+  memset(&r, 0, sizeof(r));
+  r.status = st->status;
+  if (st->status == TILT_PATCH_CONVERGED) {
+    r.status = st->conv ? TILT_PATCH_CONVERGED : TILT_PATCH_MAX_OUTER;
+    r.outer_iters = 1;
+    r.inner_iters = st->iters;
+    r.jacobi_sweeps = st->sweeps;
+    r.aux_sweeps = st->aux_sweeps;
+    r.rank = st->relrank;
+    r.rank_band = st->band;
+    r.svt_rank = st->svt_rank;
+    r.sweep_cap_hits = st->caps;
+    r.objective = st->nuc + st->lam * (float)st->acc[ACC_L1];
+    r.crit1 = st->crit1;
+    r.crit2 = st->crit2;
+    r.patch_norm = st->denom0;
+    r.mu_last = st->mu;
+    r.jacobi_rotations = st->rotations;
+    r.kernel_path = 3;
+  }
+  rep[b] = r;
+}
+
+// ---------------------------------------------------------------------------------------------
+// SVT pieces
+// ---------------------------------------------------------------------------------------------
+// eps_mode 0: eps = 1/mu (LADMAP), 1: eps from the caller's array, 2: eps = 0 (sigma_1 SVD)
+__global__ void k_svt_begin(Args a, const float* __restrict__ eps, int eps_mode) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= a.B) return;
+  St* st = state(a, b);
+  st->svt_done = st->done;
+  st->big_any = st->rot_any = 0;
+  st->sw_cur = st->cap_cur = st->rot_cur = 0;
+  st->fro2 = 0.0;
+  if (st->done) return;
+  st->eps = eps_mode == 0 ? 1.f / st->mu : (eps_mode == 1 ? eps[b] : 0.f);
+  atomicAdd(a.counter, 1);
+}
+
+__global__ void k_sweep_end(Args a) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= a.B) return;
+  St* st = state(a, b);
+  if (st->svt_done) return;
+  st->sw_cur += 1;
+  if (!st->big_any) {
+    st->svt_done = 1;
+  } else if (st->sw_cur >= a.max_sweeps) {
+    st->svt_done = 1;
+    st->cap_cur = st->rot_any;
+  }
+  st->big_any = st->rot_any = 0;
+  if (!st->svt_done) atomicAdd(a.counter, 1);
+}
+
+// sigma_j = ||b_j|| / ||v_j||, ||v_j||^2 (one warp per column)
+__global__ void __launch_bounds__(256) k_svt_sig(Args a) {
+  const int b = blockIdx.y;
+  St* st = state(a, b);
+  if (st->done) return;
+  const int j = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (j >= a.L.n) return;
+  const float* w = slot(a, b);
+  const float* bj = w + a.L.oB + (size_t)j * a.L.ldm;
+  const float* vj = w + a.oV + (size_t)j * a.L.ldn;
+  float sb = 0.f, sv = 0.f;
+  for (int i = lane; i < a.L.m; i += 32) sb = fmaf(bj[i], bj[i], sb);
+  for (int i = lane; i < a.L.n; i += 32) sv = fmaf(vj[i], vj[i], sv);
+  sb = warp_sum(sb);
+  sv = warp_sum(sv);
+  if (lane == 0) {
+    float* sig = slot(a, b) + a.L.oSig;
+    float* vv = slot(a, b) + a.L.oVv;
+    sig[j] = sv > 0.f ? sqrtf(sb / sv) : 0.f;
+    vv[j] = sv;
+  }
+}
+
+// SVT statistics (svt_stats in tilt_device.cuh): ||A||_*, sigma_1, #{sigma > eps}, the Z19 rank and
+// band flag; one warp per problem. Also folds the sweep counters into the totals.
+__global__ void __launch_bounds__(32) k_svt_stats(Args a, int count_sweeps) {
+  const int b = blockIdx.x;
+  St* st = state(a, b);
+  if (st->done) return;
+  const float* sig = slot(a, b) + a.L.oSig;
+  const float eps = st->eps;
+  const int lane = threadIdx.x, n = a.L.n;
+  float nuc = 0.f, smax = 0.f, amax = 0.f;
+  int cnt = 0;
+  for (int j = lane; j < n; j += 32) {
+    const float sg = sig[j];
+    const float x = fmaxf(sg - eps, 0.f);
+    nuc += x;
+    smax = fmaxf(smax, sg);
+    amax = fmaxf(amax, x);
+    cnt += (sg > eps);
+  }
+#pragma unroll
+  for (int off = 16; off; off >>= 1) {
+    nuc += __shfl_xor_sync(0xffffffffu, nuc, off);
+    smax = fmaxf(smax, __shfl_xor_sync(0xffffffffu, smax, off));
+    amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, off));
+    cnt += __shfl_xor_sync(0xffffffffu, cnt, off);
+  }
+  int rel = 0, band = 0;
+  for (int j = lane; j < n; j += 32) {
+    const float x = fmaxf(sig[j] - eps, 0.f);
+    if (amax > 0.f) {
+      const float ratio = x / amax;
+      rel += ratio > 1e-3f;
+      band |= (ratio >= 3e-4f && ratio <= 3e-3f);
+    }
+  }
+#pragma unroll
+  for (int off = 16; off; off >>= 1) {
+    rel += __shfl_xor_sync(0xffffffffu, rel, off);
+    band |= __shfl_xor_sync(0xffffffffu, band, off);
+  }
+  if (lane == 0) {
+    st->nuc = nuc;
+    st->sig1 = smax;
+    st->svt_rank = cnt;
+    st->relrank = rel;
+    st->band = band;
+    if (count_sweeps) {
+      st->sweeps += st->sw_cur;
+      st->caps += st->cap_cur ? 1 : 0;
+      st->rotations += st->rot_cur;
+    }
+  }
+}
+
+// B <- B diag(h_j / ||v_j||^2), h_j = max(sigma_j - eps, 0) / sigma_j (ready for A = B V^T)
+__global__ void __launch_bounds__(ENT) k_svt_scale(Args a) {
+  const int b = blockIdx.y;
+  St* st = state(a, b);
+  if (st->done) return;
+  float* w = slot(a, b);
+  const float* sig = w + a.L.oSig;
+  const float* vv = w + a.L.oVv;
+  const float eps = st->eps;
+  const int ldm = a.L.ldm;
+  FOR_ELEMS(a.L.plane) {
+    const int j = (int)(idx / ldm);
+    if (j >= a.L.n) continue;
+    const float sg = sig[j], v2 = vv[j];
+    const float h = sg > eps ? (sg - eps) / sg : 0.f;
+    w[a.L.oB + idx] *= v2 > 0.f ? h / v2 : 0.f;
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// One Jacobi round over a block pair (CROSS) or within one block (intra): see the header.
+// Shared memory: X [NCOL][MAXD] (the columns, rows >= m zero), W [NCOL][NCOL] (column-major),
+// ns [NCOL] (alpha, d, 1/d, -) of the fast rotations (tilt_jacobi.cuh).
+// ---------------------------------------------------------------------------------------------
+template <int RPL, int CROSS>
+__global__ void __launch_bounds__(RNT, 1) k_round(Args a, int r) {
+  constexpr int MAXD = 32 * RPL;
+  constexpr int NCOL = CROSS ? 2 * BW : BW;
+  extern __shared__ float4 sm4[];
+  float* X = reinterpret_cast<float*>(sm4);
+  float* W = X + NCOL * MAXD;
+  float4* ns = reinterpret_cast<float4*>(W + NCOL * NCOL);
+  __shared__ int s_any, s_big, s_cnt;
+  const int b = blockIdx.y;
+  St* st = state(a, b);
+  if (st->svt_done) return;
+  const Lay& L = a.L;
+  int I, J = -1;
+  if (CROSS) {
+    const int q = a.NBp - 1, k = blockIdx.x;
+    I = k == 0 ? q : (r + k) % q;
+    J = k == 0 ? r : (r - k + q) % q;
+    if (I >= a.NB || J >= a.NB) return;  // the dummy block
+  } else {
+    I = blockIdx.x;
+  }
+  const int nI = min(BW, L.n - I * BW), nJ = CROSS ? min(BW, L.n - J * BW) : 0;
+  auto gcol = [&](int c) { return c < BW ? I * BW + c : J * BW + (c - BW); };
+  auto cvalid = [&](int c) { return c < BW ? c < nI : (c - BW) < nJ; };
+  float* w = slot(a, b);
+  float* Bm = w + L.oB;
+  float* V = w + a.oV;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) s_any = s_big = s_cnt = 0;
+  // stage the columns (float4; rows >= ldm zero), W = I
+  constexpr int C4 = MAXD / 4;
+  for (int e = tid; e < NCOL * C4; e += RNT) {
+    const int c = e / C4, i4 = e % C4;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (cvalid(c) && 4 * i4 < L.ldm) v = *reinterpret_cast<const float4*>(Bm + (size_t)gcol(c) * L.ldm + 4 * i4);
+    sm4[e] = v;
+  }
+  for (int e = tid; e < NCOL * NCOL; e += RNT) W[e] = (e / NCOL == e % NCOL) ? 1.f : 0.f;
+  __syncthreads();
+  using CL = Col<RPL, 32>;
+  const uint32_t sX = smem_u32(X);
+  for (int c = warp; c < NCOL; c += RNT / 32) {  // fresh norms, d = 1
+    CL x;
+    x.sload_full(sX + c * MAXD * 4 + lane * 16);
+    const float ss = unit_sum<32>(x.sq());
+    if (lane == 0) ns[c] = make_float4(ss, 1.f, 1.f, 0.f);
+  }
+  __syncthreads();
+  const float tol2 = a.tol * a.tol, big2 = a.big2;
+  const float amin = (float)(a.tiny2 * st->fro2);
+  int rot = 0, big = 0, cnt = 0;
+  constexpr int STEPS = CROSS ? BW : BW - 1;
+  for (int s = 0; s < STEPS; ++s) {
+    int i, j;
+    bool on;
+    if (CROSS) {
+      i = warp;
+      j = BW + (warp + s) % BW;
+      on = true;
+    } else {
+      const int q = BW - 1, k = warp;
+      on = k < BW / 2;
+      i = k == 0 ? q : (s + k) % q;
+      j = k == 0 ? s : (s - k + q) % q;
+      if (!on) i = j = 0;
+    }
+    const bool valid = on && cvalid(i) && cvalid(j);
+    if (valid) {  // warp-uniform
+      CL xi, xj;
+      const uint32_t ai = sX + i * MAXD * 4 + lane * 16, aj = sX + j * MAXD * 4 + lane * 16;
+      xi.sload_full(ai);
+      xj.sload_full(aj);
+      const float g = unit_sum<32>(xi.dot(xj));
+      const float4 ni = ns[i], nj = ns[j];
+      const float gam = g * ni.y * nj.y;
+      const float ab = ni.x * nj.x;
+      const bool doit = ni.x > amin && nj.x > amin && gam * gam > tol2 * ab;
+      if (doit) {
+        const Rot rp = rot_params(ni, nj, gam, true);
+#pragma unroll
+        for (int e = 0; e < RPL; ++e) {
+          const float o = xi.v[e];
+          xi.v[e] = fmaf(-rp.ca, xj.v[e], o);
+          xj.v[e] = fmaf(rp.cb, o, xj.v[e]);
+        }
+        xi.sstore(ai, 0xffffffffu);
+        xj.sstore(aj, 0xffffffffu);
+        if (lane < NCOL) {
+          const float wi = W[i * NCOL + lane], wj = W[j * NCOL + lane];
+          W[i * NCOL + lane] = fmaf(-rp.ca, wj, wi);
+          W[j * NCOL + lane] = fmaf(rp.cb, wi, wj);
+        }
+        if (lane == 0) {
+          const float sx = rp.c * fmaf(rp.t, rp.t, 1.f);  // sqrt(1 + t^2)
+          ns[i] = make_float4(fmaxf(fmaf(-rp.t, gam, ni.x), 0.f), rp.c * ni.y, sx * ni.z, 0.f);
+          ns[j] = make_float4(fmaf(rp.t, gam, nj.x), rp.c * nj.y, sx * nj.z, 0.f);
+        }
+        rot = 1;
+        cnt += 1;
+        big |= gam * gam > big2 * ab ? 1 : 0;
+      }
+    }
+    __syncthreads();
+  }
+  if (lane == 0 && rot) {
+    atomicOr(&s_any, 1);
+    atomicAdd(&s_cnt, cnt);
+  }
+  if (lane == 0 && big) atomicOr(&s_big, 1);
+  __syncthreads();
+  if (!s_any) return;  // nothing rotated: B and V unchanged
+  if (tid == 0) {
+    atomicOr(&st->rot_any, 1);
+    if (s_big) atomicOr(&st->big_any, 1);
+    atomicAdd(&st->rot_cur, s_cnt);
+  }
+  // apply the scales d_c: B columns = d_c x_c, W_eff[:, c] = d_c W[:, c]
+  for (int e = tid; e < NCOL * C4; e += RNT) {
+    const int c = e / C4, i4 = e % C4;
+    if (!cvalid(c) || 4 * i4 >= L.ldm) continue;
+    const float d = ns[c].y;
+    float4 v = sm4[e];
+    v.x *= d; v.y *= d; v.z *= d; v.w *= d;
+    *reinterpret_cast<float4*>(Bm + (size_t)gcol(c) * L.ldm + 4 * i4) = v;
+  }
+  for (int e = tid; e < NCOL * NCOL; e += RNT) W[e] *= ns[e / NCOL].y;
+  __syncthreads();
+  // V[:, cols] <- V[:, cols] W_eff, one row per thread
+  for (int row = tid; row < L.n; row += RNT) {
+    float v[NCOL];  // the row is in registers, so each output can be stored as soon as it is formed
+#pragma unroll
+    for (int c = 0; c < NCOL; ++c) v[c] = cvalid(c) ? V[(size_t)gcol(c) * L.ldn + row] : 0.f;
+#pragma unroll 1
+    for (int c2 = 0; c2 < NCOL; ++c2) {
+      const float4* w4 = reinterpret_cast<const float4*>(W + c2 * NCOL);
+      float o0 = 0.f, o1 = 0.f;
+#pragma unroll
+      for (int c = 0; c < NCOL; c += 4) {
+        const float4 ww = w4[c / 4];
+        o0 = fmaf(v[c], ww.x, o0);
+        o1 = fmaf(v[c + 1], ww.y, o1);
+        o0 = fmaf(v[c + 2], ww.z, o0);
+        o1 = fmaf(v[c + 3], ww.w, o1);
+      }
+      if (cvalid(c2)) V[(size_t)gcol(c2) * L.ldn + row] = o0 + o1;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// Host side
+// ---------------------------------------------------------------------------------------------
+struct Run {
+  Ctx& ctx;
+  Args a;
+  cublasHandle_t cb;
+  tilt_status st = TILT_OK;
+  int rpl = 32;
+
+  explicit Run(Ctx& c) : ctx(c), cb((cublasHandle_t)c.cublas) {}
+
+  bool fail_cuda(cudaError_t e, const char* what) {
+    if (e == cudaSuccess) return false;
+    *ctx.err = std::string(what) + ": " + cudaGetErrorString(e);
+    st = TILT_E_CUDA;
+    return true;
+  }
+  bool check(const char* what) { return fail_cuda(cudaGetLastError(), what); }
+  bool cub(cublasStatus_t s, const char* what) {
+    if (s == CUBLAS_STATUS_SUCCESS) return false;
+    *ctx.err = std::string(what) + ": cuBLAS status " + std::to_string((int)s);
+    st = TILT_E_CUDA;
+    return true;
+  }
+  dim3 egrid(size_t count) const {
+    return dim3((unsigned)((count + (size_t)ENT * EPT - 1) / ((size_t)ENT * EPT)), (unsigned)a.B);
+  }
+  dim3 sgrid() const { return dim3((unsigned)((a.B + 127) / 128)); }
+  void launched(int k = 1) { *ctx.launches += k; }
+  int read_counter() {
+    if (fail_cuda(cudaMemcpyAsync(ctx.h_counter, ctx.counter, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream),
+                  "cudaMemcpyAsync(counter)"))
+      return -1;
+    if (fail_cuda(cudaStreamSynchronize(ctx.stream), "cudaStreamSynchronize")) return -1;
+    return *ctx.h_counter;
+  }
+  bool zero_counter() { return fail_cuda(cudaMemsetAsync(ctx.counter, 0, sizeof(int), ctx.stream), "memset"); }
+
+  // C = op(X) op(Y) with per-problem strides (column-major; cuBLAS FP32, default math: no TF32)
+  bool gemm(cublasOperation_t ta, cublasOperation_t tb, int M, int N, int K, size_t oX, int ldx, size_t oY,
+            int ldy, size_t oC, int ldc, float alpha = 1.f, float beta = 0.f) {
+    const long long s = (long long)a.L.stride;
+    const bool bad = cub(cublasSgemmStridedBatched(cb, ta, tb, M, N, K, &alpha, a.ws + oX, ldx, s, a.ws + oY, ldy, s,
+                                                   &beta, a.ws + oC, ldc, s, a.B),
+                         "cublasSgemmStridedBatched");
+    launched();
+    return bad;
+  }
+
+  template <int RPL>
+  bool sweeps_rpl() {
+    const size_t sm_cross = (size_t)(2 * BW * 32 * RPL + 4 * BW * BW + 8 * BW) * sizeof(float);
+    const size_t sm_intra = (size_t)(BW * 32 * RPL + BW * BW + 4 * BW) * sizeof(float);
+    if (fail_cuda(cudaFuncSetAttribute((const void*)k_round<RPL, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)sm_cross),
+                  "cudaFuncSetAttribute(k_round)"))
+      return true;
+    if (fail_cuda(cudaFuncSetAttribute((const void*)k_round<RPL, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)sm_intra),
+                  "cudaFuncSetAttribute(k_round)"))
+      return true;
+    for (int sw = 0; sw < a.max_sweeps; ++sw) {
+      k_round<RPL, 0><<<dim3(a.NB, a.B), RNT, sm_intra, ctx.stream>>>(a, 0);
+      launched();
+      for (int r = 0; r < a.NBp - 1; ++r) {
+        k_round<RPL, 1><<<dim3(a.NBp / 2, a.B), RNT, sm_cross, ctx.stream>>>(a, r);
+        launched();
+      }
+      if (zero_counter()) return true;
+      k_sweep_end<<<sgrid(), 128, 0, ctx.stream>>>(a);
+      launched();
+      if (check("jacobi sweep")) return true;
+      const int act = read_counter();
+      if (act < 0) return true;
+      if (act == 0) break;
+    }
+    return false;
+  }
+
+  // Jacobi sweeps on (B, V) until every problem's SVT stopped (k_svt_begin ran before)
+  bool sweeps() {
+    switch (rpl) {
+      case 4: return sweeps_rpl<4>();
+      case 8: return sweeps_rpl<8>();
+      case 16: return sweeps_rpl<16>();
+      default: return sweeps_rpl<32>();
+    }
+  }
+
+  // one SVT of S (eps per eps_mode) with the V in a.oV; leaves B scaled, sigma/stats in the state
+  bool svt_core(const float* eps, int eps_mode, int count_sweeps, bool do_scale) {
+    if (zero_counter()) return true;
+    k_svt_begin<<<sgrid(), 128, 0, ctx.stream>>>(a, eps, eps_mode);
+    launched();
+    const Lay& L = a.L;
+    if (gemm(CUBLAS_OP_N, CUBLAS_OP_N, L.m, L.n, L.n, L.oS, L.ldm, a.oV, L.ldn, L.oB, L.ldm)) return true;
+    k_fro<<<egrid(L.plane), ENT, 0, ctx.stream>>>(a);
+    launched();
+    if (sweeps()) return true;
+    k_svt_sig<<<dim3((L.n + 7) / 8, a.B), 256, 0, ctx.stream>>>(a);
+    k_svt_stats<<<a.B, 32, 0, ctx.stream>>>(a, count_sweeps);
+    launched(2);
+    if (do_scale) {
+      k_svt_scale<<<egrid(L.plane), ENT, 0, ctx.stream>>>(a);
+      launched();
+    }
+    return check("svt");
+  }
+
+  bool ns_step() {
+    const Lay& L = a.L;
+    if (gemm(CUBLAS_OP_T, CUBLAS_OP_N, L.n, L.n, L.n, a.oV, L.ldn, a.oV, L.ldn, L.oT, L.ldn)) return true;
+    k_ns_mid<<<egrid(L.vplane), ENT, 0, ctx.stream>>>(a);
+    launched();
+    const size_t other = a.oV == L.oV ? L.oV2 : L.oV;
+    if (gemm(CUBLAS_OP_N, CUBLAS_OP_N, L.n, L.n, L.n, a.oV, L.ldn, L.oT, L.ldn, other, L.ldn)) return true;
+    a.oV = other;
+    return check("ns");
+  }
+
+  void setup(int B, int m, int n, int p, const DevParams& P) {
+    a.ws = ctx.ws;
+    a.L = make_lay(m, n, p);
+    a.B = B;
+    a.P = P;
+    a.oV = a.L.oV;
+    a.counter = ctx.counter;
+    a.tiny2 = 1e-14f;  // ||b_j|| <= 1e-7 ||M||_F: below fp32 resolution of the SVT output
+    a.NB = (n + BW - 1) / BW;
+    a.NBp = a.NB + (a.NB & 1);
+    if (a.NBp < 2) a.NBp = 2;
+    const int d = m;  // column length of the Jacobi columns
+    rpl = d <= 128 ? 4 : d <= 256 ? 8 : d <= 512 ? 16 : 32;
+  }
+};
+
+}  // namespace
+
+size_t ws_need(int B, int m, int n, int p) { return (size_t)B * make_lay(m, n, p).stride; }
+
+tilt_status ensure(Ctx& ctx, size_t floats) {
+  if (!ctx.counter) {
+    if (cudaMalloc(&ctx.counter, 64 * sizeof(int)) != cudaSuccess) return TILT_E_OOM;
+    if (cudaMallocHost(&ctx.h_counter, 64 * sizeof(int)) != cudaSuccess) return TILT_E_OOM;
+  }
+  if (!ctx.cublas) {
+    cublasHandle_t h;
+    if (cublasCreate(&h) != CUBLAS_STATUS_SUCCESS) {
+      *ctx.err = "cublasCreate failed";
+      return TILT_E_CUDA;
+    }
+    cublasSetMathMode(h, CUBLAS_DEFAULT_MATH);  // FP32 SGEMM, no TF32 (the 1e-4 parity needs FP32)
+    ctx.cublas = h;
+  }
+  cublasSetStream((cublasHandle_t)ctx.cublas, ctx.stream);
+  if (ctx.ws_floats < floats) {
+    if (ctx.ws) cudaFree(ctx.ws);
+    ctx.ws = nullptr;
+    ctx.ws_floats = 0;
+    if (cudaMalloc(&ctx.ws, floats * sizeof(float)) != cudaSuccess) {
+      *ctx.err = "cudaMalloc(multi-CTA workspace) failed";
+      return TILT_E_OOM;
+    }
+    ctx.ws_floats = floats;
+  }
+  return TILT_OK;
+}
+
+void release(Ctx& ctx) {
+  if (ctx.ws) cudaFree(ctx.ws);
+  if (ctx.counter) cudaFree(ctx.counter);
+  if (ctx.h_counter) cudaFreeHost(ctx.h_counter);
+  if (ctx.cublas) cublasDestroy((cublasHandle_t)ctx.cublas);
+  ctx = Ctx();
+}
+
+tilt_status inner(Ctx& ctx, const float* D, const float* J, const float* Q, int l, int B, int m, int n, int p,
+                  const DevParams& P, float* A, float* E, float* Y, tilt_report* rep) {
+  tilt_status s0 = ensure(ctx, ws_need(B, m, n, p));
+  if (s0 != TILT_OK) return s0;
+  Run R(ctx);
+  R.setup(B, m, n, p, P);
+  Args& a = R.a;
+  const Lay& L = a.L;
+  a.tol = P.jacobi_tol > 0.f ? P.jacobi_tol : default_jacobi_tol(m);
+  a.big2 = a.tol / (float)n;
+  a.max_sweeps = P.jacobi_max_sweeps;
+  a.niter = P.fixed_inner > 0 ? P.fixed_inner : P.max_inner;
+  cudaStream_t sm = ctx.stream;
+  if (R.fail_cuda(cudaMemsetAsync(ctx.ws, 0, (size_t)B * L.stride * sizeof(float), sm), "memset(ws)")) return R.st;
+  const dim3 tg((n + 31) / 32, (m + 31) / 32, B), tgj((n + 31) / 32, (m + 31) / 32, B * p);
+  k_to_plane<<<tg, dim3(32, 8), 0, sm>>>(D, 1, a, L.oD);
+  k_to_plane<<<tgj, dim3(32, 8), 0, sm>>>(J, p, a, L.oK);
+  k_init<<<R.sgrid(), 128, 0, sm>>>(a);
+  k_gram<<<R.egrid(L.plane), ENT, 0, sm>>>(a);
+  k_chol<<<R.sgrid(), 128, 0, sm>>>(a, Q, l);
+  k_apply_linv<<<R.egrid(L.plane), ENT, 0, sm>>>(a);
+  R.launched(6);
+  // A_0 = D, E_0 = Y_0 = 0 (memset), V = I; ||W^TW D||
+  k_copy_plane<<<R.egrid(L.plane), ENT, 0, sm>>>(a, L.oA, L.oD);
+  k_identity<<<R.egrid(L.vplane), ENT, 0, sm>>>(a, L.oV);
+  k_kt<0><<<R.egrid(L.plane), ENT, 0, sm>>>(a);
+  k_denom<<<R.egrid(L.plane), ENT, 0, sm>>>(a);
+  k_sc_denom<<<R.sgrid(), 128, 0, sm>>>(a);
+  R.launched(5);
+  if (R.check("inner setup")) return R.st;
+  // sigma_1(D) by the same Jacobi (Z3); its V warm-starts the first SVT
+  k_copy_plane<<<R.egrid(L.plane), ENT, 0, sm>>>(a, L.oS, L.oD);
+  R.launched();
+  if (R.svt_core(nullptr, 2, 0, false)) return R.st;
+  k_sc_mu0<<<R.sgrid(), 128, 0, sm>>>(a);
+  k_kt<1><<<R.egrid(L.plane), ENT, 0, sm>>>(a);
+  k_m0<<<R.egrid(L.plane), ENT, 0, sm>>>(a);
+  R.launched(3);
+  const bool warm = P.svd_warm != 0;
+  for (int k = 0; k < a.niter; ++k) {
+    if (!warm) {
+      k_identity<<<R.egrid(L.vplane), ENT, 0, sm>>>(a, a.oV);
+      R.launched();
+    }
+    if (R.svt_core(nullptr, 0, 1, true)) return R.st;
+    if (R.gemm(CUBLAS_OP_N, CUBLAS_OP_T, m, n, n, L.oB, L.ldm, a.oV, L.ldn, L.oAn, L.ldm)) return R.st;
+    if (warm && (k % P.ns_period == P.ns_period - 1 || k + 1 == a.niter))
+      if (R.ns_step()) return R.st;
+    k_kt<2><<<R.egrid(L.plane), ENT, 0, sm>>>(a);
+    k_estep<<<R.egrid(L.plane), ENT, 0, sm>>>(a);
+    k_sc1<<<R.sgrid(), 128, 0, sm>>>(a, k);
+    k_ystep<<<R.egrid(L.plane), ENT, 0, sm>>>(a);
+    if (R.zero_counter()) return R.st;
+    k_sc2<<<R.sgrid(), 128, 0, sm>>>(a, k);
+    R.launched(5);
+    if (R.check("ladmap iteration")) return R.st;
+    const int act = R.read_counter();
+    if (act < 0) return R.st;
+    if (act == 0) break;
+  }
+  k_l1<<<R.egrid(L.plane), ENT, 0, sm>>>(a);
+  k_report<<<R.sgrid(), 128, 0, sm>>>(a, rep);
+  const dim3 og((n + 31) / 32, (m + 31) / 32, B);
+  k_from_plane<<<og, dim3(32, 8), 0, sm>>>(A, a, L.oA, m, n, L.ldm, 1);
+  k_from_plane<<<og, dim3(32, 8), 0, sm>>>(E, a, L.oE, m, n, L.ldm, 1);
+  R.launched(4);
+  if (Y) {
+    k_from_plane<<<og, dim3(32, 8), 0, sm>>>(Y, a, L.oY, m, n, L.ldm, 1);
+    R.launched();
+  }
+  R.check("inner outputs");
+  return R.st;
+}
+
+__global__ void k_svt_out(Args a, float* sigma, int32_t* sweeps) {
+  const int b = blockIdx.y;
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const St* st = state(a, b);
+  if (sigma && j < a.L.n) sigma[(size_t)b * a.L.n + j] = slot(a, b)[a.L.oSig + j];
+  if (sweeps && j == 0) sweeps[b] = st->sw_cur;
+}
+
+__global__ void k_svt_clear(Args a) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= a.B) return;
+  St* st = state(a, b);
+  st->done = 0;
+  st->status = TILT_PATCH_CONVERGED;
+}
+
+tilt_status svt(Ctx& ctx, const float* M, int B, int m, int n, const float* eps, float* V_io, float* A,
+                float* sigma, int32_t* sweeps, float tol, int max_sweeps) {
+  tilt_status s0 = ensure(ctx, ws_need(B, m, n, 1));
+  if (s0 != TILT_OK) return s0;
+  Run R(ctx);
+  DevParams P;
+  memset(&P, 0, sizeof(P));
+  R.setup(B, m, n, 1, P);
+  Args& a = R.a;
+  const Lay& L = a.L;
+  a.tol = tol;
+  a.big2 = tol / (float)n;
+  a.max_sweeps = max_sweeps;
+  cudaStream_t sm = ctx.stream;
+  if (R.fail_cuda(cudaMemsetAsync(ctx.ws, 0, (size_t)B * L.stride * sizeof(float), sm), "memset(ws)")) return R.st;
+  k_svt_clear<<<R.sgrid(), 128, 0, sm>>>(a);
+  k_to_plane<<<dim3((n + 31) / 32, (m + 31) / 32, B), dim3(32, 8), 0, sm>>>(M, 1, a, L.oS);
+  R.launched(2);
+  if (V_io) {  // row-major [n][n] -> column-major plane (ld = ldn)
+    Args av = a;
+    av.L.m = n;
+    av.L.ldm = L.ldn;
+    k_to_plane<<<dim3((n + 31) / 32, (n + 31) / 32, B), dim3(32, 8), 0, sm>>>(V_io, 1, av, L.oV);
+  } else {
+    k_identity<<<R.egrid(L.vplane), ENT, 0, sm>>>(a, L.oV);
+  }
+  R.launched();
+  if (R.svt_core(eps, 1, 0, true)) return R.st;
+  if (R.gemm(CUBLAS_OP_N, CUBLAS_OP_T, m, n, n, L.oB, L.ldm, a.oV, L.ldn, L.oAn, L.ldm)) return R.st;
+  k_from_plane<<<dim3((n + 31) / 32, (m + 31) / 32, B), dim3(32, 8), 0, sm>>>(A, a, L.oAn, m, n, L.ldm, 0);
+  k_svt_out<<<dim3((n + 127) / 128, B), 128, 0, sm>>>(a, sigma, sweeps);
+  R.launched(2);
+  if (V_io) {
+    k_from_plane<<<dim3((n + 31) / 32, (n + 31) / 32, B), dim3(32, 8), 0, sm>>>(V_io, a, a.oV, n, n, L.ldn, 0);
+    R.launched();
+  }
+  R.check("svt outputs");
+  return R.st;
+}
+
+}  // namespace lp
+}  // namespace tilt

@@ -1,0 +1,46 @@
+// tilt_large_host.h — host side of the multi-CTA path for large windows (tilt_large.cu), called by
+// the C ABI in tilt.cu. Internal interface (not part of include/tilt.h).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/tilt.h"
+
+namespace tilt {
+struct DevParams;
+namespace lp {
+
+constexpr int MAX_DIM = 1024;  // largest m, n of the multi-CTA path
+
+// Library state of the multi-CTA path (owned by the tilt_handle; workspace allocated on first use).
+struct Ctx {
+  int device = 0;
+  int num_sms = 0;
+  cudaStream_t stream = nullptr;
+  float* ws = nullptr;       // per-problem slots (planes, V buffers, state)
+  size_t ws_floats = 0;
+  int* counter = nullptr;    // device: active-problem counter
+  int* h_counter = nullptr;  // pinned host mirror
+  void* cublas = nullptr;    // cublasHandle_t
+  int64_t* launches = nullptr;
+  std::string* err = nullptr;
+};
+
+// workspace floats of B problems of size m x n with p Jacobian planes
+size_t ws_need(int B, int m, int n, int p);
+// (re)allocate ctx.ws for at least `floats` floats and create the cuBLAS handle
+tilt_status ensure(Ctx& ctx, size_t floats);
+void release(Ctx& ctx);
+
+// LADMAP inner loop (tilt_inner_batch semantics) on the multi-CTA path
+tilt_status inner(Ctx& ctx, const float* D, const float* J, const float* Q, int l, int B, int m, int n, int p,
+                  const DevParams& P, float* A, float* E, float* Y, tilt_report* rep);
+// SVT (tilt_svt_batch semantics) on the multi-CTA path
+tilt_status svt(Ctx& ctx, const float* M, int B, int m, int n, const float* eps, float* V_io, float* A,
+                float* sigma, int32_t* sweeps, float tol, int max_sweeps);
+
+}  // namespace lp
+}  // namespace tilt

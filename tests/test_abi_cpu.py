@@ -48,9 +48,11 @@ def test_argument_validation_without_gpu(pkg):
     prm = pkg.default_params()
     assert pkg.lib.tilt_solve_batch(None, None, 0, 0, 0, None, None, None, 0, 0, ctypes.byref(prm),
                                     None, None, None, None, None) == _abi.TILT_E_ARG
-    opts = _abi.TiltCreateOpts(device=0, stream=None, max_batch=1, max_m=300, max_n=32, max_p=6)
+    opts = _abi.TiltCreateOpts(device=0, stream=None, max_batch=1, max_m=1100, max_n=32, max_p=6)
     h = ctypes.c_void_p()
-    assert pkg.lib.tilt_create(ctypes.byref(h), ctypes.byref(opts)) == _abi.TILT_E_ARG  # max_m > 256
+    assert pkg.lib.tilt_create(ctypes.byref(h), ctypes.byref(opts)) == _abi.TILT_E_ARG  # max_m > 1024
+    opts = _abi.TiltCreateOpts(device=0, stream=None, max_batch=1, max_m=32, max_n=32, max_p=7)
+    assert pkg.lib.tilt_create(ctypes.byref(h), ctypes.byref(opts)) == _abi.TILT_E_ARG  # p not 6 or 8
 
 
 def test_no_cpu_fallback_in_product(pkg):

@@ -1,0 +1,148 @@
+"""Multi-CTA path for large windows (Table 1's 300x300 ... 1000x1000 sizes,
+PAPER.md P:940-978) against the fp64 oracle, through the C ABI (tilt_svt_batch with svt path 3,
+tilt_inner_batch with tilt_params.kernel_path = 3; windows above 256 take this path automatically).
+Tolerances as tests/test_gpu_steps.py."""
+import math
+
+import numpy as np
+import pytest
+
+import oracle as O
+import tilt_synth as ts
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def T():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import __graft_entry__ as g
+    g.build()
+    import paper_1205_5351_b200 as T
+    return T
+
+
+@pytest.fixture(scope="module")
+def solver(T):
+    s = T.TiltSolver(0, max_batch=16, max_m=1024, max_n=1024, max_p=8)
+    yield s
+    s.close()
+
+
+LARGE_SVT = [(50, 50), (100, 100), (130, 70), (70, 130), (300, 300), (257, 300), (600, 520), (1000, 1000)]
+
+
+@pytest.mark.parametrize("m,n", LARGE_SVT)
+def test_svt_parity_multi_cta(solver, m, n):
+    """S_eps (Eqs. A_1, S_operator) by the block-cyclic multi-CTA Jacobi, cold start."""
+    B = 2 if m * n > 100_000 else 4
+    Ms = np.stack([ts.lowrank_sparse(m, n, 3 + k, k) for k in range(B)])
+    sig1 = np.array([np.linalg.svd(x, compute_uv=False)[0] for x in Ms])
+    eps = (sig1 * np.array([0.01, 0.2, 0.05, 1e-4])[:B]).astype(np.float32)
+    out = solver.svt(Ms.astype(np.float32), eps, path=3)
+    A = out["A"].double().cpu().numpy()
+    for k in range(B):
+        ref, s = O.svt(Ms[k].astype(np.float32).astype(np.float64), float(eps[k]))
+        err = np.linalg.norm(A[k] - ref) / np.linalg.norm(Ms[k])
+        assert err < 3e-5, (m, n, k, err)
+        gs = np.sort(out["sigma"][k].double().cpu().numpy())[::-1][:min(m, n)]
+        np.testing.assert_allclose(gs, s[:min(m, n)], atol=1e-5 * s[0])
+    assert int(out["sweeps"].max()) < 20
+
+
+def test_svt_multi_cta_warm_start(solver):
+    """The warm start (reading Z14): V of a nearby matrix cuts the sweeps, same S_eps."""
+    m = n = 300
+    M0 = ts.lowrank_sparse(m, n, 4, 0)
+    rng = np.random.default_rng(0)
+    M1 = M0 + 1e-4 * rng.normal(size=(m, n))
+    cold = solver.svt(M0[None].astype(np.float32), [1e-3], path=3)
+    warm = solver.svt(M1[None].astype(np.float32), [1e-3], V=cold["V"], path=3)
+    ref, _ = O.svt(M1.astype(np.float32).astype(np.float64), 1e-3)
+    assert np.linalg.norm(warm["A"][0].double().cpu().numpy() - ref) < 3e-5 * np.linalg.norm(M1)
+    assert int(warm["sweeps"][0]) < int(cold["sweeps"][0])
+
+
+def _inner_ref(D, J, lam, K, max_inner):
+    proj = O.Projector(J, None)
+    sigma1 = np.linalg.svd(D, compute_uv=False)[0]
+    mu0 = 1.25 / sigma1
+    z = np.zeros_like(D)
+    return O.ladmap(D, proj, lam, mu0, 1e6 * mu0, 2.0, 1e-6, 0.1, max_inner, D.copy(), z, z, fixed_iters=K)
+
+
+@pytest.mark.parametrize("m,n,p,K", [(50, 50, 6, 20), (100, 100, 6, 20), (300, 300, 6, 20), (200, 300, 8, 20)])
+def test_inner_fixed_count_parity_multi_cta(solver, T, m, n, p, K):
+    """Table 1's inner loop at a fixed count with the oracle's rho decisions replayed
+    (Z21): A and E within 1e-4 relative Frobenius."""
+    B = 2
+    insts = [ts.table1_instance(n, p, s, m=m) for s in range(B)]
+    D = np.stack([i["D"] for i in insts]).astype(np.float32)
+    J = np.stack([i["J"] for i in insts]).astype(np.float32)
+    lam = insts[0]["lam"]
+    refs = [_inner_ref(D[k].astype(np.float64), J[k].astype(np.float64), lam, K, K) for k in range(B)]
+    bits = np.array([[t[3] for t in r.trace] for r in refs], np.uint8)
+    prm = T.default_params(fixed_inner_iters=K, max_inner=K, kernel_path=3)
+    out = solver.inner(D, J, params=prm, rho_replay=bits, trace=True)
+    rep = out["rep"]
+    assert np.all(rep["kernel_path"] == 3)
+    for k in range(B):
+        a = out["A"][k].double().cpu().numpy()
+        e = out["E"][k].double().cpu().numpy()
+        ra = np.linalg.norm(a - refs[k].A) / np.linalg.norm(refs[k].A)
+        re = np.linalg.norm(e - refs[k].E) / max(np.linalg.norm(refs[k].E), 1e-30)
+        assert ra < 1e-4 and re < 1e-4, (m, n, p, K, k, ra, re)
+        assert rep["inner_iters"][k] == K
+        # the mu sequence is the oracle's (mu_0 from the exact sigma_1, Z3; replayed rho)
+        mus = out["trace"][k, :K, 0].double().cpu().numpy()
+        np.testing.assert_allclose(mus, [t[0] for t in refs[k].trace], rtol=1e-5)
+
+
+def test_inner_multi_cta_matches_cta_kernel(solver, T):
+    """Free-running at 100 x 100: the multi-CTA path and the CTA-per-patch kernel stop on the same
+    iteration with the same objective (both fp32; independent Jacobi orderings)."""
+    insts = [ts.table1_instance(100, 6, s) for s in range(3)]
+    D = np.stack([i["D"] for i in insts]).astype(np.float32)
+    J = np.stack([i["J"] for i in insts]).astype(np.float32)
+    r1 = solver.inner(D, J, params=T.default_params(kernel_path=1))["rep"]
+    r3 = solver.inner(D, J, params=T.default_params(kernel_path=3))["rep"]
+    assert np.all(r3["status"] == T.CONVERGED)
+    assert np.all(np.abs(r1["inner_iters"] - r3["inner_iters"]) <= 1)
+    np.testing.assert_allclose(r3["objective"], r1["objective"], rtol=1e-4)
+
+
+def test_inner_free_running_table1_300(solver, T):
+    """Statistical pin of Table 1 at 300 x 300: objective 1123.67, ~22 iterations; and the
+    oracle's own stop iteration on the first instances."""
+    B = 4
+    insts = [ts.table1_instance(300, 6, s) for s in range(B)]
+    D = np.stack([i["D"] for i in insts]).astype(np.float32)
+    J = np.stack([i["J"] for i in insts]).astype(np.float32)
+    out = solver.inner(D, J)
+    rep = out["rep"]
+    assert np.all(rep["status"] == T.CONVERGED)
+    assert np.all(rep["kernel_path"] == 3)
+    assert np.mean(rep["objective"]) == pytest.approx(1123.67, rel=0.02)
+    assert 12 <= np.mean(rep["inner_iters"]) <= 40
+    lam = 1 / math.sqrt(300)
+    for k in range(2):
+        r = _inner_ref(D[k].astype(np.float64), J[k].astype(np.float64), lam, 0, 1000)
+        assert abs(int(rep["inner_iters"][k]) - r.iters) <= 1
+        assert rep["objective"][k] == pytest.approx(O.objective(r.A, r.E, lam), rel=1e-4)
+
+
+def test_inner_free_running_table1_1000(solver, T):
+    """Table 1's largest size (1000 x 1000): objective 6844.14, 23 iterations (paper); the
+    objective is pinned statistically (2%), the iteration count to the paper's range."""
+    B = 2
+    insts = [ts.table1_instance(1000, 6, s) for s in range(B)]
+    D = np.stack([i["D"] for i in insts]).astype(np.float32)
+    J = np.stack([i["J"] for i in insts]).astype(np.float32)
+    out = solver.inner(D, J)
+    rep = out["rep"]
+    assert np.all(rep["status"] == T.CONVERGED)
+    assert np.mean(rep["objective"]) == pytest.approx(6844.14, rel=0.02)
+    assert 12 <= np.mean(rep["inner_iters"]) <= 40
+    assert np.all(rep["sweep_cap_hits"] == 0)
