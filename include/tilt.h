@@ -95,9 +95,11 @@ typedef struct {
   /* window size of the call (all boxes share it). 0: read back from boxes[0] with a stream sync;
    * > 0: taken as given (no host sync; the call is then graph-capturable). */
   int32_t win_h, win_w;
-  /* kernel family: 0 = auto (currently the CTA-per-patch kernels), 1 = CTA-per-patch kernels,
-   * 2 = warp-per-patch kernel (m <= 64 and n <= 50; TILT_E_ARG otherwise). Both compute the same
-   * method; they differ only in data layout and Jacobi ordering. */
+  /* kernel family: 0 = auto (the CTA-per-patch kernels up to 256 x 256, the multi-CTA path above),
+   * 1 = CTA-per-patch kernels, 2 = warp-per-patch kernel (m <= 64 and n <= 50; TILT_E_ARG otherwise),
+   * 3 = multi-CTA path (tilt_inner_batch only, LADMAP, m, n <= 1024: one problem spread over many
+   * CTAs, block-cyclic Jacobi, cuBLAS SGEMMs). All compute the same method; they
+   * differ in data layout, Jacobi ordering and how a problem maps to the GPU. */
   int32_t kernel_path;
   /* Newton-Schulz re-orthonormalisation of the carried V (reading Z14) after every ns_period-th
    * LADMAP SVT of an inner loop (and after the last one); <= 1: after every SVT. Default 4 (the
@@ -144,7 +146,8 @@ typedef struct {
   int32_t device;        /* CUDA device ordinal */
   void* stream;          /* cudaStream_t, NULL = legacy default stream */
   int32_t max_batch;     /* largest B of any call */
-  int32_t max_m, max_n;  /* largest window (<= 256 each) */
+  int32_t max_m, max_n;  /* largest window (<= 1024 each; tilt_solve_batch serves windows up to
+                            256 x 256, tilt_inner_batch / tilt_svt_batch up to 1024 x 1024) */
   int32_t max_p;         /* 6 or 8 */
   int64_t max_image_elems; /* largest n_images*H*W of a pyramid call (0: no pyramid workspace) */
 } tilt_create_opts;
@@ -208,7 +211,8 @@ tilt_status tilt_warp_batch(tilt_handle* h, const float* images, int32_t n_image
  * [B][m][n] with per-matrix eps [B], by warm one-sided Jacobi. V_io [B][n][n] row-major: input
  * warm start (NULL -> identity) and output right singular vectors (may be NULL). Outputs:
  * A [B][m][n]; sigma [B][n] singular values of M (unsorted, Jacobi column order; may be NULL);
- * sweeps [B] int32 (may be NULL). m, n <= 256. */
+ * sweeps [B] int32 (may be NULL). m, n <= 1024 (above 256: the multi-CTA path, which allocates its
+ * workspace on first use, B x ~(10 + p) m n floats). */
 tilt_status tilt_svt_batch(tilt_handle* h, const float* M, int32_t B, int32_t m, int32_t n,
                            const float* eps, float* V_io, float* A, float* sigma, int32_t* sweeps);
 
@@ -223,14 +227,18 @@ tilt_status tilt_project_batch(tilt_handle* h, const float* J, const float* Q, i
  * (not normalised) and J [B][p][m][n] with optional Q [B][l][p], cold start A_0 = D, E_0 = Y_0 = 0.
  * Uses prm (lambda, mu0_scale, mu_max_ratio, rho0, eps1, eps2, max_inner, fixed_inner_iters,
  * rho_replay [B][max_inner], trace [B][max_inner][4], Jacobi controls). Outputs A, E, Y [B][m][n]
- * (Y may be NULL) and rep [B] (inner_iters, jacobi_sweeps, objective, crit1, crit2, rank...). */
+ * (Y may be NULL) and rep [B] (inner_iters, jacobi_sweeps, objective, crit1, crit2, rank...).
+ * m, n <= 1024: windows above 256 (or prm->kernel_path = 3) run on the multi-CTA path, which
+ * allocates its workspace on first use (B x ~(10 + p) m n floats) and synchronises the handle's
+ * stream once per Jacobi sweep and per LADMAP iteration (it reads an active-problem counter). */
 tilt_status tilt_inner_batch(tilt_handle* h, const float* D, const float* J, const float* Q,
                              int32_t l, int32_t B, int32_t m, int32_t n, int32_t p,
                              const tilt_params* prm, float* A, float* E, float* Y,
                              tilt_report* rep);
 
-/* Kernel family used by tilt_svt_batch: 0 = auto (CTA-per-patch), 1 = CTA-per-patch,
- * 2 = warp-per-patch (m <= 64, n <= 50) (step parity of both implementations). */
+/* Kernel family used by tilt_svt_batch: 0 = auto (CTA-per-patch up to 256 x 256, else multi-CTA),
+ * 1 = CTA-per-patch, 2 = warp-per-patch (m <= 64, n <= 50), 3 = multi-CTA block-cyclic Jacobi
+ * (m, n <= 1024) (step parity of every implementation). */
 tilt_status tilt_set_svt_path(tilt_handle* h, int32_t path);
 
 /* Number of kernel launches issued by this handle since creation (for bench accounting). */
