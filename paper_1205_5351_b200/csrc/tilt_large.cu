@@ -737,12 +737,16 @@ __global__ void __launch_bounds__(RNT, 1) k_round(Args a, int r) {
   if (tid == 0) s_any = s_big = s_cnt = 0;
   // stage the columns (float4; rows >= ldm zero), W = I
   constexpr int C4 = MAXD / 4;
+  // cp.async (16 B per request, all in flight at once; src-size 0 zero-fills the padding)
   for (int e = tid; e < NCOL * C4; e += RNT) {
     const int c = e / C4, i4 = e % C4;
-    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (cvalid(c) && 4 * i4 < L.ldm) v = *reinterpret_cast<const float4*>(Bm + (size_t)gcol(c) * L.ldm + 4 * i4);
-    sm4[e] = v;
+    const bool in = cvalid(c) && 4 * i4 < L.ldm;
+    const float* src = in ? Bm + (size_t)gcol(c) * L.ldm + 4 * i4 : Bm;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(sm4 + e)), "l"(src),
+                 "r"(in ? 16 : 0)
+                 : "memory");
   }
+  asm volatile("cp.async.wait_all;" ::: "memory");
   for (int e = tid; e < NCOL * NCOL; e += RNT) W[e] = (e / NCOL == e % NCOL) ? 1.f : 0.f;
   __syncthreads();
   using CL = Col<RPL, 32>;
@@ -757,58 +761,91 @@ __global__ void __launch_bounds__(RNT, 1) k_round(Args a, int r) {
   const float tol2 = a.tol * a.tol, big2 = a.big2;
   const float amin = (float)(a.tiny2 * st->fro2);
   int rot = 0, big = 0, cnt = 0;
-  constexpr int STEPS = CROSS ? BW : BW - 1;
-  for (int s = 0; s < STEPS; ++s) {
-    int i, j;
-    bool on;
-    if (CROSS) {
-      i = warp;
-      j = BW + (warp + s) % BW;
-      on = true;
-    } else {
-      const int q = BW - 1, k = warp;
-      on = k < BW / 2;
-      i = k == 0 ? q : (s + k) % q;
-      j = k == 0 ? s : (s - k + q) % q;
-      if (!on) i = j = 0;
-    }
-    const bool valid = on && cvalid(i) && cvalid(j);
-    if (valid) {  // warp-uniform
-      CL xi, xj;
-      const uint32_t ai = sX + i * MAXD * 4 + lane * 16, aj = sX + j * MAXD * 4 + lane * 16;
-      xi.sload_full(ai);
-      xj.sload_full(aj);
-      const float g = unit_sum<32>(xi.dot(xj));
-      const float4 ni = ns[i], nj = ns[j];
-      const float gam = g * ni.y * nj.y;
-      const float ab = ni.x * nj.x;
-      const bool doit = ni.x > amin && nj.x > amin && gam * gam > tol2 * ab;
-      if (doit) {
-        const Rot rp = rot_params(ni, nj, gam, true);
+  // one rotation of local columns (i, j) with x_i, x_j, their states and W entries in registers
+  auto rotate = [&](CL& xi, CL& xj, float4& ni, float4& nj, float& wi, float& wj) -> bool {
+    const float g = unit_sum<32>(xi.dot(xj));
+    const float gam = g * ni.y * nj.y;
+    const float ab = ni.x * nj.x;
+    const bool doit = ni.x > amin && nj.x > amin && gam * gam > tol2 * ab;
+    if (doit) {  // warp-uniform
+      const Rot rp = rot_params(ni, nj, gam, true);
 #pragma unroll
-        for (int e = 0; e < RPL; ++e) {
-          const float o = xi.v[e];
-          xi.v[e] = fmaf(-rp.ca, xj.v[e], o);
-          xj.v[e] = fmaf(rp.cb, o, xj.v[e]);
-        }
-        xi.sstore(ai, 0xffffffffu);
-        xj.sstore(aj, 0xffffffffu);
-        if (lane < NCOL) {
-          const float wi = W[i * NCOL + lane], wj = W[j * NCOL + lane];
-          W[i * NCOL + lane] = fmaf(-rp.ca, wj, wi);
-          W[j * NCOL + lane] = fmaf(rp.cb, wi, wj);
-        }
-        if (lane == 0) {
-          const float sx = rp.c * fmaf(rp.t, rp.t, 1.f);  // sqrt(1 + t^2)
-          ns[i] = make_float4(fmaxf(fmaf(-rp.t, gam, ni.x), 0.f), rp.c * ni.y, sx * ni.z, 0.f);
-          ns[j] = make_float4(fmaf(rp.t, gam, nj.x), rp.c * nj.y, sx * nj.z, 0.f);
-        }
-        rot = 1;
-        cnt += 1;
-        big |= gam * gam > big2 * ab ? 1 : 0;
+      for (int e = 0; e < RPL; ++e) {
+        const float o = xi.v[e];
+        xi.v[e] = fmaf(-rp.ca, xj.v[e], o);
+        xj.v[e] = fmaf(rp.cb, o, xj.v[e]);
       }
+      const float w0 = wi;
+      wi = fmaf(-rp.ca, wj, w0);
+      wj = fmaf(rp.cb, w0, wj);
+      const float sx = rp.c * fmaf(rp.t, rp.t, 1.f);  // sqrt(1 + t^2)
+      ni = make_float4(fmaxf(fmaf(-rp.t, gam, ni.x), 0.f), rp.c * ni.y, sx * ni.z, 0.f);
+      nj = make_float4(fmaf(rp.t, gam, nj.x), rp.c * nj.y, sx * nj.z, 0.f);
+      rot = 1;
+      cnt += 1;
+      big |= gam * gam > big2 * ab ? 1 : 0;
     }
-    __syncthreads();
+    return doit;
+  };
+  if constexpr (CROSS) {
+    // warp w keeps column w of block I (x, state, its W column entry) in registers for all 16
+    // steps; step s pairs it with column BW + (w + s) % BW of block J, loaded from shared memory
+    const int i = warp;
+    const bool vi = cvalid(i);
+    const uint32_t ai = sX + i * MAXD * 4 + lane * 16;
+    CL xi;
+    xi.sload_full(ai);
+    float4 ni = ns[i];
+    float wi = W[i * NCOL + lane];
+    for (int s = 0; s < BW; ++s) {
+      const int j = BW + (warp + s) % BW;
+      if (vi && cvalid(j)) {  // warp-uniform
+        const uint32_t aj = sX + j * MAXD * 4 + lane * 16;
+        CL xj;
+        xj.sload_full(aj);
+        float4 nj = ns[j];
+        float wj = W[j * NCOL + lane];
+        if (rotate(xi, xj, ni, nj, wi, wj)) {
+          xj.sstore(aj, 0xffffffffu);
+          W[j * NCOL + lane] = wj;
+          if (lane == 0) ns[j] = nj;
+        }
+      }
+      __syncthreads();
+    }
+    if (vi) {
+      xi.sstore(ai, 0xffffffffu);
+      W[i * NCOL + lane] = wi;
+      if (lane == 0) ns[i] = ni;
+    }
+  } else {
+    for (int s = 0; s < BW - 1; ++s) {  // circle method on the block's BW columns, BW/2 warps
+      const int q = BW - 1, k = warp;
+      const bool on = k < BW / 2;
+      const int i = on ? (k == 0 ? q : (s + k) % q) : 0;
+      const int j = on ? (k == 0 ? s : (s - k + q) % q) : 0;
+      if (on && cvalid(i) && cvalid(j)) {  // warp-uniform
+        CL xi, xj;
+        const uint32_t ai = sX + i * MAXD * 4 + lane * 16, aj = sX + j * MAXD * 4 + lane * 16;
+        xi.sload_full(ai);
+        xj.sload_full(aj);
+        float4 ni = ns[i], nj = ns[j];
+        float wi = lane < NCOL ? W[i * NCOL + lane] : 0.f, wj = lane < NCOL ? W[j * NCOL + lane] : 0.f;
+        if (rotate(xi, xj, ni, nj, wi, wj)) {
+          xi.sstore(ai, 0xffffffffu);
+          xj.sstore(aj, 0xffffffffu);
+          if (lane < NCOL) {
+            W[i * NCOL + lane] = wi;
+            W[j * NCOL + lane] = wj;
+          }
+          if (lane == 0) {
+            ns[i] = ni;
+            ns[j] = nj;
+          }
+        }
+      }
+      __syncthreads();
+    }
   }
   if (lane == 0 && rot) {
     atomicOr(&s_any, 1);
@@ -839,18 +876,24 @@ __global__ void __launch_bounds__(RNT, 1) k_round(Args a, int r) {
 #pragma unroll
     for (int c = 0; c < NCOL; ++c) v[c] = cvalid(c) ? V[(size_t)gcol(c) * L.ldn + row] : 0.f;
 #pragma unroll 1
-    for (int c2 = 0; c2 < NCOL; ++c2) {
-      const float4* w4 = reinterpret_cast<const float4*>(W + c2 * NCOL);
-      float o0 = 0.f, o1 = 0.f;
+    for (int c2 = 0; c2 < NCOL; c2 += 8) {  // 8 outputs at a time: 8 independent FMA chains
+      float o[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) o[u] = 0.f;
 #pragma unroll
       for (int c = 0; c < NCOL; c += 4) {
-        const float4 ww = w4[c / 4];
-        o0 = fmaf(v[c], ww.x, o0);
-        o1 = fmaf(v[c + 1], ww.y, o1);
-        o0 = fmaf(v[c + 2], ww.z, o0);
-        o1 = fmaf(v[c + 3], ww.w, o1);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const float4 ww = *reinterpret_cast<const float4*>(W + (c2 + u) * NCOL + c);
+          o[u] = fmaf(v[c], ww.x, o[u]);
+          o[u] = fmaf(v[c + 1], ww.y, o[u]);
+          o[u] = fmaf(v[c + 2], ww.z, o[u]);
+          o[u] = fmaf(v[c + 3], ww.w, o[u]);
+        }
       }
-      if (cvalid(c2)) V[(size_t)gcol(c2) * L.ldn + row] = o0 + o1;
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (cvalid(c2 + u)) V[(size_t)gcol(c2 + u) * L.ldn + row] = o[u];
     }
   }
 }
