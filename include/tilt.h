@@ -118,6 +118,9 @@ typedef struct {
    * (0: the occupancy limit). Fewer in-flight patches run faster each, which shortens the tail of
    * a batch whose per-patch work varies widely. */
   int32_t ctas_per_sm;
+  /* 2-level pyramid only: 1 = the fine level's first inner loop starts from the coarse level's A, E,
+   * Y replicated 2x2 and halved (reading Z26; needs vws); 0 = tau only (Z18). */
+  int32_t pyramid_warm;
 } tilt_params;
 
 /* Per-patch report (device array written by tilt_solve_batch). */

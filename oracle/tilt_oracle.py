@@ -60,6 +60,8 @@ class Params:
     adm_rho: float = 1.25       # ADM penalty growth mu_{k+1} = rho mu_k, unbounded (reading Z24)
     adm_tol: float = 1e-6       # ADM stop: ||D + J dtau - A - E||_F / ||D||_F < adm_tol (reading Z24;
                                 # 1e-7 reproduces Table 1's ADM counts in fp64, 1e-6 is fp32-resolvable)
+    pyramid_warm: bool = False  # 2-level pyramid: the fine level's first inner loop starts from the
+                                # coarse A, E, Y upsampled (reading Z26)
 
 
 # ----------------------------------------------------------------------------------------------
@@ -560,7 +562,7 @@ def relative_rank(sigma_a):
     return int(np.sum(ratio > 1e-3)), bool(np.any((ratio >= 3e-4) & (ratio <= 3e-3)))
 
 
-def tilt(image, box, tau0, kind, prm: Params = Params(), rho_replay=None):
+def tilt(image, box, tau0, kind, prm: Params = Params(), rho_replay=None, warm=None):
     """Algorithm 1 for one window; returns a dict (tau, A, E, Y, report fields, traces).
 
     Step 1: normalise D o tau and compute J; Q per reading Z10.
@@ -571,11 +573,16 @@ def tilt(image, box, tau0, kind, prm: Params = Params(), rho_replay=None):
     Step 4: tau^{i+1} = tau^i + Delta tau* (P:568-570).
     Outer stop ("while not converged", reading Z9).
     ``rho_replay``: optional list (per outer iteration) of 0/1 sequences (reading Z21).
+    ``warm``: optional (A, E, Y) that replace the first inner loop's cold start A_0 = D_hat,
+    E_0 = Y_0 = 0 (then Y_0 <- W^TW Y as every warm start, Eq. Y_new_warmstart); used by
+    the pyramid's fine level (reading Z26). Ignored without VWS.
     """
     m, n = int(box[3]), int(box[2])
     lam = prm.lam if prm.lam > 0 else 1.0 / math.sqrt(max(m, n))
     tau = np.asarray(tau0, dtype=np.float64).copy()
     a = e = y = None
+    if warm is not None and prm.vws:
+        a, e, y = (np.asarray(x, dtype=np.float64).copy() for x in warm)
     f_prev = None
     status = MAX_OUTER
     stop_rule = STOP_NONE
@@ -663,9 +670,20 @@ def downsample2x(image):
     return 0.25 * (img[0::2, 0::2] + img[0::2, 1::2] + img[1::2, 0::2] + img[1::2, 1::2])
 
 
+def upsample2x_warm(x):
+    """Coarse-level state -> fine-level warm start (reading Z26): 2x2 replication, halved. The
+    coarse and fine D_hat are both unit-norm and replication doubles the Frobenius and spectral
+    norms, so up(X)/2 keeps ||.||_F and ||.||_2 (the dual's ||Y||_2 <= 1 and, as lambda_f =
+    lambda_c/sqrt(2) >= lambda_c/2, ||Y||_inf <= lambda_f stay feasible)."""
+    x = np.asarray(x, dtype=np.float64)
+    return 0.5 * np.repeat(np.repeat(x, 2, axis=0), 2, axis=1)
+
+
 def tilt_pyramid(image, box, tau0, kind, prm: Params = Params(), levels: int = 2):
     """Coarse-to-fine TILT (reading Z18): solve on the 2x2-downsampled image with box/2, then on the
-    full image starting from the coarse tau (unchanged: the normalised frames coincide)."""
+    full image starting from the coarse tau (unchanged: the normalised frames coincide); with
+    ``prm.pyramid_warm`` the fine level's first inner loop also starts from the coarse A, E, Y
+    (upsample2x_warm, reading Z26) when the coarse level produced them."""
     if levels <= 1:
         return tilt(image, box, tau0, kind, prm)
     coarse_img = np.asarray(image, dtype=np.float64)
@@ -676,7 +694,10 @@ def tilt_pyramid(image, box, tau0, kind, prm: Params = Params(), levels: int = 2
     res_c = tilt(coarse_img.astype(np.float32).astype(np.float64), (x0, y0, w, h), tau0, kind,
                  replace(prm, lam=prm.lam))
     # the fine level always starts from the coarse tau (a failed coarse level keeps its last tau)
-    res_f = tilt(image, box, res_c["tau"], kind, prm)
+    warm = None
+    if prm.pyramid_warm and levels == 2 and res_c["status"] in (CONVERGED, MAX_OUTER) and res_c["A"] is not None:
+        warm = tuple(upsample2x_warm(res_c[k]) for k in ("A", "E", "Y"))
+    res_f = tilt(image, box, res_c["tau"], kind, prm, warm=warm)
     for key in ("outer_iters", "inner_iters"):
         res_f[key] += res_c[key]
     res_f["coarse"] = res_c

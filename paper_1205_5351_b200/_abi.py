@@ -48,6 +48,7 @@ class TiltParams(ctypes.Structure):
         ("adm_rho", ctypes.c_float),
         ("adm_tol", ctypes.c_float),
         ("ctas_per_sm", ctypes.c_int32),
+        ("pyramid_warm", ctypes.c_int32),
     ]
 
 

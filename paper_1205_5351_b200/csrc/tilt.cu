@@ -57,6 +57,7 @@ struct tilt_handle {
   float* coarse_images = nullptr;
   int* coarse_boxes = nullptr;
   tilt_report* coarse_rep = nullptr;
+  float* coarse_aey = nullptr;  // pyramid warm start: coarse A, E, Y [3][B][m/2][n/2]
   // host-entry staging
   float* h_images = nullptr;
   int* h_patch = nullptr;
@@ -134,6 +135,8 @@ bool params_ok(const tilt_params* p) {
   if (p->inner_solver == 1 && p->kernel_path == 3) return false;  // the multi-CTA path runs LADMAP only
   if (p->inner_solver < 0 || p->inner_solver > 1) return false;
   if (p->ctas_per_sm < 0) return false;
+  if (p->pyramid_warm < 0 || p->pyramid_warm > 1) return false;
+  if (p->pyramid_warm && p->kernel_path == 2) return false;  // the warp-per-patch kernel starts cold
   if (p->inner_solver == 1 && p->kernel_path == 2) return false;  // the warp-per-patch kernel runs LADMAP only
   if (!std::isfinite(p->adm_rho) || !std::isfinite(p->adm_tol) || p->adm_rho < 1.f || p->adm_tol <= 0.f) return false;
   return true;
@@ -368,7 +371,7 @@ tilt_status tilt_default_params(tilt_params* prm) {
 tilt_status tilt_destroy(tilt_handle* h) {
   if (!h) return TILT_OK;
   cudaSetDevice(h->device);
-  void* ptrs[] = {h->ws, h->counter, h->coarse_images, h->coarse_boxes, h->coarse_rep, h->h_images, h->h_patch,
+  void* ptrs[] = {h->ws, h->counter, h->coarse_images, h->coarse_boxes, h->coarse_rep, h->coarse_aey, h->h_images, h->h_patch,
                   h->h_boxes, h->h_tau0, h->h_tau, h->h_A, h->h_E, h->h_rep};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -435,6 +438,9 @@ tilt_status tilt_create(tilt_handle** out, const tilt_create_opts* o) {
       return fail(e, "cudaMalloc(coarse)");
     if ((e = cudaMalloc(&h->coarse_boxes, 4 * nb * sizeof(int) + 64)) != cudaSuccess) return fail(e, "cudaMalloc");
     if ((e = cudaMalloc(&h->coarse_rep, nb * sizeof(tilt_report) + 64)) != cudaSuccess) return fail(e, "cudaMalloc");
+    if ((e = cudaMalloc(&h->coarse_aey, 3 * nb * (size_t)(h->max_m / 2) * (h->max_n / 2) * sizeof(float) + 64)) !=
+        cudaSuccess)
+      return fail(e, "cudaMalloc(coarse A/E/Y)");
     if ((e = cudaMalloc(&h->h_images, (size_t)h->max_image_elems * sizeof(float))) != cudaSuccess)
       return fail(e, "cudaMalloc");
     if ((e = cudaMalloc(&h->h_patch, nb * sizeof(int) + 64)) != cudaSuccess) return fail(e, "cudaMalloc");
@@ -466,7 +472,8 @@ tilt_status tilt_set_svt_path(tilt_handle* h, int32_t path) {
 static tilt_status solve_level(tilt_handle* h, const float* images, int32_t n_images, int32_t H, int32_t W,
                                const int32_t* patch_image, const int32_t* boxes, const float* tau0, int32_t B,
                                int m, int n, int32_t kind, const tilt_params* prm, float* tau_out, float* A_out,
-                               float* E_out, float* Y_out, tilt_report* rep, const tilt_report* rep_prev) {
+                               float* E_out, float* Y_out, tilt_report* rep, const tilt_report* rep_prev,
+                               const float* warm_aey = nullptr, const tilt_report* warm_rep = nullptr) {
   SolveArgs a;
   memset(&a, 0, sizeof(a));
   a.images = images;
@@ -490,6 +497,13 @@ static tilt_status solve_level(tilt_handle* h, const float* images, int32_t n_im
   a.rep_prev = rep_prev;
   a.counter = h->counter;
   a.ctas_per_sm = prm->ctas_per_sm;
+  if (warm_aey) {
+    const size_t cn = (size_t)B * (m / 2) * (n / 2);
+    a.warm_A = warm_aey;
+    a.warm_E = warm_aey + cn;
+    a.warm_Y = warm_aey + 2 * cn;
+    a.warm_rep = warm_rep;
+  }
   if (prm->kernel_path == 3 || m > 256 || n > 256) {
     g_last_error = "tilt_solve_batch: windows up to 256 x 256 (the multi-CTA path serves tilt_inner_batch / tilt_svt_batch)";
     return TILT_E_ARG;
@@ -558,11 +572,15 @@ tilt_status tilt_solve_batch(tilt_handle* h, const float* images, int32_t n_imag
     tilt_params pc = *prm;
     pc.rho_replay = nullptr;
     pc.trace = nullptr;
+    const bool pw = prm->pyramid_warm != 0 && prm->vws != 0;
+    const size_t cn = (size_t)B * (m / 2) * (n / 2);
+    float* cA = pw ? h->coarse_aey : nullptr;
     s = solve_level(h, h->coarse_images, n_images, H / 2, W / 2, patch_image, h->coarse_boxes, tau0, B, m / 2,
-                    n / 2, kind, &pc, tau_out, nullptr, nullptr, nullptr, h->coarse_rep, nullptr);
+                    n / 2, kind, &pc, tau_out, cA, pw ? cA + cn : nullptr, pw ? cA + 2 * cn : nullptr, h->coarse_rep,
+                    nullptr);
     if (s != TILT_OK) return s;
     return solve_level(h, images, n_images, H, W, patch_image, boxes, tau_out, B, m, n, kind, prm, tau_out, A_out,
-                       E_out, Y_out, rep, rep ? h->coarse_rep : nullptr);
+                       E_out, Y_out, rep, rep ? h->coarse_rep : nullptr, cA, h->coarse_rep);
   }
   return solve_level(h, images, n_images, H, W, patch_image, boxes, tau0, B, m, n, kind, prm, tau_out, A_out, E_out,
                      Y_out, rep, nullptr);

@@ -407,6 +407,11 @@ struct SolveArgs {
   float* ws;
   size_t ws_stride;
   int ctas_per_sm;  // host-side launch cap (0: occupancy limit)
+  // pyramid warm start (reading Z26): the coarse level's A, E, Y [B][m/2][n/2] and its reports
+  const float* warm_A;
+  const float* warm_E;
+  const float* warm_Y;
+  const tilt_report* warm_rep;
 };
 
 template <class C>
@@ -467,8 +472,24 @@ __device__ void solve_patch(const SolveArgs& a, Ctx<C>& cx, int b) {
       status = st;
       break;
     }
-    // Step 2 warm start (Eq. warm_start; Eq. Y_new_warmstart; Z4)
-    if (!have_state || !P.vws) {
+    // Step 2 warm start (Eq. warm_start; Eq. Y_new_warmstart; Z4); the
+    // pyramid's fine level may start from the coarse state replicated 2x2 and halved (Z26)
+    const bool from_coarse = it == 0 && P.vws && a.warm_A &&
+                             (a.warm_rep[b].status == TILT_PATCH_CONVERGED || a.warm_rep[b].status == TILT_PATCH_MAX_OUTER);
+    if (from_coarse) {
+      const int mc = m / 2, nc = n / 2;
+      const size_t o = (size_t)b * mc * nc;
+      for (PixIter pi(threadIdx.x, C::NT, ld); pi.idx < pl; pi.next(C::NT)) {
+        if (pi.i >= m) continue;
+        const size_t c = o + (size_t)(pi.i / 2) * nc + pi.j / 2;
+        cx.A[pi.idx] = 0.5f * a.warm_A[c];
+        cx.E[pi.idx] = 0.5f * a.warm_E[c];
+        cx.Y[pi.idx] = 0.5f * a.warm_Y[c];
+      }
+      __syncthreads();
+      project_plane<C, PR>(cx, cx.Y);
+      have_state = true;
+    } else if (!have_state || !P.vws) {
       for (int idx = threadIdx.x; idx < pl; idx += C::NT) {
         cx.A[idx] = cx.D[idx];
         cx.E[idx] = 0.f;

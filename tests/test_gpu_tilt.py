@@ -236,14 +236,17 @@ def test_ragged_sizes_fixed_count(solver, T, m, n, kind):
         assert np.max(np.abs(out["tau"][k].double().cpu().numpy() - refs[k]["tau"])) < 1e-3
 
 
-def test_pyramid_config3_small(solver, T):
+@pytest.mark.parametrize("warm", [0, 1])
+def test_pyramid_config3_small(solver, T, warm):
+    """2-level pyramid (reading Z18); warm = 1: the fine level starts from the coarse A, E, Y (Z26)."""
     cfg = ts.CONFIGS[3]
     B, K = 2, 20
     b = ts.gen_batch(cfg, 0, B)
-    prm_o = O.Params(fixed_inner_iters=K, fixed_outer_iters=2, max_inner=K, max_outer=2)
+    prm_o = O.Params(fixed_inner_iters=K, fixed_outer_iters=2, max_inner=K, max_outer=2, pyramid_warm=bool(warm))
     refs = [O.tilt_pyramid(b["images"][k], b["boxes"][k], b["tau0"][k], cfg.kind, prm_o, levels=2)
             for k in range(B)]
-    prm = T.default_params(fixed_inner_iters=K, fixed_outer_iters=2, max_inner=K, max_outer=2, pyramid_levels=2)
+    prm = T.default_params(fixed_inner_iters=K, fixed_outer_iters=2, max_inner=K, max_outer=2, pyramid_levels=2,
+                           pyramid_warm=warm)
     out = solver.solve(b["images"], b["patch_image"], b["boxes"], b["tau0"], cfg.kind, prm)
     rep = T.reports_to_numpy(out["rep"])
     for k in range(B):
