@@ -121,6 +121,12 @@ typedef struct {
   /* 2-level pyramid only: 1 = the fine level's first inner loop starts from the coarse level's A, E,
    * Y replicated 2x2 and halved (reading Z26; needs vws); 0 = tau only (Z18). */
   int32_t pyramid_warm;
+  /* SVT of the LADMAP iterations: 0 = warm one-sided Jacobi every iteration; 1 = LADMAP+SVDWS
+   * (Algorithm 2): when ||M_k - M_{k-1}||_F < svd_ws_gate ||D||_F one Taylor step along
+   * the Cayley curve from the previous SVD replaces the Jacobi SVT (reading Z27; multi-CTA path,
+   * tilt_inner_batch, m >= n). */
+  int32_t svd_mode;
+  float svd_ws_gate;      /* default 2e-5 */
 } tilt_params;
 
 /* Per-patch report (device array written by tilt_solve_batch). */
@@ -142,7 +148,8 @@ typedef struct {
   float dtau_inf;         /* ||dtau||_inf of the last outer iteration */
   float mu_last;          /* mu_K of the last SVT */
   int32_t jacobi_rotations; /* Jacobi rotations applied, summed over the LADMAP SVTs */
-  int32_t kernel_path;      /* 1: CTA-per-patch kernel, 2: warp-per-patch kernel solved this patch */
+  int32_t kernel_path;      /* 1: CTA-per-patch kernel, 2: warp-per-patch kernel, 3: multi-CTA path */
+  int32_t svd_warm_steps;   /* SVTs replaced by the Alg. 2 warm step (svd_mode 1) */
 } tilt_report;
 
 typedef struct {

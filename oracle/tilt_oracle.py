@@ -400,7 +400,13 @@ def cayley_objective(m_k, u, sig, v, t):
 class SvdWarm:
     """The SVD warm start of LADMAP+SVDWS (Algorithm 2): keeps the previous (approximate) SVD and
     M_{k-1}; S_eps(M_k) uses one ``svd_warm_start`` step when ||M_k - M_{k-1}||_F < eps_svd, else a
-    full SVD ("Else do full svd"). m < n is handled on the transpose (S_eps(M^T) = S_eps(M)^T)."""
+    full SVD ("Else do full svd"). m < n is handled on the transpose (S_eps(M^T) = S_eps(M)^T).
+    Reading Z27: a step whose Cayley generators are not small, ||(t*/2) P_U||_F >= 0.5 or
+    ||(t*/2) P_V||_F >= 0.5, is rejected (full SVD instead) -- the GPU solves the Cayley systems by
+    Richardson iteration, which needs them below 1. ``decisions`` logs 1 (warm step) / 0 (full SVD)
+    per call."""
+
+    CAYLEY_MAX = 0.5
 
     def __init__(self, eps_svd):
         self.eps_svd = eps_svd
@@ -408,18 +414,29 @@ class SvdWarm:
         self.m_prev = None
         self.warm_steps = 0
         self.full_svds = 0
+        self.decisions = []
 
     def svt(self, m_k, eps):
         m_k = np.asarray(m_k, dtype=np.float64)
         tr = m_k.shape[0] < m_k.shape[1]
         x = m_k.T if tr else m_k
+        step = None
         if self.prev is not None and np.linalg.norm(x - self.m_prev) < self.eps_svd:
-            u, sig, v, _ = svd_warm_start(x, *self.prev)
+            u, sig, v, t = svd_warm_start(x, *self.prev)
+            w = (self.prev[0] * self.prev[1]) @ self.prev[2].T
+            p_u = w @ x.T - x @ w.T
+            p_v = w.T @ x - x.T @ w
+            if max(np.linalg.norm(0.5 * t * p_u), np.linalg.norm(0.5 * t * p_v)) < self.CAYLEY_MAX:
+                step = (u, sig, v)
+        if step is not None:
+            u, sig, v = step
             self.warm_steps += 1
+            self.decisions.append(1)
         else:
             u, sig, vt = np.linalg.svd(x, full_matrices=False)
             v = vt.T
             self.full_svds += 1
+            self.decisions.append(0)
         self.prev = (u, sig, v)
         self.m_prev = x.copy()
         a = (u * shrink(sig, eps)) @ v.T

@@ -49,6 +49,8 @@ class TiltParams(ctypes.Structure):
         ("adm_tol", ctypes.c_float),
         ("ctas_per_sm", ctypes.c_int32),
         ("pyramid_warm", ctypes.c_int32),
+        ("svd_mode", ctypes.c_int32),
+        ("svd_ws_gate", ctypes.c_float),
     ]
 
 
@@ -72,6 +74,7 @@ class TiltReport(ctypes.Structure):
         ("mu_last", ctypes.c_float),
         ("jacobi_rotations", ctypes.c_int32),
         ("kernel_path", ctypes.c_int32),
+        ("svd_warm_steps", ctypes.c_int32),
     ]
 
 

@@ -114,6 +114,8 @@ DevParams to_dev(const tilt_params* prm) {
   P.inner_solver = prm->inner_solver;
   P.adm_rho = prm->adm_rho;
   P.adm_tol = prm->adm_tol;
+  P.svd_mode = prm->svd_mode;
+  P.svd_ws_gate = prm->svd_ws_gate;
   P.rho_replay = prm->rho_replay;
   P.trace = prm->trace;
   return P;
@@ -137,6 +139,8 @@ bool params_ok(const tilt_params* p) {
   if (p->ctas_per_sm < 0) return false;
   if (p->pyramid_warm < 0 || p->pyramid_warm > 1) return false;
   if (p->pyramid_warm && p->kernel_path == 2) return false;  // the warp-per-patch kernel starts cold
+  if (p->svd_mode < 0 || p->svd_mode > 1) return false;
+  if (!std::isfinite(p->svd_ws_gate) || p->svd_ws_gate < 0.f) return false;
   if (p->inner_solver == 1 && p->kernel_path == 2) return false;  // the warp-per-patch kernel runs LADMAP only
   if (!std::isfinite(p->adm_rho) || !std::isfinite(p->adm_tol) || p->adm_rho < 1.f || p->adm_tol <= 0.f) return false;
   return true;
@@ -365,6 +369,8 @@ tilt_status tilt_default_params(tilt_params* prm) {
   prm->inner_solver = 0;
   prm->adm_rho = 1.25f;
   prm->adm_tol = 1e-6f;
+  prm->svd_mode = 0;
+  prm->svd_ws_gate = 2e-5f;
   return TILT_OK;
 }
 
@@ -504,8 +510,8 @@ static tilt_status solve_level(tilt_handle* h, const float* images, int32_t n_im
     a.warm_Y = warm_aey + 2 * cn;
     a.warm_rep = warm_rep;
   }
-  if (prm->kernel_path == 3 || m > 256 || n > 256) {
-    g_last_error = "tilt_solve_batch: windows up to 256 x 256 (the multi-CTA path serves tilt_inner_batch / tilt_svt_batch)";
+  if (prm->kernel_path == 3 || m > 256 || n > 256 || prm->svd_mode != 0) {
+    g_last_error = "tilt_solve_batch: windows up to 256 x 256, svd_mode 0 (the multi-CTA path serves tilt_inner_batch / tilt_svt_batch)";
     return TILT_E_ARG;
   }
   const bool rj_ok = tilt::rjh::fits(m, n);
@@ -734,8 +740,8 @@ tilt_status tilt_inner_batch(tilt_handle* h, const float* D, const float* J, con
   a.E = E;
   a.Y = Y;
   a.rep = rep;
-  if (prm->kernel_path == 3 || m > 256 || n > 256) {
-    if (prm->inner_solver != 0) return TILT_E_ARG;
+  if (prm->kernel_path == 3 || m > 256 || n > 256 || prm->svd_mode == 1) {
+    if (prm->inner_solver != 0 || (prm->svd_mode == 1 && m < n)) return TILT_E_ARG;
     return tilt::lp::inner(lp_ctx(h), D, J, Q, Q ? l : 0, B, m, n, p, a.P, A, E, Y, rep);
   }
   return dispatch<InnerF>(size_class(m, n), h, a);

@@ -60,6 +60,8 @@ struct DevParams {
   int ns_period;
   int inner_solver;      // 0 LADMAP (the paper's), 1 ADM baseline
   float adm_rho, adm_tol;
+  int svd_mode;          // 0 warm Jacobi every iteration, 1 LADMAP+SVDWS (Alg. 2, multi-CTA path)
+  float svd_ws_gate;     // eps_svd = svd_ws_gate ||D||_F
   const uint8_t* rho_replay;
   float* trace;
 };

@@ -55,17 +55,24 @@ struct St {
   int svt_done, big_any, rot_any, sw_cur, cap_cur, rot_cur;
   int sweeps, caps, rotations, aux_sweeps;
   double fro2;  // ||B||_F^2 at the start of the current SVT (negligible-column threshold)
+  // SVD warm start (Algorithm 2, svd_mode 1; readings Z26/Z27)
+  double wacc[8];  // ||M - M_prev||^2, <h0, h1>, ||h1||^2, <h0, h2>, ||P_U||^2, ||P_V||^2
+  float eps_svd, t_star;
+  int warm, have_prev, cay_k, warm_steps;
 };
 
 struct Lay {
   int m, n, p, ldm, ldn;
   size_t plane, vplane;
   size_t oD, oA, oAn, oE, oY, oS, oB, oK, oV, oV2, oT, oSig, oVv, oSt, stride;
+  // SVD warm start buffers (0 when not allocated): U, M_prev, W, H1, Z, H2, X, X2 (m x n),
+  // P_U (m x m, ld = ldm), P_V, Vt, Vt2 (n x n), signed Sigma, P_Sigma (n)
+  size_t oU, oMp, oW, oH1, oZ, oH2, oX, oX2, oPU, oPV, oVt, oVt2, oSg, oPs;
 };
 
 inline size_t up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
-Lay make_lay(int m, int n, int p) {
+Lay make_lay(int m, int n, int p, bool svdws = false) {
   Lay L;
   L.m = m;
   L.n = n;
@@ -89,6 +96,23 @@ Lay make_lay(int m, int n, int p) {
   L.oSig = o; o += up(n, 64);
   L.oVv = o; o += up(n, 64);
   L.oSt = o; o += up(sizeof(St) / 4 + 1, 64);
+  L.oU = L.oMp = L.oW = L.oH1 = L.oZ = L.oH2 = L.oX = L.oX2 = L.oPU = L.oPV = L.oVt = L.oVt2 = L.oSg = L.oPs = 0;
+  if (svdws) {
+    L.oU = o; o += L.plane;
+    L.oMp = o; o += L.plane;
+    L.oW = o; o += L.plane;
+    L.oH1 = o; o += L.plane;
+    L.oZ = o; o += L.plane;
+    L.oH2 = o; o += L.plane;
+    L.oX = o; o += L.plane;
+    L.oX2 = o; o += L.plane;
+    L.oPU = o; o += up((size_t)L.ldm * m, 64);
+    L.oPV = o; o += L.vplane;
+    L.oVt = o; o += L.vplane;
+    L.oVt2 = o; o += L.vplane;
+    L.oSg = o; o += up(n, 64);
+    L.oPs = o; o += up(n, 64);
+  }
   L.stride = o;
   return L;
 }
@@ -567,6 +591,7 @@ __global__ void k_report(Args a, tilt_report* rep) {
     r.mu_last = st->mu;
     r.jacobi_rotations = st->rotations;
     r.kernel_path = 3;
+    r.svd_warm_steps = st->warm_steps;
   }
   rep[b] = r;
 }
@@ -579,13 +604,13 @@ __global__ void k_svt_begin(Args a, const float* __restrict__ eps, int eps_mode)
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= a.B) return;
   St* st = state(a, b);
-  st->svt_done = st->done;
+  st->svt_done = st->done || st->warm;  // a warm-step problem (Alg. 2) skips the Jacobi sweeps
   st->big_any = st->rot_any = 0;
   st->sw_cur = st->cap_cur = st->rot_cur = 0;
   st->fro2 = 0.0;
   if (st->done) return;
   st->eps = eps_mode == 0 ? 1.f / st->mu : (eps_mode == 1 ? eps[b] : 0.f);
-  atomicAdd(a.counter, 1);
+  if (!st->svt_done) atomicAdd(a.counter, 1);
 }
 
 __global__ void k_sweep_end(Args a) {
@@ -608,7 +633,7 @@ __global__ void k_sweep_end(Args a) {
 __global__ void __launch_bounds__(256) k_svt_sig(Args a) {
   const int b = blockIdx.y;
   St* st = state(a, b);
-  if (st->done) return;
+  if (st->done || st->warm) return;
   const int j = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (j >= a.L.n) return;
   const float* w = slot(a, b);
@@ -629,10 +654,11 @@ __global__ void __launch_bounds__(256) k_svt_sig(Args a) {
 
 // SVT statistics (svt_stats in tilt_device.cuh): ||A||_*, sigma_1, #{sigma > eps}, the Z19 rank and
 // band flag; one warp per problem. Also folds the sweep counters into the totals.
-__global__ void __launch_bounds__(32) k_svt_stats(Args a, int count_sweeps) {
+// which: 0 = problems of the Jacobi SVT, 1 = problems of the Alg. 2 warm step (sig holds |Sigma|)
+__global__ void __launch_bounds__(32) k_svt_stats(Args a, int count_sweeps, int which = 0) {
   const int b = blockIdx.x;
   St* st = state(a, b);
-  if (st->done) return;
+  if (st->done || st->warm != which) return;
   const float* sig = slot(a, b) + a.L.oSig;
   const float eps = st->eps;
   const int lane = threadIdx.x, n = a.L.n;
@@ -685,7 +711,7 @@ __global__ void __launch_bounds__(32) k_svt_stats(Args a, int count_sweeps) {
 __global__ void __launch_bounds__(ENT) k_svt_scale(Args a) {
   const int b = blockIdx.y;
   St* st = state(a, b);
-  if (st->done) return;
+  if (st->done || st->warm) return;
   float* w = slot(a, b);
   const float* sig = w + a.L.oSig;
   const float* vv = w + a.L.oVv;
@@ -899,6 +925,234 @@ __global__ void __launch_bounds__(RNT, 1) k_round(Args a, int r) {
 }
 
 // ---------------------------------------------------------------------------------------------
+// SVD warm start (Algorithm 2; Appendix A; oracle.svd_warm_start): for a
+// problem whose M_k is within eps_svd of M_{k-1}, one Taylor step along the Cayley curve from the
+// previous SVD (U, Sigma, V) replaces the Jacobi SVT:
+//   W = U Sigma V^T, P_U = W M^T - M W^T, P_V = W^T M - M^T W, P_Sigma = Sigma - diag(U^T M V),
+//   h1 = P_U W + U P_Sigma V^T - W P_V, Z = h1 + U P_Sigma V^T, h2 = -P_U Z + Z P_V,
+//   t* = -<h0, h1> / (||h1||^2 + <h0, h2>), h0 = M - W,
+//   U <- (I + t/2 P_U)^{-1} (I - t/2 P_U) U, Sigma <- Sigma - t P_Sigma, V likewise with P_V,
+// then A = U T_eps(Sigma) V^T. The products are cuBLAS SGEMMs over the batch; the Cayley systems
+// are solved by Richardson iteration X <- R - (t/2) P X (P skew, so it converges when
+// ||(t/2) P||_F < 1; a step with ||(t/2) P||_F >= 0.5 is rejected for a full SVD, reading Z27).
+// ---------------------------------------------------------------------------------------------
+// dst = src diag(vec) (mode 0), src diag(T_eps(vec)) (mode 1); problems with st->warm == want
+__global__ void __launch_bounds__(ENT) k_colscale(Args a, size_t dst, size_t src, size_t vec, int mode, int want) {
+  const int b = blockIdx.y;
+  St* st = state(a, b);
+  if (st->done || st->warm != want) return;
+  float* w = slot(a, b);
+  const int ldm = a.L.ldm;
+  const float eps = st->eps;
+  FOR_ELEMS(a.L.plane) {
+    const int j = (int)(idx / ldm);
+    float f = j < a.L.n ? w[vec + j] : 0.f;
+    if (mode == 1) f = copysignf(fmaxf(fabsf(f) - eps, 0.f), f);
+    w[dst + idx] = w[src + idx] * f;
+  }
+}
+
+// plane copy (count floats) for problems with st->warm == want (want < 0: every active problem)
+__global__ void __launch_bounds__(ENT) k_copy_if(Args a, size_t dst, size_t src, size_t count, int want) {
+  const int b = blockIdx.y;
+  St* st = state(a, b);
+  if (st->done || (want >= 0 && st->warm != want)) return;
+  float* w = slot(a, b);
+  FOR_ELEMS(count) w[dst + idx] = w[src + idx];
+}
+
+// X <- X - X^T in place (an n x n block, leading dimension ld): the skew part of Eqs.
+// projected_gradient1-2; optionally scaled by t*/2 (scale_t)
+__global__ void __launch_bounds__(ENT) k_skew(Args a, size_t off, int nn, int ld, int scale_t) {
+  const int b = blockIdx.y;
+  St* st = state(a, b);
+  if (st->done || !st->warm) return;
+  float* X = slot(a, b) + off;
+  const float f = scale_t ? 0.5f * st->t_star : 1.f;
+  FOR_ELEMS((size_t)nn * nn) {
+    const int j = (int)(idx / nn), i = (int)(idx % nn);
+    if (scale_t) {
+      X[(size_t)j * ld + i] *= f;
+    } else if (i < j) {
+      const float x = X[(size_t)j * ld + i], y = X[(size_t)i * ld + j];
+      X[(size_t)j * ld + i] = x - y;
+      X[(size_t)i * ld + j] = y - x;
+    } else if (i == j) {
+      X[(size_t)j * ld + i] = 0.f;
+    }
+  }
+}
+
+// ||M - M_prev||_F^2 (the gate of Alg. 2)
+__global__ void __launch_bounds__(ENT) k_ws_diff(Args a) {
+  const int b = blockIdx.y;
+  St* st = state(a, b);
+  if (st->done || !st->have_prev) return;
+  const float* w = slot(a, b);
+  float s[1] = {0.f};
+  FOR_ELEMS(a.L.plane) {
+    const float d = w[a.L.oS + idx] - w[a.L.oMp + idx];
+    s[0] = fmaf(d, d, s[0]);
+  }
+  block_add<1>(s, st->wacc);
+}
+
+// gate: warm iff ||M_k - M_{k-1}||_F < eps_svd (replay bit 2 overrides, reading Z21's protocol)
+__global__ void k_ws_gate(Args a, int k) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= a.B) return;
+  St* st = state(a, b);
+  st->warm = 0;
+  if (st->done || !st->have_prev) return;
+  bool w = sqrt(st->wacc[0]) < (double)st->eps_svd;
+  if (a.P.rho_replay) w = (a.P.rho_replay[(size_t)b * a.P.max_inner + k] & 4) != 0;
+  for (int e = 0; e < 8; ++e) st->wacc[e] = 0.0;
+  st->eps = 1.f / st->mu;
+  if (w) {
+    st->warm = 1;
+    atomicAdd(a.counter + 1, 1);
+  }
+}
+
+// P_Sigma_j = Sigma_j - u_j . (M V)_j (one warp per column; M V in H2)
+__global__ void __launch_bounds__(256) k_ws_psig(Args a) {
+  const int b = blockIdx.y;
+  St* st = state(a, b);
+  if (st->done || !st->warm) return;
+  const int j = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (j >= a.L.n) return;
+  float* w = slot(a, b);
+  const float* u = w + a.L.oU + (size_t)j * a.L.ldm;
+  const float* mv = w + a.L.oH2 + (size_t)j * a.L.ldm;
+  float s = 0.f;
+  for (int i = lane; i < a.L.m; i += 32) s = fmaf(u[i], mv[i], s);
+  s = warp_sum(s);
+  if (lane == 0) w[a.L.oPs + j] = w[a.L.oSg + j] - s;
+}
+
+// Z <- H1 + Z (Z holds U P_Sigma V^T)
+__global__ void __launch_bounds__(ENT) k_ws_z(Args a) {
+  const int b = blockIdx.y;
+  St* st = state(a, b);
+  if (st->done || !st->warm) return;
+  float* w = slot(a, b);
+  FOR_ELEMS(a.L.plane) w[a.L.oZ + idx] += w[a.L.oH1 + idx];
+}
+
+// <h0, h1>, ||h1||^2, <h0, h2> with h0 = M - W
+__global__ void __launch_bounds__(ENT) k_ws_red(Args a) {
+  const int b = blockIdx.y;
+  St* st = state(a, b);
+  if (st->done || !st->warm) return;
+  const float* w = slot(a, b);
+  float s[3] = {0.f, 0.f, 0.f};
+  FOR_ELEMS(a.L.plane) {
+    const float h0 = w[a.L.oS + idx] - w[a.L.oW + idx];
+    const float h1 = w[a.L.oH1 + idx], h2 = w[a.L.oH2 + idx];
+    s[0] = fmaf(h0, h1, s[0]);
+    s[1] = fmaf(h1, h1, s[1]);
+    s[2] = fmaf(h0, h2, s[2]);
+  }
+  block_add<3>(s, st->wacc + 1);
+}
+
+// ||X||_F^2 of an nn x nn block (ld) -> wacc[slot]
+__global__ void __launch_bounds__(ENT) k_ws_norm(Args a, size_t off, int nn, int ld, int slotk) {
+  const int b = blockIdx.y;
+  St* st = state(a, b);
+  if (st->done || !st->warm) return;
+  const float* X = slot(a, b) + off;
+  float s[1] = {0.f};
+  FOR_ELEMS((size_t)nn * nn) {
+    const float x = X[(idx / nn) * ld + idx % nn];
+    s[0] = fmaf(x, x, s[0]);
+  }
+  block_add<1>(s, st->wacc + slotk);
+}
+
+// t* = -f'(0)/f''(0) (Eq. ft; 0 when f''(0) <= 0), the Z27 acceptance test and the Richardson count
+__global__ void k_ws_t(Args a) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= a.B) return;
+  St* st = state(a, b);
+  if (st->done || !st->warm) return;
+  const double f1 = st->wacc[1], f2 = st->wacc[2] + st->wacc[3];
+  const double t = f2 > 0.0 ? -f1 / f2 : 0.0;
+  const double r = 0.5 * fabs(t) * fmax(sqrt(st->wacc[4]), sqrt(st->wacc[5]));
+  st->t_star = (float)t;
+  if (!(r < 0.5)) {  // rejected: full SVD (Z27)
+    st->warm = 0;
+    return;
+  }
+  int K = 1;
+  if (r > 1e-30) K = (int)ceil(log(1e-8) / log(r));
+  K = K < 1 ? 1 : (K > 40 ? 40 : K);
+  st->cay_k = K;
+  atomicAdd(a.counter + 1, 1);
+  atomicMax(a.counter + 2, K);
+}
+
+// Sigma <- Sigma - t P_Sigma; |Sigma| for the statistics; count the warm step
+__global__ void k_ws_sigma(Args a) {
+  const int b = blockIdx.y;
+  St* st = state(a, b);
+  if (st->done || !st->warm) return;
+  float* w = slot(a, b);
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < a.L.n) {
+    const float sg = w[a.L.oSg + j] - st->t_star * w[a.L.oPs + j];
+    w[a.L.oSg + j] = sg;
+    w[a.L.oSig + j] = fabsf(sg);
+  }
+  if (j == 0) st->warm_steps += 1;
+}
+
+// state of a full SVD (Jacobi problems): U_j = b_j / ||b_j||, Sigma_j = sigma_j (before the scale)
+__global__ void __launch_bounds__(256) k_ws_state(Args a) {
+  const int b = blockIdx.y;
+  St* st = state(a, b);
+  if (st->done || st->warm) return;
+  const int j = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (j >= a.L.n) return;
+  float* w = slot(a, b);
+  const float* bj = w + a.L.oB + (size_t)j * a.L.ldm;
+  float* uj = w + a.L.oU + (size_t)j * a.L.ldm;
+  float s = 0.f;
+  for (int i = lane; i < a.L.m; i += 32) s = fmaf(bj[i], bj[i], s);
+  s = warp_sum(s);
+  const float inv = s > 0.f ? rsqrtf(s) : 0.f;
+  for (int i = lane; i < a.L.m; i += 32) uj[i] = bj[i] * inv;
+  if (lane == 0) w[a.L.oSg + j] = w[a.L.oSig + j];
+}
+
+// after the SVT: M_prev <- M for the next gate
+__global__ void __launch_bounds__(ENT) k_ws_after(Args a) {
+  const int b = blockIdx.y;
+  St* st = state(a, b);
+  if (st->done) return;
+  float* w = slot(a, b);
+  FOR_ELEMS(a.L.plane) w[a.L.oMp + idx] = w[a.L.oS + idx];
+  if (blockIdx.x == 0 && threadIdx.x == 0) st->have_prev = 1;
+}
+
+__global__ void k_ws_init(Args a, float gate) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= a.B) return;
+  St* st = state(a, b);
+  // eps_svd = gate ||D||_F (the oracle's SvdWarm takes the absolute threshold)
+  st->eps_svd = gate * (float)sqrt(st->acc[ACC_R + 2]);
+}
+
+__global__ void __launch_bounds__(ENT) k_dnorm(Args a) {
+  const int b = blockIdx.y;
+  St* st = state(a, b);
+  const float* D = slot(a, b) + a.L.oD;
+  float s[1] = {0.f};
+  FOR_ELEMS(a.L.plane) s[0] = fmaf(D[idx], D[idx], s[0]);
+  block_add<1>(s, st->acc + ACC_R + 2);
+}
+
+// ---------------------------------------------------------------------------------------------
 // Host side
 // ---------------------------------------------------------------------------------------------
 struct Run {
@@ -907,6 +1161,7 @@ struct Run {
   cublasHandle_t cb;
   tilt_status st = TILT_OK;
   int rpl = 32;
+  bool svdws = false;  // LADMAP+SVDWS (DevParams::svd_mode 1)
 
   explicit Run(Ctx& c) : ctx(c), cb((cublasHandle_t)c.cublas) {}
 
@@ -935,7 +1190,16 @@ struct Run {
     if (fail_cuda(cudaStreamSynchronize(ctx.stream), "cudaStreamSynchronize")) return -1;
     return *ctx.h_counter;
   }
-  bool zero_counter() { return fail_cuda(cudaMemsetAsync(ctx.counter, 0, sizeof(int), ctx.stream), "memset"); }
+  bool zero_counter() { return fail_cuda(cudaMemsetAsync(ctx.counter, 0, 4 * sizeof(int), ctx.stream), "memset"); }
+  // counters [0..3) after a stream sync (false on error)
+  bool read_counters(int* out) {
+    if (fail_cuda(cudaMemcpyAsync(ctx.h_counter, ctx.counter, 3 * sizeof(int), cudaMemcpyDeviceToHost, ctx.stream),
+                  "cudaMemcpyAsync(counters)"))
+      return false;
+    if (fail_cuda(cudaStreamSynchronize(ctx.stream), "cudaStreamSynchronize")) return false;
+    for (int i = 0; i < 3; ++i) out[i] = ctx.h_counter[i];
+    return true;
+  }
 
   // C = op(X) op(Y) with per-problem strides (column-major; cuBLAS FP32, default math: no TF32)
   bool gemm(cublasOperation_t ta, cublasOperation_t tb, int M, int N, int K, size_t oX, int ldx, size_t oY,
@@ -989,7 +1253,7 @@ struct Run {
   }
 
   // one SVT of S (eps per eps_mode) with the V in a.oV; leaves B scaled, sigma/stats in the state
-  bool svt_core(const float* eps, int eps_mode, int count_sweeps, bool do_scale) {
+  bool svt_core(const float* eps, int eps_mode, int count_sweeps, bool do_scale, bool ws_state = false) {
     if (zero_counter()) return true;
     k_svt_begin<<<sgrid(), 128, 0, ctx.stream>>>(a, eps, eps_mode);
     launched();
@@ -1001,11 +1265,91 @@ struct Run {
     k_svt_sig<<<dim3((L.n + 7) / 8, a.B), 256, 0, ctx.stream>>>(a);
     k_svt_stats<<<a.B, 32, 0, ctx.stream>>>(a, count_sweeps);
     launched(2);
+    if (ws_state) {  // U = B / ||b||, Sigma = sigma for the next warm step (before B is scaled)
+      k_ws_state<<<dim3((L.n + 7) / 8, a.B), 256, 0, ctx.stream>>>(a);
+      launched();
+    }
     if (do_scale) {
       k_svt_scale<<<egrid(L.plane), ENT, 0, ctx.stream>>>(a);
       launched();
     }
     return check("svt");
+  }
+
+  // Alg. 2, first half (problems with st->warm): W, P_U, P_V, P_Sigma, h1, h2, t*
+  bool ws_part1() {
+    const Lay& L = a.L;
+    const int m = L.m, n = L.n, ldm = L.ldm, ldn = L.ldn;
+    const dim3 ep = egrid(L.plane);
+    k_colscale<<<ep, ENT, 0, ctx.stream>>>(a, L.oX, L.oU, L.oSg, 0, 1);
+    launched();
+    if (gemm(CUBLAS_OP_N, CUBLAS_OP_T, m, n, n, L.oX, ldm, a.oV, ldn, L.oW, ldm)) return true;      // W
+    if (gemm(CUBLAS_OP_N, CUBLAS_OP_T, m, m, n, L.oW, ldm, L.oS, ldm, L.oPU, ldm)) return true;     // W M^T
+    k_skew<<<egrid((size_t)m * m), ENT, 0, ctx.stream>>>(a, L.oPU, m, ldm, 0);                     // P_U
+    if (gemm(CUBLAS_OP_T, CUBLAS_OP_N, n, n, m, L.oW, ldm, L.oS, ldm, L.oPV, ldn)) return true;     // W^T M
+    k_skew<<<egrid((size_t)n * n), ENT, 0, ctx.stream>>>(a, L.oPV, n, ldn, 0);                     // P_V
+    launched(2);
+    if (gemm(CUBLAS_OP_N, CUBLAS_OP_N, m, n, n, L.oS, ldm, a.oV, ldn, L.oH2, ldm)) return true;     // M V
+    k_ws_psig<<<dim3((n + 7) / 8, a.B), 256, 0, ctx.stream>>>(a);                                  // P_Sigma
+    k_colscale<<<ep, ENT, 0, ctx.stream>>>(a, L.oX2, L.oU, L.oPs, 0, 1);
+    launched(2);
+    if (gemm(CUBLAS_OP_N, CUBLAS_OP_T, m, n, n, L.oX2, ldm, a.oV, ldn, L.oZ, ldm)) return true;    // U P_S V^T
+    k_copy_if<<<ep, ENT, 0, ctx.stream>>>(a, L.oH1, L.oZ, L.plane, 1);
+    launched();
+    if (gemm(CUBLAS_OP_N, CUBLAS_OP_N, m, n, m, L.oPU, ldm, L.oW, ldm, L.oH1, ldm, 1.f, 1.f)) return true;
+    if (gemm(CUBLAS_OP_N, CUBLAS_OP_N, m, n, n, L.oW, ldm, L.oPV, ldn, L.oH1, ldm, -1.f, 1.f)) return true;
+    k_ws_z<<<ep, ENT, 0, ctx.stream>>>(a);                                                          // Z
+    launched();
+    if (gemm(CUBLAS_OP_N, CUBLAS_OP_N, m, n, m, L.oPU, ldm, L.oZ, ldm, L.oH2, ldm, -1.f, 0.f)) return true;
+    if (gemm(CUBLAS_OP_N, CUBLAS_OP_N, m, n, n, L.oZ, ldm, L.oPV, ldn, L.oH2, ldm, 1.f, 1.f)) return true;
+    k_ws_red<<<ep, ENT, 0, ctx.stream>>>(a);
+    k_ws_norm<<<egrid((size_t)m * m), ENT, 0, ctx.stream>>>(a, L.oPU, m, ldm, 4);
+    k_ws_norm<<<egrid((size_t)n * n), ENT, 0, ctx.stream>>>(a, L.oPV, n, ldn, 5);
+    launched(3);
+    if (zero_counter()) return true;
+    k_ws_t<<<sgrid(), 128, 0, ctx.stream>>>(a);
+    launched();
+    return check("svd warm step (1)");
+  }
+
+  // Cayley update X <- (I + S)^{-1} (I - S) X0 for S = (t/2) P (already scaled) by Richardson
+  // iteration: R = X0 - S X0, X_{k+1} = R - S X_k (K iterations); the result lands in `dst`
+  bool cayley(size_t oP, int ldp, size_t oX0, size_t oR, size_t oA1, size_t oA2, int rows, int cols, int ldx,
+              size_t count, int K, size_t dst) {
+    const dim3 eg = egrid(count);
+    k_copy_if<<<eg, ENT, 0, ctx.stream>>>(a, oR, oX0, count, 1);
+    launched();
+    if (gemm(CUBLAS_OP_N, CUBLAS_OP_N, rows, cols, rows, oP, ldp, oX0, ldx, oR, ldx, -1.f, 1.f)) return true;
+    k_copy_if<<<eg, ENT, 0, ctx.stream>>>(a, oA1, oR, count, 1);
+    launched();
+    size_t cur = oA1, nxt = oA2;
+    for (int it = 0; it < K; ++it) {
+      k_copy_if<<<eg, ENT, 0, ctx.stream>>>(a, nxt, oR, count, 1);
+      launched();
+      if (gemm(CUBLAS_OP_N, CUBLAS_OP_N, rows, cols, rows, oP, ldp, cur, ldx, nxt, ldx, -1.f, 1.f)) return true;
+      const size_t t = cur;
+      cur = nxt;
+      nxt = t;
+    }
+    k_copy_if<<<eg, ENT, 0, ctx.stream>>>(a, dst, cur, count, 1);
+    launched();
+    return check("cayley");
+  }
+
+  // Alg. 2, second half: U(t), V(t), Sigma(t); B <- U T_eps(Sigma) so that A = B V^T for every problem
+  bool ws_part2(int K) {
+    const Lay& L = a.L;
+    const int m = L.m, n = L.n, ldm = L.ldm, ldn = L.ldn;
+    k_skew<<<egrid((size_t)m * m), ENT, 0, ctx.stream>>>(a, L.oPU, m, ldm, 1);  // (t/2) P_U
+    k_skew<<<egrid((size_t)n * n), ENT, 0, ctx.stream>>>(a, L.oPV, n, ldn, 1);  // (t/2) P_V
+    launched(2);
+    if (cayley(L.oPU, ldm, L.oU, L.oX, L.oX2, L.oH2, m, n, ldm, L.plane, K, L.oU)) return true;
+    if (cayley(L.oPV, ldn, a.oV, L.oVt, L.oVt2, L.oT, n, n, ldn, L.vplane, K, a.oV)) return true;
+    k_ws_sigma<<<dim3((n + 127) / 128, a.B), 128, 0, ctx.stream>>>(a);
+    k_svt_stats<<<a.B, 32, 0, ctx.stream>>>(a, 0, 1);
+    k_colscale<<<egrid(L.plane), ENT, 0, ctx.stream>>>(a, L.oB, L.oU, L.oSg, 1, 1);
+    launched(3);
+    return check("svd warm step (2)");
   }
 
   bool ns_step() {
@@ -1021,7 +1365,8 @@ struct Run {
 
   void setup(int B, int m, int n, int p, const DevParams& P) {
     a.ws = ctx.ws;
-    a.L = make_lay(m, n, p);
+    svdws = P.svd_mode == 1;
+    a.L = make_lay(m, n, p, svdws);
     a.B = B;
     a.P = P;
     a.oV = a.L.oV;
@@ -1037,7 +1382,7 @@ struct Run {
 
 }  // namespace
 
-size_t ws_need(int B, int m, int n, int p) { return (size_t)B * make_lay(m, n, p).stride; }
+size_t ws_need(int B, int m, int n, int p, bool svdws) { return (size_t)B * make_lay(m, n, p, svdws).stride; }
 
 tilt_status ensure(Ctx& ctx, size_t floats) {
   if (!ctx.counter) {
@@ -1077,7 +1422,7 @@ void release(Ctx& ctx) {
 
 tilt_status inner(Ctx& ctx, const float* D, const float* J, const float* Q, int l, int B, int m, int n, int p,
                   const DevParams& P, float* A, float* E, float* Y, tilt_report* rep) {
-  tilt_status s0 = ensure(ctx, ws_need(B, m, n, p));
+  tilt_status s0 = ensure(ctx, ws_need(B, m, n, p, P.svd_mode == 1));
   if (s0 != TILT_OK) return s0;
   Run R(ctx);
   R.setup(B, m, n, p, P);
@@ -1102,6 +1447,11 @@ tilt_status inner(Ctx& ctx, const float* D, const float* J, const float* Q, int 
   k_identity<<<R.egrid(L.vplane), ENT, 0, sm>>>(a, L.oV);
   k_kt<0><<<R.egrid(L.plane), ENT, 0, sm>>>(a);
   k_denom<<<R.egrid(L.plane), ENT, 0, sm>>>(a);
+  if (R.svdws) {
+    k_dnorm<<<R.egrid(L.plane), ENT, 0, sm>>>(a);
+    k_ws_init<<<R.sgrid(), 128, 0, sm>>>(a, P.svd_ws_gate);
+    R.launched(2);
+  }
   k_sc_denom<<<R.sgrid(), 128, 0, sm>>>(a);
   R.launched(5);
   if (R.check("inner setup")) return R.st;
@@ -1119,10 +1469,30 @@ tilt_status inner(Ctx& ctx, const float* D, const float* J, const float* Q, int 
       k_identity<<<R.egrid(L.vplane), ENT, 0, sm>>>(a, a.oV);
       R.launched();
     }
-    if (R.svt_core(nullptr, 0, 1, true)) return R.st;
+    int nwarm = 0, K = 0;
+    if (R.svdws && k > 0) {  // Alg. 2 gate, then the warm step's first half for the gated problems
+      if (R.zero_counter()) return R.st;
+      k_ws_diff<<<R.egrid(L.plane), ENT, 0, sm>>>(a);
+      k_ws_gate<<<R.sgrid(), 128, 0, sm>>>(a, k);
+      R.launched(2);
+      int c[3];
+      if (!R.read_counters(c)) return R.st;
+      if (c[1] > 0) {
+        if (R.ws_part1()) return R.st;
+        if (!R.read_counters(c)) return R.st;
+        nwarm = c[1];
+        K = c[2];
+      }
+    }
+    if (R.svt_core(nullptr, 0, 1, true, R.svdws)) return R.st;
+    if (nwarm > 0 && R.ws_part2(K)) return R.st;
     if (R.gemm(CUBLAS_OP_N, CUBLAS_OP_T, m, n, n, L.oB, L.ldm, a.oV, L.ldn, L.oAn, L.ldm)) return R.st;
     if (warm && (k % P.ns_period == P.ns_period - 1 || k + 1 == a.niter))
       if (R.ns_step()) return R.st;
+    if (R.svdws) {
+      k_ws_after<<<R.egrid(L.plane), ENT, 0, sm>>>(a);
+      R.launched();
+    }
     k_kt<2><<<R.egrid(L.plane), ENT, 0, sm>>>(a);
     k_estep<<<R.egrid(L.plane), ENT, 0, sm>>>(a);
     k_sc1<<<R.sgrid(), 128, 0, sm>>>(a, k);
@@ -1167,7 +1537,7 @@ __global__ void k_svt_clear(Args a) {
 
 tilt_status svt(Ctx& ctx, const float* M, int B, int m, int n, const float* eps, float* V_io, float* A,
                 float* sigma, int32_t* sweeps, float tol, int max_sweeps) {
-  tilt_status s0 = ensure(ctx, ws_need(B, m, n, 1));
+  tilt_status s0 = ensure(ctx, ws_need(B, m, n, 1, false));
   if (s0 != TILT_OK) return s0;
   Run R(ctx);
   DevParams P;

@@ -30,7 +30,7 @@ struct Ctx {
 };
 
 // workspace floats of B problems of size m x n with p Jacobian planes
-size_t ws_need(int B, int m, int n, int p);
+size_t ws_need(int B, int m, int n, int p, bool svdws = false);
 // (re)allocate ctx.ws for at least `floats` floats and create the cuBLAS handle
 tilt_status ensure(Ctx& ctx, size_t floats);
 void release(Ctx& ctx);

@@ -1281,6 +1281,7 @@ __device__ void solve_patch_rj(const SolveArgs& a, const W<NC>& w, int b) {
       r.mu_last = mu_last;
       r.jacobi_rotations = rot_total;
       r.kernel_path = 2;
+      r.svd_warm_steps = 0;
       if (a.rep_prev) {
         const tilt_report& pr = a.rep_prev[b];
         r.outer_iters += pr.outer_iters;

@@ -25,9 +25,24 @@ def test_header_symbols_exported(pkg):
         assert hasattr(pkg.lib, name), name
 
 
+def _header_fields(struct_name):
+    hdr = open(os.path.join(ROOT, "include", "tilt.h")).read()
+    hdr = re.sub(r"/\*.*?\*/", "", hdr, flags=re.S)
+    body = re.search(r"typedef struct \{([^}]*)\}\s*" + struct_name + ";", hdr).group(1)
+    names = []
+    for decl in body.split(";"):
+        decl = decl.strip()
+        if decl:  # "type name" or "type a, b": the identifiers that end each comma-separated piece
+            names += [re.search(r"(\w+)\s*$", piece).group(1) for piece in decl.split(",")]
+    return names
+
+
 def test_struct_sizes_match_header(pkg):
     from paper_1205_5351_b200 import _abi
-    assert ctypes.sizeof(_abi.TiltReport) == 18 * 4
+    assert [f[0] for f in _abi.TiltReport._fields_] == _header_fields("tilt_report")
+    assert ctypes.sizeof(_abi.TiltReport) == 4 * len(_header_fields("tilt_report"))
+    # (the Python field for the C member `lambda` is `lambda_`: a Python keyword)
+    assert [f[0].rstrip("_") for f in _abi.TiltParams._fields_] == _header_fields("tilt_params")
     assert pkg.lib.tilt_abi_version() == 1
 
 

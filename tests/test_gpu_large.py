@@ -146,3 +146,54 @@ def test_inner_free_running_table1_1000(solver, T):
     assert np.mean(rep["objective"]) == pytest.approx(6844.14, rel=0.02)
     assert 12 <= np.mean(rep["inner_iters"]) <= 40
     assert np.all(rep["sweep_cap_hits"] == 0)
+
+
+# ---------------------------------------------------------------------------------------------
+# LADMAP+SVDWS (Algorithm 2; readings Z27) on the multi-CTA path
+# ---------------------------------------------------------------------------------------------
+def _svdws_ref(D, J, lam, K, gate):
+    proj = O.Projector(J, None)
+    mu0 = 1.25 / np.linalg.svd(D, compute_uv=False)[0]
+    z = np.zeros_like(D)
+    sw = O.SvdWarm(gate * np.linalg.norm(D))
+    r = O.ladmap(D, proj, lam, mu0, 1e6 * mu0, 2.0, 1e-6, 0.1, max(K, 1000), D.copy(), z, z, fixed_iters=K, svd=sw)
+    return r, sw
+
+
+@pytest.mark.parametrize("n,gate", [(100, 1e-4), (300, 1e-4), (200, 1e-3)])
+def test_svdws_fixed_count_parity(solver, T, n, gate):
+    """A fixed count of LADMAP+SVDWS iterations with the oracle's rho decisions and warm/full
+    decisions replayed (bits 0 and 2): both compute the same Cayley-curve step (Appendix A) from the
+    same previous SVD, so A and E agree to the fixed-count bar (1e-4)."""
+    K, B = 20, 2
+    insts = [ts.table1_instance(n, 6, s) for s in range(B)]
+    D = np.stack([i["D"] for i in insts]).astype(np.float32)
+    J = np.stack([i["J"] for i in insts]).astype(np.float32)
+    lam = insts[0]["lam"]
+    refs = [_svdws_ref(D[k].astype(np.float64), J[k].astype(np.float64), lam, K, gate) for k in range(B)]
+    bits = np.array([[t[3] | (dcs << 2) for t, dcs in zip(r.trace, sw.decisions)] for r, sw in refs], np.uint8)
+    assert sum(sw.warm_steps for _, sw in refs) > 0
+    prm = T.default_params(fixed_inner_iters=K, max_inner=K, kernel_path=3, svd_mode=1, svd_ws_gate=gate)
+    out = solver.inner(D, J, params=prm, rho_replay=bits)
+    rep = out["rep"]
+    for k, (r, sw) in enumerate(refs):
+        assert rep["svd_warm_steps"][k] == sw.warm_steps
+        a = out["A"][k].double().cpu().numpy()
+        e = out["E"][k].double().cpu().numpy()
+        ra = np.linalg.norm(a - r.A) / np.linalg.norm(r.A)
+        re = np.linalg.norm(e - r.E) / max(np.linalg.norm(r.E), 1e-30)
+        assert ra < 1e-4 and re < 1e-4, (n, gate, k, ra, re, sw.decisions)
+
+
+def test_svdws_free_running_keeps_ladmap_objective(solver, T):
+    """Table 1's third column: LADMAP+SVDWS stops at nearly LADMAP's objective (the paper:
+    1123.70 vs 1123.67 at 300x300) after taking warm steps."""
+    B = 3
+    insts = [ts.table1_instance(300, 6, s) for s in range(B)]
+    D = np.stack([i["D"] for i in insts]).astype(np.float32)
+    J = np.stack([i["J"] for i in insts]).astype(np.float32)
+    r0 = solver.inner(D, J, params=T.default_params(kernel_path=3))["rep"]
+    r1 = solver.inner(D, J, params=T.default_params(kernel_path=3, svd_mode=1, svd_ws_gate=1e-4))["rep"]
+    assert np.all(r1["status"] == T.CONVERGED)
+    assert np.sum(r1["svd_warm_steps"]) > 0
+    np.testing.assert_allclose(r1["objective"], r0["objective"], rtol=1e-3)
