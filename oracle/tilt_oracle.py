@@ -401,9 +401,9 @@ class SvdWarm:
     """The SVD warm start of LADMAP+SVDWS (Algorithm 2): keeps the previous (approximate) SVD and
     M_{k-1}; S_eps(M_k) uses one ``svd_warm_start`` step when ||M_k - M_{k-1}||_F < eps_svd, else a
     full SVD ("Else do full svd"). m < n is handled on the transpose (S_eps(M^T) = S_eps(M)^T).
-    Reading Z27: a step whose Cayley generators are not small, ||(t*/2) P_U||_F >= 0.5 or
-    ||(t*/2) P_V||_F >= 0.5, is rejected (full SVD instead) -- the GPU solves the Cayley systems by
-    Richardson iteration, which needs them below 1. ``decisions`` logs 1 (warm step) / 0 (full SVD)
+    Reading Z27: a step without a descent model (f''(0) <= 0, t* = 0) or whose Cayley generators are
+    not small, ||(t*/2) P_U||_F >= 0.5 or ||(t*/2) P_V||_F >= 0.5, is rejected (full SVD instead) --
+    the GPU solves the Cayley systems by Richardson iteration, which needs them below 1. ``decisions`` logs 1 (warm step) / 0 (full SVD)
     per call."""
 
     CAYLEY_MAX = 0.5
@@ -426,7 +426,7 @@ class SvdWarm:
             w = (self.prev[0] * self.prev[1]) @ self.prev[2].T
             p_u = w @ x.T - x @ w.T
             p_v = w.T @ x - x.T @ w
-            if max(np.linalg.norm(0.5 * t * p_u), np.linalg.norm(0.5 * t * p_v)) < self.CAYLEY_MAX:
+            if t != 0.0 and max(np.linalg.norm(0.5 * t * p_u), np.linalg.norm(0.5 * t * p_v)) < self.CAYLEY_MAX:
                 step = (u, sig, v)
         if step is not None:
             u, sig, v = step

@@ -1080,7 +1080,7 @@ __global__ void k_ws_t(Args a) {
   const double t = f2 > 0.0 ? -f1 / f2 : 0.0;
   const double r = 0.5 * fabs(t) * fmax(sqrt(st->wacc[4]), sqrt(st->wacc[5]));
   st->t_star = (float)t;
-  if (!(r < 0.5)) {  // rejected: full SVD (Z27)
+  if (!(f2 > 0.0) || !(r < 0.5)) {  // rejected: full SVD (Z27)
     st->warm = 0;
     return;
   }

@@ -91,3 +91,19 @@ def test_ladmap_svdws_tight_gate_keeps_ladmap_iterations():
     assert warm > 0
     assert abs(np.mean(its_w) - np.mean(its)) <= 3
     assert max(rel) < 1e-4
+
+
+def test_svdws_rejects_large_cayley_steps():
+    """Reading Z27: with an open gate, a step whose generators (t*/2)P are not small is rejected and a
+    full SVD is taken (the result is then the exact S_eps); a small perturbation is accepted."""
+    rng = np.random.default_rng(5)
+    m0 = rng.normal(size=(12, 10))
+    sw = O.SvdWarm(1e9)  # the gate never closes
+    sw.svt(m0, 0.1)                                   # first call: full SVD
+    far = rng.normal(size=(12, 10))                   # unrelated matrix: a large Cayley step
+    a_far, _ = sw.svt(far, 0.1)
+    near = far + 1e-6 * rng.normal(size=(12, 10))     # tiny change: accepted
+    sw.svt(near, 0.1)
+    assert sw.decisions == [0, 0, 1]
+    ref, _ = O.svt(far, 0.1)
+    np.testing.assert_allclose(a_far, ref, atol=1e-12)
