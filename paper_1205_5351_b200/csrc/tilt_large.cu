@@ -1152,6 +1152,24 @@ __global__ void __launch_bounds__(ENT) k_dnorm(Args a) {
   block_add<1>(s, st->acc + ACC_R + 2);
 }
 
+// pointer arrays of a subset GEMM: ptrs[k * nsub + w] = slot(widx[w]) + off_k
+__global__ void k_ptrs(float* ws, size_t stride, const int* __restrict__ widx, int nsub, size_t o0, size_t o1, size_t o2,
+                       void** ptrs) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= 3 * nsub) return;
+  const int k = e / nsub, w = e % nsub;
+  const size_t off = k == 0 ? o0 : (k == 1 ? o1 : o2);
+  ptrs[e] = ws + (size_t)widx[w] * stride + off;
+}
+
+// the problems taking the Alg. 2 step (order irrelevant: every problem's GEMMs are independent)
+__global__ void k_ws_index(Args a, int* widx) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= a.B) return;
+  const St* st = state(a, b);
+  if (!st->done && st->warm) widx[atomicAdd(a.counter + 3, 1)] = b;
+}
+
 // ---------------------------------------------------------------------------------------------
 // Host side
 // ---------------------------------------------------------------------------------------------
@@ -1202,8 +1220,19 @@ struct Run {
   }
 
   // C = op(X) op(Y) with per-problem strides (column-major; cuBLAS FP32, default math: no TF32)
+  int nsub = 0;  // > 0: GEMMs run on the nsub problems listed in ctx.widx only (pointer-array batch)
+
   bool gemm(cublasOperation_t ta, cublasOperation_t tb, int M, int N, int K, size_t oX, int ldx, size_t oY,
             int ldy, size_t oC, int ldc, float alpha = 1.f, float beta = 0.f) {
+    if (nsub > 0) {
+      k_ptrs<<<(3 * nsub + 127) / 128, 128, 0, ctx.stream>>>(a.ws, a.L.stride, ctx.widx, nsub, oX, oY, oC, ctx.ptrs);
+      const bool bad = cub(cublasSgemmBatched(cb, ta, tb, M, N, K, &alpha, (const float**)ctx.ptrs, ldx,
+                                              (const float**)(ctx.ptrs + nsub), ldy, &beta, (float**)(ctx.ptrs + 2 * nsub),
+                                              ldc, nsub),
+                           "cublasSgemmBatched");
+      launched(2);
+      return bad;
+    }
     const long long s = (long long)a.L.stride;
     const bool bad = cub(cublasSgemmStridedBatched(cb, ta, tb, M, N, K, &alpha, a.ws + oX, ldx, s, a.ws + oY, ldy, s,
                                                    &beta, a.ws + oC, ldc, s, a.B),
@@ -1274,6 +1303,15 @@ struct Run {
       launched();
     }
     return check("svt");
+  }
+
+  // list the problems with st->warm in ctx.widx; the following GEMMs run on them only
+  bool ws_subset(int count) {
+    if (zero_counter()) return true;
+    k_ws_index<<<sgrid(), 128, 0, ctx.stream>>>(a, ctx.widx);
+    launched();
+    nsub = count;
+    return check("subset index");
   }
 
   // Alg. 2, first half (problems with st->warm): W, P_U, P_V, P_Sigma, h1, h2, t*
@@ -1384,10 +1422,20 @@ struct Run {
 
 size_t ws_need(int B, int m, int n, int p, bool svdws) { return (size_t)B * make_lay(m, n, p, svdws).stride; }
 
-tilt_status ensure(Ctx& ctx, size_t floats) {
+tilt_status ensure(Ctx& ctx, size_t floats, int B) {
   if (!ctx.counter) {
     if (cudaMalloc(&ctx.counter, 64 * sizeof(int)) != cudaSuccess) return TILT_E_OOM;
     if (cudaMallocHost(&ctx.h_counter, 64 * sizeof(int)) != cudaSuccess) return TILT_E_OOM;
+  }
+  if (ctx.cap_b < B) {
+    if (ctx.widx) cudaFree(ctx.widx);
+    if (ctx.ptrs) cudaFree(ctx.ptrs);
+    ctx.widx = nullptr;
+    ctx.ptrs = nullptr;
+    ctx.cap_b = 0;
+    if (cudaMalloc(&ctx.widx, (size_t)B * sizeof(int)) != cudaSuccess) return TILT_E_OOM;
+    if (cudaMalloc(&ctx.ptrs, (size_t)3 * B * sizeof(void*)) != cudaSuccess) return TILT_E_OOM;
+    ctx.cap_b = B;
   }
   if (!ctx.cublas) {
     cublasHandle_t h;
@@ -1414,6 +1462,8 @@ tilt_status ensure(Ctx& ctx, size_t floats) {
 
 void release(Ctx& ctx) {
   if (ctx.ws) cudaFree(ctx.ws);
+  if (ctx.widx) cudaFree(ctx.widx);
+  if (ctx.ptrs) cudaFree(ctx.ptrs);
   if (ctx.counter) cudaFree(ctx.counter);
   if (ctx.h_counter) cudaFreeHost(ctx.h_counter);
   if (ctx.cublas) cublasDestroy((cublasHandle_t)ctx.cublas);
@@ -1422,7 +1472,7 @@ void release(Ctx& ctx) {
 
 tilt_status inner(Ctx& ctx, const float* D, const float* J, const float* Q, int l, int B, int m, int n, int p,
                   const DevParams& P, float* A, float* E, float* Y, tilt_report* rep) {
-  tilt_status s0 = ensure(ctx, ws_need(B, m, n, p, P.svd_mode == 1));
+  tilt_status s0 = ensure(ctx, ws_need(B, m, n, p, P.svd_mode == 1), B);
   if (s0 != TILT_OK) return s0;
   Run R(ctx);
   R.setup(B, m, n, p, P);
@@ -1478,14 +1528,20 @@ tilt_status inner(Ctx& ctx, const float* D, const float* J, const float* Q, int 
       int c[3];
       if (!R.read_counters(c)) return R.st;
       if (c[1] > 0) {
+        if (R.ws_subset(c[1])) return R.st;
         if (R.ws_part1()) return R.st;
+        R.nsub = 0;
         if (!R.read_counters(c)) return R.st;
         nwarm = c[1];
         K = c[2];
       }
     }
     if (R.svt_core(nullptr, 0, 1, true, R.svdws)) return R.st;
-    if (nwarm > 0 && R.ws_part2(K)) return R.st;
+    if (nwarm > 0) {
+      if (R.ws_subset(nwarm)) return R.st;
+      if (R.ws_part2(K)) return R.st;
+      R.nsub = 0;
+    }
     if (R.gemm(CUBLAS_OP_N, CUBLAS_OP_T, m, n, n, L.oB, L.ldm, a.oV, L.ldn, L.oAn, L.ldm)) return R.st;
     if (warm && (k % P.ns_period == P.ns_period - 1 || k + 1 == a.niter))
       if (R.ns_step()) return R.st;
@@ -1537,7 +1593,7 @@ __global__ void k_svt_clear(Args a) {
 
 tilt_status svt(Ctx& ctx, const float* M, int B, int m, int n, const float* eps, float* V_io, float* A,
                 float* sigma, int32_t* sweeps, float tol, int max_sweeps) {
-  tilt_status s0 = ensure(ctx, ws_need(B, m, n, 1, false));
+  tilt_status s0 = ensure(ctx, ws_need(B, m, n, 1, false), B);
   if (s0 != TILT_OK) return s0;
   Run R(ctx);
   DevParams P;
