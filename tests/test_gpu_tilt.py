@@ -140,12 +140,29 @@ def test_convergence_parity(solver, T, cfg_id, path):
     assert not bad, bad
 
 
+def _unstable(cfg, idx, r, rel=1e-7):
+    """Reading Z22: the fp64 oracle's own tau moves by > 1e-3 when its input is perturbed by 1e-7
+    relative (same outer count): a basin-edge patch, excluded from tau parity and counted."""
+    b = ts.gen_batch(cfg, idx, 1)
+    rng = np.random.default_rng([22, idx])
+    img = b["images"][0] * (1.0 + rel * rng.standard_normal(b["images"][0].shape))
+    prm = O.Params(fixed_outer_iters=max(1, r["outer_iters"]), max_outer=max(1, r["outer_iters"]))
+    rp = O.tilt(img, b["boxes"][0], b["tau0"][0], cfg.kind, prm)
+    return float(np.max(np.abs(rp["tau"] - r["tau"]))) > 1e-3
+
+
 def test_convergence_free_running(solver, T):
     """Free-running rho decisions (only the outer count replayed): fp32 vs fp64 branch flips
-    (reading Z21) can move the flat aspect direction; most patches still agree to 1e-3."""
-    res = _convergence_case(solver, T, ts.CONFIGS[1], list(range(8)), replay=False)
+    (reading Z21) can move the flat aspect direction. Disagreeing patches are classified by Z22;
+    the stable ones must agree (at most one fp32 branch-flip case among 8 is tolerated)."""
+    cfg = ts.CONFIGS[1]
+    res = _convergence_case(solver, T, cfg, list(range(8)), replay=False)
     bad = _disagreements(res)
+    unstable = [d for d in bad if _unstable(cfg, d[0], res[d[0]][0])]
+    stable_bad = [d for d in bad if d not in unstable]
+    print(f"free-running: {len(bad)} of 8 disagree, {len(unstable)} of them unstable (Z22)")
     assert len(bad) <= 3, bad
+    assert len(stable_bad) <= 1, (stable_bad, unstable)
 
 
 def test_full_size_config2(solver, T):
