@@ -134,7 +134,7 @@ bool params_ok(const tilt_params* p) {
   if (p->pyramid_levels < 1 || p->pyramid_levels > 2) return false;
   if (p->constraint_mode != TILT_CONSTRAINTS_NONE && p->constraint_mode != TILT_CONSTRAINTS_CENTER_AREA) return false;
   if (p->kernel_path < 0 || p->kernel_path > 3) return false;
-  if (p->inner_solver == 1 && p->kernel_path == 3) return false;  // the multi-CTA path runs LADMAP only
+  if (p->inner_solver == 1 && p->svd_mode == 1) return false;  // SVDWS is LADMAP's (Table 1's third column)
   if (p->inner_solver < 0 || p->inner_solver > 1) return false;
   if (p->ctas_per_sm < 0) return false;
   if (p->pyramid_warm < 0 || p->pyramid_warm > 1) return false;
@@ -741,7 +741,7 @@ tilt_status tilt_inner_batch(tilt_handle* h, const float* D, const float* J, con
   a.Y = Y;
   a.rep = rep;
   if (prm->kernel_path == 3 || m > 256 || n > 256 || prm->svd_mode == 1) {
-    if (prm->inner_solver != 0 || (prm->svd_mode == 1 && m < n)) return TILT_E_ARG;
+    if (prm->svd_mode == 1 && m < n) return TILT_E_ARG;
     return tilt::lp::inner(lp_ctx(h), D, J, Q, Q ? l : 0, B, m, n, p, a.P, A, E, Y, rep);
   }
   return dispatch<InnerF>(size_class(m, n), h, a);

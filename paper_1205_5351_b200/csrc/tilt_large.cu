@@ -50,6 +50,7 @@ struct St {
   double Linv[64];
   float mu, mu_next, mu0, mu_max, denom, denom0, lam, eps;
   float crit1, crit2, nuc, sig1;
+  float inv_nd;  // ADM: 1 / ||D||_F
   int svt_rank, relrank, band;
   int iters, done, status, conv;
   int svt_done, big_any, rot_any, sw_cur, cap_cur, rot_cur;
@@ -326,6 +327,8 @@ __global__ void __launch_bounds__(ENT) k_kt(Args a) {
       v = D[idx];
     } else if (MODE == 1) {
       v = A[idx] + E[idx] - D[idx];
+    } else if (MODE == 3) {  // ADM dtau step: v = A + E - D - Y/mu
+      v = fmaf(-w[L.oY + idx], 1.f / st->mu, A[idx] + E[idx] - D[idx]);
     } else {
       const float an = An[idx];
       v = an + E[idx] - D[idx];
@@ -1171,6 +1174,91 @@ __global__ void k_ws_index(Args a, int* widx) {
 }
 
 // ---------------------------------------------------------------------------------------------
+// ADM baseline (adm_inner in tilt_kernels.cuh, reading Z24) on the multi-CTA path:
+//   A = S_{1/mu}(D + J dtau - E + Y/mu), E = T_{lam/mu}(D + J dtau - A + Y/mu),
+//   J dtau = K K^T (A + E - D - Y/mu), Y += mu (D + J dtau - A - E), mu *= rho;
+//   stop at ||D + J dtau - A - E||_F / ||D||_F < adm_tol. J dtau lives in the An plane.
+// ---------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(ENT) k_adm_m(Args a) {
+  const int b = blockIdx.y;
+  St* st = state(a, b);
+  if (st->done) return;
+  const Lay& L = a.L;
+  float* w = slot(a, b);
+  const float inv_mu = 1.f / st->mu;
+  FOR_ELEMS(L.plane) w[L.oS + idx] = fmaf(w[L.oY + idx], inv_mu, w[L.oD + idx] + w[L.oAn + idx] - w[L.oE + idx]);
+}
+
+__global__ void __launch_bounds__(ENT) k_adm_e(Args a) {
+  const int b = blockIdx.y;
+  St* st = state(a, b);
+  if (st->done) return;
+  const Lay& L = a.L;
+  float* w = slot(a, b);
+  const float inv_mu = 1.f / st->mu, thr = st->lam * inv_mu;
+  FOR_ELEMS(L.plane) {
+    const float x = fmaf(w[L.oY + idx], inv_mu, w[L.oD + idx] + w[L.oAn + idx] - w[L.oA + idx]);
+    w[L.oE + idx] = copysignf(fmaxf(fabsf(x) - thr, 0.f), x);
+  }
+}
+
+__global__ void __launch_bounds__(ENT) k_adm_y(Args a) {
+  const int b = blockIdx.y;
+  St* st = state(a, b);
+  if (st->done) return;
+  const Lay& L = a.L;
+  float* w = slot(a, b);
+  float s[8];
+  load_s(st->acc + ACC_S1, L.p, s);
+  const float mu = st->mu;
+  float r2[1] = {0.f};
+  FOR_ELEMS(L.plane) {
+    const float jdt = kdot(w + L.oK, L.plane, idx, L.p, s);
+    w[L.oAn + idx] = jdt;
+    const float r = w[L.oD + idx] + jdt - w[L.oA + idx] - w[L.oE + idx];
+    w[L.oY + idx] = fmaf(mu, r, w[L.oY + idx]);
+    r2[0] = fmaf(r, r, r2[0]);
+  }
+  block_add<1>(r2, st->acc + ACC_C1);
+}
+
+__global__ void k_adm_init(Args a) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= a.B) return;
+  St* st = state(a, b);
+  const double nd2 = st->acc[ACC_R + 2];
+  st->inv_nd = nd2 > 0.0 ? (float)(1.0 / sqrt(nd2)) : 1.f;
+}
+
+__global__ void k_adm_sc(Args a, int k) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= a.B) return;
+  St* st = state(a, b);
+  if (st->done) return;
+  const float resid = (float)sqrt(st->acc[ACC_C1]) * st->inv_nd;
+  if (a.P.trace) {
+    float* t = a.P.trace + 4 * ((size_t)b * a.P.max_inner + k);
+    t[0] = st->mu;
+    t[1] = resid;
+    t[2] = 0.f;
+    t[3] = 0.f;
+  }
+  st->crit1 = resid;
+  st->iters = k + 1;
+  const float mu_used = st->mu;
+  st->mu *= a.P.adm_rho;
+  for (int e = 0; e < NACC; ++e) st->acc[e] = 0.0;
+  const bool stop = resid < a.P.adm_tol;
+  if (stop) st->conv = 1;
+  if ((stop && a.P.fixed_inner <= 0) || k + 1 >= a.niter) {
+    st->done = 1;
+    st->mu = mu_used;
+  } else {
+    atomicAdd(a.counter, 1);
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
 // Host side
 // ---------------------------------------------------------------------------------------------
 struct Run {
@@ -1497,9 +1585,10 @@ tilt_status inner(Ctx& ctx, const float* D, const float* J, const float* Q, int 
   k_identity<<<R.egrid(L.vplane), ENT, 0, sm>>>(a, L.oV);
   k_kt<0><<<R.egrid(L.plane), ENT, 0, sm>>>(a);
   k_denom<<<R.egrid(L.plane), ENT, 0, sm>>>(a);
-  if (R.svdws) {
+  if (R.svdws || P.inner_solver == 1) {
     k_dnorm<<<R.egrid(L.plane), ENT, 0, sm>>>(a);
-    k_ws_init<<<R.sgrid(), 128, 0, sm>>>(a, P.svd_ws_gate);
+    if (R.svdws) k_ws_init<<<R.sgrid(), 128, 0, sm>>>(a, P.svd_ws_gate);
+    if (P.inner_solver == 1) k_adm_init<<<R.sgrid(), 128, 0, sm>>>(a);
     R.launched(2);
   }
   k_sc_denom<<<R.sgrid(), 128, 0, sm>>>(a);
@@ -1510,10 +1599,36 @@ tilt_status inner(Ctx& ctx, const float* D, const float* J, const float* Q, int 
   R.launched();
   if (R.svt_core(nullptr, 2, 0, false)) return R.st;
   k_sc_mu0<<<R.sgrid(), 128, 0, sm>>>(a);
+  R.launched();
+  const bool warm = P.svd_warm != 0;
+  if (P.inner_solver == 1) {  // ADM baseline (reading Z24): cold start A = D, E = Y = J dtau = 0
+    for (int k = 0; k < a.niter; ++k) {
+      if (!warm) {
+        k_identity<<<R.egrid(L.vplane), ENT, 0, sm>>>(a, a.oV);
+        R.launched();
+      }
+      k_adm_m<<<R.egrid(L.plane), ENT, 0, sm>>>(a);
+      R.launched();
+      if (R.svt_core(nullptr, 0, 1, true)) return R.st;
+      if (R.gemm(CUBLAS_OP_N, CUBLAS_OP_T, m, n, n, L.oB, L.ldm, a.oV, L.ldn, L.oA, L.ldm)) return R.st;
+      if (warm && (k % P.ns_period == P.ns_period - 1 || k + 1 == a.niter))
+        if (R.ns_step()) return R.st;
+      k_adm_e<<<R.egrid(L.plane), ENT, 0, sm>>>(a);
+      k_kt<3><<<R.egrid(L.plane), ENT, 0, sm>>>(a);
+      k_adm_y<<<R.egrid(L.plane), ENT, 0, sm>>>(a);
+      R.launched(3);
+      if (R.zero_counter()) return R.st;
+      k_adm_sc<<<R.sgrid(), 128, 0, sm>>>(a, k);
+      R.launched();
+      if (R.check("adm iteration")) return R.st;
+      const int act = R.read_counter();
+      if (act < 0) return R.st;
+      if (act == 0) break;
+    }
+  } else {
   k_kt<1><<<R.egrid(L.plane), ENT, 0, sm>>>(a);
   k_m0<<<R.egrid(L.plane), ENT, 0, sm>>>(a);
-  R.launched(3);
-  const bool warm = P.svd_warm != 0;
+  R.launched(2);
   for (int k = 0; k < a.niter; ++k) {
     if (!warm) {
       k_identity<<<R.egrid(L.vplane), ENT, 0, sm>>>(a, a.oV);
@@ -1560,6 +1675,7 @@ tilt_status inner(Ctx& ctx, const float* D, const float* J, const float* Q, int 
     const int act = R.read_counter();
     if (act < 0) return R.st;
     if (act == 0) break;
+  }
   }
   k_l1<<<R.egrid(L.plane), ENT, 0, sm>>>(a);
   k_report<<<R.sgrid(), 128, 0, sm>>>(a, rep);

@@ -197,3 +197,45 @@ def test_svdws_free_running_keeps_ladmap_objective(solver, T):
     assert np.all(r1["status"] == T.CONVERGED)
     assert np.sum(r1["svd_warm_steps"]) > 0
     np.testing.assert_allclose(r1["objective"], r0["objective"], rtol=1e-3)
+
+
+# ---------------------------------------------------------------------------------------------
+# ADM baseline (reading Z24) on the multi-CTA path
+# ---------------------------------------------------------------------------------------------
+def _oracle_adm(inst, K=0, max_inner=500, tol=1e-6):
+    proj = O.Projector(inst["J"].astype(np.float32).astype(np.float64))
+    d = inst["D"].astype(np.float32).astype(np.float64)
+    mu0 = 1.25 / np.linalg.svd(d, compute_uv=False)[0]
+    return O.adm(d, proj, inst["lam"], mu0, 1.25, tol, max_inner, fixed_iters=K)
+
+
+@pytest.mark.parametrize("n,K", [(100, 20), (300, 30)])
+def test_adm_fixed_count_parity_multi_cta(solver, T, n, K):
+    B = 2
+    insts = [ts.table1_instance(n, 6, s) for s in range(B)]
+    D = np.stack([i["D"] for i in insts]).astype(np.float32)
+    J = np.stack([i["J"] for i in insts]).astype(np.float32)
+    out = solver.inner(D, J, params=T.default_params(inner_solver=1, kernel_path=3, fixed_inner_iters=K, max_inner=K))
+    for k in range(B):
+        r = _oracle_adm(insts[k], K)
+        a = out["A"][k].double().cpu().numpy()
+        e = out["E"][k].double().cpu().numpy()
+        assert np.linalg.norm(a - r.A) < 1e-4 * np.linalg.norm(r.A), (n, K, k)
+        assert np.linalg.norm(e - r.E) < 1e-4 * np.linalg.norm(r.E), (n, K, k)
+        assert out["rep"]["inner_iters"][k] == K and out["rep"]["kernel_path"][k] == 3
+
+
+def test_adm_free_running_table1_300(solver, T):
+    """Table 1 at 300x300: ADM 50 iterations vs LADMAP 21.9; at the fp32-resolvable
+    tolerance (Z24) the GPU stop count equals the oracle's (+-1) and LADMAP needs < 0.6x the iterations."""
+    B = 2
+    insts = [ts.table1_instance(300, 6, s) for s in range(B)]
+    D = np.stack([i["D"] for i in insts]).astype(np.float32)
+    J = np.stack([i["J"] for i in insts]).astype(np.float32)
+    rep = solver.inner(D, J, params=T.default_params(inner_solver=1, kernel_path=3))["rep"]
+    lad = solver.inner(D, J, params=T.default_params(kernel_path=3))["rep"]
+    assert np.all(rep["status"] == T.CONVERGED)
+    assert np.mean(lad["inner_iters"]) < 0.6 * np.mean(rep["inner_iters"])
+    r = _oracle_adm(insts[0])
+    assert abs(int(rep["inner_iters"][0]) - r.iters) <= 1
+    assert rep["objective"][0] == pytest.approx(O.objective(r.A, r.E, 1 / math.sqrt(300)), rel=1e-4)

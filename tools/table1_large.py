@@ -30,6 +30,9 @@ ap.add_argument("--p", type=int, default=6)
 ap.add_argument("--out", default="")
 ap.add_argument("--svd-mode", type=int, default=0, help="tilt_params.svd_mode (1: LADMAP+SVDWS, Alg. 2)")
 ap.add_argument("--gate", type=float, default=2e-5, help="tilt_params.svd_ws_gate (eps_svd / ||D||_F)")
+ap.add_argument("--adm", type=int, default=0, help="1: the ADM baseline (tilt_params.inner_solver = 1)")
+ap.add_argument("--eps2-scale", type=float, default=0.0,
+                help="> 0: eps2 = scale * 50 / n (Cond2 is not scale-invariant, Z7; the paper tunes eps2 per size)")
 a = ap.parse_args()
 sizes = [int(x) for x in a.sizes.split(",")]
 nmax = max(sizes)
@@ -39,7 +42,9 @@ for n in sizes:
     insts = [ts.table1_instance(n, a.p, k) for k in range(a.trials)]
     D = torch.as_tensor(np.stack([i["D"] for i in insts]).astype(np.float32), device="cuda")
     J = torch.as_tensor(np.stack([i["J"] for i in insts]).astype(np.float32), device="cuda")
-    prm = T.default_params(kernel_path=3, svd_mode=a.svd_mode, svd_ws_gate=a.gate)
+    prm = T.default_params(kernel_path=3, svd_mode=a.svd_mode, svd_ws_gate=a.gate, inner_solver=a.adm)
+    if a.eps2_scale > 0:
+        prm.eps2 = a.eps2_scale * 50.0 / n
     s.inner(D[:1], J[:1], params=prm)  # warm-up (workspace, cuBLAS)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
@@ -54,8 +59,9 @@ for n in sizes:
     t_all = e0.elapsed_time(e1) / 1e3
     rep = out["rep"]
     it, sw = rep["inner_iters"], rep["jacobi_sweeps"]
-    lad = PAPER.get(n, ((None,) * 3,) * 3)[2 if a.svd_mode == 1 else 0]
-    row = {"size": n, "trials": a.trials, "p": a.p, "svd_mode": a.svd_mode, "gate": a.gate,
+    lad = PAPER.get(n, ((None,) * 3,) * 3)[1 if a.adm else (2 if a.svd_mode == 1 else 0)]
+    row = {"size": n, "trials": a.trials, "p": a.p, "solver": "adm" if a.adm else "ladmap", "svd_mode": a.svd_mode, "eps2": float(prm.eps2),
+           "gate": a.gate,
            "warm_steps_mean": float(rep["svd_warm_steps"].mean()), "iters_mean": float(it.mean()),
            "objective_mean": float(rep["objective"].mean()), "sweeps_per_svt": float(sw.sum() / it.sum()),
            "converged": int((rep["status"] == T.CONVERGED).sum()),
