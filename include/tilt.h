@@ -108,7 +108,8 @@ typedef struct {
   int32_t ns_period;
   /* inner solver: 0 = LADMAP (the paper's), 1 = the ADM baseline of Zhang et al. as
    * restated in P:241-264 (three variables, mu_{k+1} = adm_rho mu_k unbounded, cold start every outer
-   * iteration, dtau from the ADM). CTA kernels only. */
+   * iteration, dtau from the ADM). CTA kernels and the multi-CTA path (not the
+   * warp-per-patch kernel; not with svd_mode 1). */
   int32_t inner_solver;
   float adm_rho;          /* ADM penalty growth (default 1.25) */
   float adm_tol;          /* ADM stop: ||D + J dtau - A - E||_F / ||D||_F < adm_tol (default 1e-6: the
