@@ -271,3 +271,33 @@ def test_pyramid_config3_small(solver, T, warm):
         a = out["A"][k].double().cpu().numpy()
         assert np.linalg.norm(a - refs[k]["A"]) / np.linalg.norm(refs[k]["A"]) < 1e-3
         assert rep["outer_iters"][k] == 4 and rep["inner_iters"][k] == 4 * K
+
+
+@pytest.fixture(scope="module")
+def solver_big(T):
+    s = T.TiltSolver(0, max_batch=4, max_m=200, max_n=200, max_p=8, max_image_elems=4 * 400 * 400)
+    yield s
+    s.close()
+
+
+@pytest.mark.parametrize("cfg_id", [3, 4])
+def test_fixed_count_parity_large_configs(solver_big, T, cfg_id):
+    """Configs 3 (100x100 homography, fine level without the pyramid: the S128 class) and 4
+    (200x200 affine: the S256 class, B in shared memory, V and S in the workspace): one outer
+    iteration of 20 LADMAP iterations with replayed rho, A and E within 1e-4 of the oracle."""
+    cfg = ts.CONFIGS[cfg_id]
+    B, K = 2, 20
+    b = ts.gen_batch(cfg, 0, B)
+    prm_o = O.Params(fixed_inner_iters=K, fixed_outer_iters=1, max_inner=K, max_outer=1)
+    refs = [O.tilt(b["images"][k], b["boxes"][k], b["tau0"][k], cfg.kind, prm_o) for k in range(B)]
+    rr = _replay_tensor([r["traces"] for r in refs], 1, K)
+    prm = T.default_params(fixed_inner_iters=K, fixed_outer_iters=1, max_inner=K, max_outer=1)
+    prm.rho_replay = rr.data_ptr()
+    out = solver_big.solve(b["images"], b["patch_image"], b["boxes"], b["tau0"], cfg.kind, prm)
+    for k in range(B):
+        a = out["A"][k].double().cpu().numpy()
+        e = out["E"][k].double().cpu().numpy()
+        ra = np.linalg.norm(a - refs[k]["A"]) / np.linalg.norm(refs[k]["A"])
+        re = np.linalg.norm(e - refs[k]["E"]) / np.linalg.norm(refs[k]["E"])
+        assert ra < 1e-4 and re < 1e-4, (cfg_id, k, ra, re)
+        assert np.max(np.abs(out["tau"][k].double().cpu().numpy() - refs[k]["tau"])) < 1e-3
