@@ -510,9 +510,13 @@ static tilt_status solve_level(tilt_handle* h, const float* images, int32_t n_im
     a.warm_Y = warm_aey + 2 * cn;
     a.warm_rep = warm_rep;
   }
-  if (prm->kernel_path == 3 || m > 256 || n > 256 || prm->svd_mode != 0) {
-    g_last_error = "tilt_solve_batch: windows up to 256 x 256, svd_mode 0 (the multi-CTA path serves tilt_inner_batch / tilt_svt_batch)";
-    return TILT_E_ARG;
+  if (prm->kernel_path == 3 || m > 256 || n > 256 || prm->svd_mode != 0) {  // the multi-CTA path
+    if (prm->inner_solver != 0 || (prm->svd_mode == 1 && m < n)) {
+      g_last_error = "multi-CTA tilt_solve_batch: LADMAP only (svd_mode 1 needs m >= n)";
+      return TILT_E_ARG;
+    }
+    return tilt::lp::solve(lp_ctx(h), images, n_images, H, W, patch_image, boxes, tau0, B, m, n, kind, to_dev(prm),
+                           tau_out, A_out, E_out, Y_out, rep);
   }
   const bool rj_ok = tilt::rjh::fits(m, n);
   if (prm->kernel_path == 2 && !rj_ok) {

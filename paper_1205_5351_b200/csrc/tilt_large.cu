@@ -60,6 +60,11 @@ struct St {
   double wacc[8];  // ||M - M_prev||^2, <h0, h1>, ||h1||^2, <h0, h2>, ||P_U||^2, ||P_V||^2
   float eps_svd, t_star;
   int warm, have_prev, cay_k, warm_steps;
+  // Algorithm 1 state (solve entry)
+  double tau[8];
+  double Q[24];
+  float f_prev, f, dtau_inf, nd;
+  int outer_done, have_fprev, outer_iters, inner_total, stop_rule, esc;
 };
 
 struct Lay {
@@ -130,10 +135,20 @@ struct Args {
   int NB, NBp;     // Jacobi blocks
   int niter;
   int* counter;
+  int rep_outer, cur_outer;  // replay / trace rows: [B][rep_outer][max_inner] (1, 0 for the inner entry)
+  // Algorithm 1 (tilt_solve_batch on the multi-CTA path)
+  const float* images;
+  int n_images, H, W, kind;
+  const int* patch_image;
+  const int* boxes;
 };
 
 __device__ __forceinline__ float* slot(const Args& a, int b) { return a.ws + (size_t)b * a.L.stride; }
 __device__ __forceinline__ St* state(const Args& a, int b) { return reinterpret_cast<St*>(slot(a, b) + a.L.oSt); }
+// row of the replay bits / trace of inner iteration k of problem b (current outer iteration)
+__device__ __forceinline__ size_t rix(const Args& a, int b, int k) {
+  return ((size_t)b * a.rep_outer + a.cur_outer) * a.P.max_inner + k;
+}
 
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
@@ -208,7 +223,8 @@ __global__ void __launch_bounds__(256) k_from_plane(float* __restrict__ dst, Arg
   __shared__ float t[32][33];
   const int b = blockIdx.z;
   const float* s = slot(a, b) + off;
-  const bool z = zero_bad && state(a, b)->status == TILT_PATCH_SINGULAR_GRAM;
+  const bool z = (zero_bad == 1 && state(a, b)->status == TILT_PATCH_SINGULAR_GRAM) ||
+                 (zero_bad == 2 && state(a, b)->outer_iters == 0);
   float* d = dst + (size_t)b * rows * cols;
   const int i0 = blockIdx.y * 32, j0 = blockIdx.x * 32;
   for (int c = threadIdx.y; c < 32; c += 8) {
@@ -228,6 +244,7 @@ __global__ void __launch_bounds__(256) k_from_plane(float* __restrict__ dst, Arg
 // ---------------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(ENT) k_gram(Args a) {
   const int b = blockIdx.y;
+  if (state(a, b)->outer_done) return;
   const Lay& L = a.L;
   const float* K = slot(a, b) + L.oK;
   double g[36];
@@ -264,25 +281,28 @@ __global__ void __launch_bounds__(ENT) k_gram(Args a) {
   }
 }
 
-__global__ void k_chol(Args a, const float* __restrict__ Q, int l) {
+// Q: the caller's rows [B][l][p] (inner entry), or st->Q (l = 3, solve entry) when q_state
+__global__ void k_chol(Args a, const float* __restrict__ Q, int l, int q_state) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= a.B) return;
   St* st = state(a, b);
+  if (st->outer_done) return;
   double qr[24];
-  for (int e = 0; e < 24; ++e) qr[e] = 0.0;
-  if (Q)
+  for (int e = 0; e < 24; ++e) qr[e] = q_state ? st->Q[e] : 0.0;
+  if (Q && !q_state)
     for (int r = 0; r < l; ++r)
       for (int q = 0; q < a.L.p; ++q) qr[r * 8 + q] = Q[((size_t)b * l + r) * a.L.p + q];
-  const bool ok = chol_inverse(st->acc + ACC_G, qr, Q ? l : 0, a.L.p, st->Linv);
+  const bool ok = chol_inverse(st->acc + ACC_G, qr, (Q || q_state) ? l : 0, a.L.p, st->Linv);
   st->status = ok ? TILT_PATCH_CONVERGED : TILT_PATCH_SINGULAR_GRAM;
   st->done = ok ? 0 : 1;
+  if (!ok) st->outer_done = 1;
   for (int e = 0; e < NACC; ++e) st->acc[e] = 0.0;
 }
 
 __global__ void __launch_bounds__(ENT) k_apply_linv(Args a) {
   const int b = blockIdx.y;
   St* st = state(a, b);
-  if (st->status != TILT_PATCH_CONVERGED) return;
+  if (st->status != TILT_PATCH_CONVERGED || st->outer_done) return;
   const Lay& L = a.L;
   float* K = slot(a, b) + L.oK;
   const double* Li = st->Linv;
@@ -522,7 +542,7 @@ __global__ void k_sc_mu0(Args a) {
   st->mu0 = s1 > 0.f ? a.P.mu0_scale / s1 : a.P.mu0_scale;
   st->mu = st->mu0;
   st->mu_max = a.P.mu_max_ratio * st->mu0;
-  st->aux_sweeps = st->sw_cur;
+  st->aux_sweeps += st->sw_cur;
   for (int e = 0; e < NACC; ++e) st->acc[e] = 0.0;
 }
 
@@ -535,10 +555,10 @@ __global__ void k_sc1(Args a, int k) {
   const float dA = (float)st->acc[ACC_DA], dE = (float)st->acc[ACC_DE];
   const float crit2 = st->mu * sqrtf(fmaxf(dA, dE)) / st->denom;
   int rho_bit = crit2 < a.P.eps2 ? 1 : 0;
-  if (a.P.rho_replay) rho_bit = a.P.rho_replay[(size_t)b * a.P.max_inner + k] & 1;
+  if (a.P.rho_replay) rho_bit = a.P.rho_replay[rix(a, b, k)] & 1;
   st->mu_next = fminf(st->mu_max, rho_bit ? a.P.rho0 * st->mu : st->mu);
   st->crit2 = crit2;
-  if (a.P.trace) a.P.trace[4 * ((size_t)b * a.P.max_inner + k) + 3] = (float)rho_bit;
+  if (a.P.trace) a.P.trace[4 * (rix(a, b, k)) + 3] = (float)rho_bit;
 }
 
 // Cond1, the stop rule (strict), mu <- mu_{k+1}
@@ -549,7 +569,7 @@ __global__ void k_sc2(Args a, int k) {
   if (st->done) return;
   const float crit1 = (float)sqrt(st->acc[ACC_C1]) / st->denom;
   if (a.P.trace) {
-    float* t = a.P.trace + 4 * ((size_t)b * a.P.max_inner + k);
+    float* t = a.P.trace + 4 * (rix(a, b, k));
     t[0] = st->mu;
     t[1] = crit1;
     t[2] = st->crit2;
@@ -557,7 +577,7 @@ __global__ void k_sc2(Args a, int k) {
   st->crit1 = crit1;
   st->iters = k + 1;
   bool stop = crit1 < a.P.eps1 && st->crit2 < a.P.eps2;
-  if (a.P.rho_replay) stop = (a.P.rho_replay[(size_t)b * a.P.max_inner + k] & 2) != 0;
+  if (a.P.rho_replay) stop = (a.P.rho_replay[rix(a, b, k)] & 2) != 0;
   if (stop) st->conv = 1;
   const float mu_used = st->mu;
   st->mu = st->mu_next;
@@ -1008,7 +1028,7 @@ __global__ void k_ws_gate(Args a, int k) {
   st->warm = 0;
   if (st->done || !st->have_prev) return;
   bool w = sqrt(st->wacc[0]) < (double)st->eps_svd;
-  if (a.P.rho_replay) w = (a.P.rho_replay[(size_t)b * a.P.max_inner + k] & 4) != 0;
+  if (a.P.rho_replay) w = (a.P.rho_replay[rix(a, b, k)] & 4) != 0;
   for (int e = 0; e < 8; ++e) st->wacc[e] = 0.0;
   st->eps = 1.f / st->mu;
   if (w) {
@@ -1237,7 +1257,7 @@ __global__ void k_adm_sc(Args a, int k) {
   if (st->done) return;
   const float resid = (float)sqrt(st->acc[ACC_C1]) * st->inv_nd;
   if (a.P.trace) {
-    float* t = a.P.trace + 4 * ((size_t)b * a.P.max_inner + k);
+    float* t = a.P.trace + 4 * (rix(a, b, k));
     t[0] = st->mu;
     t[1] = resid;
     t[2] = 0.f;
@@ -1256,6 +1276,280 @@ __global__ void k_adm_sc(Args a, int k) {
   } else {
     atomicAdd(a.counter, 1);
   }
+}
+
+// ---------------------------------------------------------------------------------------------
+// Algorithm 1 on the multi-CTA path (tilt_solve_batch, windows above 256; solve_patch in
+// tilt_kernels.cuh is the CTA-per-patch version of the same steps)
+// ---------------------------------------------------------------------------------------------
+__global__ void k_solve_init(Args a, const float* __restrict__ tau0) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= a.B) return;
+  St* st = state(a, b);
+  const int p = a.L.p;
+  for (int q = 0; q < 8; ++q) st->tau[q] = 0.0;
+  if (tau0) {
+    for (int q = 0; q < p; ++q) st->tau[q] = tau0[(size_t)b * p + q];
+  } else {
+    st->tau[0] = 1.0;
+    st->tau[3] = 1.0;
+  }
+  st->status = TILT_PATCH_MAX_OUTER;
+  st->stop_rule = 0;
+  st->f = st->f_prev = st->dtau_inf = st->nd = __int_as_float(0x7fc00000);
+}
+
+// Step 1 (Z2, Z15, Z16), pass 1: d, gx, gy, gz per pixel (fp64 geometry, the CTA
+// kernel's warp_pixel) into D and K[0..2]; sums of d^2 and J_raw^T d; window escape
+__global__ void __launch_bounds__(ENT) k_lwarp(Args a) {
+  const int b = blockIdx.y;
+  St* st = state(a, b);
+  if (st->outer_done) return;
+  const Lay& L = a.L;
+  float* w = slot(a, b);
+  const int bx[4] = {a.boxes[4 * b], a.boxes[4 * b + 1], a.boxes[4 * b + 2], a.boxes[4 * b + 3]};
+  const WarpGeom g = make_geom(bx, st->tau, a.kind);
+  const float* img = a.images + (size_t)a.patch_image[b] * a.H * a.W;
+  const double ci = 0.5 * (L.m - 1), cj = 0.5 * (L.n - 1), inv_s = 1.0 / g.s;
+  const bool homog = a.kind == TILT_HOMOGRAPHY;
+  float acc[9];
+#pragma unroll
+  for (int q = 0; q < 9; ++q) acc[q] = 0.f;
+  int esc = 0;
+  FOR_ELEMS(L.plane) {
+    const int j = (int)(idx / L.ldm), i = (int)(idx % L.ldm);
+    if (i >= L.m || j >= L.n) continue;
+    double d, gx, gy, gz;
+    if (!warp_pixel(g, img, a.H, a.W, i, j, d, gx, gy, gz)) esc = 1;
+    const float df = (float)d, gxf = (float)gx, gyf = (float)gy, gzf = (float)gz;
+    w[L.oD + idx] = df;
+    w[L.oK + idx] = gxf;
+    w[L.oK + L.plane + idx] = gyf;
+    w[L.oK + 2 * L.plane + idx] = gzf;
+    double jr[8];
+    jraw_row(gxf, gyf, homog ? (double)gzf : 0.0, ((double)j - cj) * inv_s, ((double)i - ci) * inv_s, jr);
+    acc[8] = fmaf(df, df, acc[8]);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc[q] = fmaf((float)jr[q], df, acc[q]);
+  }
+  if (__syncthreads_or(esc) && threadIdx.x == 0) atomicOr(&st->esc, 1);
+  block_add<9>(acc, st->acc);
+}
+
+// Step 1 status: ||D o tau||, escape / zero patch (these end the problem, as in solve_patch)
+__global__ void k_lwarp_status(Args a) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= a.B) return;
+  St* st = state(a, b);
+  if (st->outer_done) return;
+  const double nd = sqrt(st->acc[8]);
+  st->nd = (float)nd;
+  if (st->esc) {
+    st->status = TILT_PATCH_WINDOW_ESCAPE;
+    st->outer_done = 1;
+  } else if (!(nd > 0.0)) {
+    st->status = TILT_PATCH_ZERO_PATCH;
+    st->outer_done = 1;
+  } else {
+    for (int q = 0; q < 8; ++q) st->Linv[q] = st->acc[q] / nd;  // c = D_hat^T J_raw (Linv is rebuilt next)
+  }
+  for (int e = 0; e < NACC; ++e) st->acc[e] = 0.0;
+}
+
+// Step 1, pass 2: D_hat = d / ||d||, J = (J_raw - D_hat c^T) / ||d|| (quotient rule)
+__global__ void __launch_bounds__(ENT) k_lwarp_norm(Args a) {
+  const int b = blockIdx.y;
+  St* st = state(a, b);
+  if (st->outer_done) return;
+  const Lay& L = a.L;
+  float* w = slot(a, b);
+  const double ind = 1.0 / (double)st->nd;
+  double c[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) c[q] = st->Linv[q];
+  const double s = 0.5 * (double)max(L.m, L.n);
+  const double ci = 0.5 * (L.m - 1), cj = 0.5 * (L.n - 1), inv_s = 1.0 / s;
+  const bool homog = a.kind == TILT_HOMOGRAPHY;
+  const int p = L.p;
+  FOR_ELEMS(L.plane) {
+    const int j = (int)(idx / L.ldm), i = (int)(idx % L.ldm);
+    if (i >= L.m || j >= L.n) continue;
+    const double d = w[L.oD + idx];
+    const double gx = w[L.oK + idx], gy = w[L.oK + L.plane + idx], gz = w[L.oK + 2 * L.plane + idx];
+    double jr[8];
+    jraw_row(gx, gy, homog ? gz : 0.0, ((double)j - cj) * inv_s, ((double)i - ci) * inv_s, jr);
+    const double dh = d * ind;
+    w[L.oD + idx] = (float)dh;
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (q < p) w[L.oK + q * L.plane + idx] = (float)((jr[q] - dh * c[q]) * ind);
+  }
+}
+
+// constraint rows Q (Z10) from tau
+__global__ void k_qrows(Args a) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= a.B) return;
+  St* st = state(a, b);
+  for (int e = 0; e < 24; ++e) st->Q[e] = 0.0;
+  if (st->outer_done || a.P.constraint_mode != TILT_CONSTRAINTS_CENTER_AREA) return;
+  constraint_rows(st->tau, a.kind, a.L.m, a.L.n, st->Q);
+}
+
+// every inner loop starts with the problems whose outer loop is still running
+__global__ void k_outer_begin(Args a) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= a.B) return;
+  St* st = state(a, b);
+  st->done = st->outer_done;
+  st->iters = 0;
+  st->conv = 0;
+}
+
+// cold start of an inner loop: A = D_hat, E = Y = 0 (Z4)
+__global__ void __launch_bounds__(ENT) k_cold(Args a) {
+  const int b = blockIdx.y;
+  if (state(a, b)->done) return;
+  float* w = slot(a, b);
+  FOR_ELEMS(a.L.plane) {
+    w[a.L.oA + idx] = w[a.L.oD + idx];
+    w[a.L.oE + idx] = 0.f;
+    w[a.L.oY + idx] = 0.f;
+  }
+}
+
+// Y <- W^TW Y (Eq. Y_new_warmstart): K^T Y, then Y -= K (K^T Y)
+__global__ void __launch_bounds__(ENT) k_kty(Args a) {
+  const int b = blockIdx.y;
+  St* st = state(a, b);
+  if (st->done) return;
+  const Lay& L = a.L;
+  const float* w = slot(a, b);
+  float s[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) s[q] = 0.f;
+  FOR_ELEMS(L.plane) {
+    const float y = w[L.oY + idx];
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (q < L.p) s[q] = fmaf(w[L.oK + q * L.plane + idx], y, s[q]);
+  }
+  block_add<8>(s, st->acc + ACC_S1);
+}
+
+__global__ void __launch_bounds__(ENT) k_projy(Args a) {
+  const int b = blockIdx.y;
+  St* st = state(a, b);
+  if (st->done) return;
+  const Lay& L = a.L;
+  float* w = slot(a, b);
+  float s[8];
+  load_s(st->acc + ACC_S1, L.p, s);
+  FOR_ELEMS(L.plane) w[L.oY + idx] -= kdot(w + L.oK, L.plane, idx, L.p, s);
+}
+
+__global__ void k_clear_acc(Args a) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= a.B) return;
+  St* st = state(a, b);
+  if (st->done) return;
+  for (int e = 0; e < NACC; ++e) st->acc[e] = 0.0;
+}
+
+// Step 3 inputs: K^T (A + E - D_hat) and ||E||_1 (problems whose outer loop runs)
+__global__ void __launch_bounds__(ENT) k_dtau_red(Args a) {
+  const int b = blockIdx.y;
+  St* st = state(a, b);
+  if (st->outer_done) return;
+  const Lay& L = a.L;
+  const float* w = slot(a, b);
+  float s[9];
+#pragma unroll
+  for (int q = 0; q < 9; ++q) s[q] = 0.f;
+  FOR_ELEMS(L.plane) {
+    const float e = w[L.oE + idx];
+    const float v = w[L.oA + idx] + e - w[L.oD + idx];
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (q < L.p) s[q] = fmaf(w[L.oK + q * L.plane + idx], v, s[q]);
+    s[8] += fabsf(e);
+  }
+  block_add<9>(s, st->acc + ACC_S1);
+}
+
+// Steps 3-4 and the outer stop (Eq. Delta_tau P:376-378 with Q; tau += dtau; Z9)
+__global__ void k_dtau(Args a, int it, int n_outer) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= a.B) return;
+  St* st = state(a, b);
+  if (st->outer_done) return;
+  const int p = a.L.p;
+  double dt_inf = 0.0;
+  bool finite = true;
+  for (int q = 0; q < p; ++q) {
+    double dq = 0.0;
+    for (int r = q; r < p; ++r) dq += st->Linv[r * 8 + q] * (double)(float)st->acc[ACC_S1 + r];
+    st->tau[q] += dq;
+    dt_inf = fmax(dt_inf, fabs(dq));
+    finite = finite && isfinite(st->tau[q]);
+  }
+  const float f = st->nuc + st->lam * (float)st->acc[ACC_S1 + 8];
+  st->dtau_inf = (float)dt_inf;
+  st->f = f;
+  st->outer_iters = it + 1;
+  st->inner_total += st->iters;
+  for (int e = 0; e < NACC; ++e) st->acc[e] = 0.0;
+  if (!finite || !isfinite(f) || f > 1e12f) {
+    st->status = TILT_PATCH_DIVERGED;
+    st->outer_done = 1;
+    return;
+  }
+  int rule = 0;
+  if (st->have_fprev && fabsf(f - st->f_prev) < a.P.obj_tol * fabsf(st->f_prev)) rule = 1;
+  else if (st->dtau_inf < a.P.tau_tol) rule = 2;
+  st->f_prev = f;
+  st->have_fprev = 1;
+  if (rule) {
+    st->status = TILT_PATCH_CONVERGED;
+    st->stop_rule = rule;
+    if (a.P.fixed_outer <= 0) st->outer_done = 1;
+  } else {
+    st->status = TILT_PATCH_MAX_OUTER;
+    st->stop_rule = 3;
+  }
+  if (it + 1 >= n_outer) st->outer_done = 1;
+  if (!st->outer_done) atomicAdd(a.counter, 1);
+}
+
+__global__ void k_report_solve(Args a, tilt_report* rep, float* tau_out) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= a.B) return;
+  const St* st = state(a, b);
+  const int p = a.L.p;
+  for (int q = 0; q < p; ++q) tau_out[(size_t)b * p + q] = (float)st->tau[q];
+  if (!rep) return;
+  tilt_report r;
+  memset(&r, 0, sizeof(r));
+  r.status = st->status;
+  r.stop_rule = st->stop_rule;
+  r.outer_iters = st->outer_iters;
+  r.inner_iters = st->inner_total;
+  r.jacobi_sweeps = st->sweeps;
+  r.aux_sweeps = st->aux_sweeps;
+  r.rank = st->relrank;
+  r.rank_band = st->band;
+  r.svt_rank = st->svt_rank;
+  r.sweep_cap_hits = st->caps;
+  r.objective = st->f;
+  r.crit1 = st->crit1;
+  r.crit2 = st->crit2;
+  r.patch_norm = st->nd;
+  r.dtau_inf = st->dtau_inf;
+  r.mu_last = st->mu;
+  r.jacobi_rotations = st->rotations;
+  r.kernel_path = 3;
+  r.svd_warm_steps = st->warm_steps;
+  rep[b] = r;
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -1497,6 +1791,11 @@ struct Run {
     a.P = P;
     a.oV = a.L.oV;
     a.counter = ctx.counter;
+    a.rep_outer = 1;
+    a.cur_outer = 0;
+    a.images = nullptr;
+    a.boxes = nullptr;
+    a.patch_image = nullptr;
     a.tiny2 = 1e-14f;  // ||b_j|| <= 1e-7 ||M||_F: below fp32 resolution of the SVT output
     a.NB = (n + BW - 1) / BW;
     a.NBp = a.NB + (a.NB & 1);
@@ -1558,6 +1857,130 @@ void release(Ctx& ctx) {
   ctx = Ctx();
 }
 
+// Orthonormalise (K2) from the planes in D / K, the (warm or cold) start, mu_0 (Z3) and one inner loop
+// (LADMAP or the ADM baseline) for every problem with done == 0. Returns true on error (R.st set).
+static bool inner_core(Run& R, const DevParams& P, const float* Q, int l, int q_state, bool first) {
+  Args& a = R.a;
+  const Lay& L = a.L;
+  const int m = L.m, n = L.n;
+  cudaStream_t sm = R.ctx.stream;
+    k_gram<<<R.egrid(L.plane), ENT, 0, sm>>>(a);
+  k_chol<<<R.sgrid(), 128, 0, sm>>>(a, Q, l, q_state);
+  k_apply_linv<<<R.egrid(L.plane), ENT, 0, sm>>>(a);
+  R.launched(3);
+  // warm start (Eq. warm_start, Eq. Y_new_warmstart) or A_0 = D, E_0 = Y_0 = 0
+  if (first || !P.vws) {
+    k_cold<<<R.egrid(L.plane), ENT, 0, sm>>>(a);
+    R.launched();
+  } else {
+    k_clear_acc<<<R.sgrid(), 128, 0, sm>>>(a);
+    k_kty<<<R.egrid(L.plane), ENT, 0, sm>>>(a);
+    k_projy<<<R.egrid(L.plane), ENT, 0, sm>>>(a);
+    k_clear_acc<<<R.sgrid(), 128, 0, sm>>>(a);
+    R.launched(4);
+  }
+  if (first) {
+    k_identity<<<R.egrid(L.vplane), ENT, 0, sm>>>(a, L.oV);
+    R.launched();
+  }
+  // ||W^TW D||
+  k_kt<0><<<R.egrid(L.plane), ENT, 0, sm>>>(a);
+  k_denom<<<R.egrid(L.plane), ENT, 0, sm>>>(a);
+  if (R.svdws || P.inner_solver == 1) {
+    k_dnorm<<<R.egrid(L.plane), ENT, 0, sm>>>(a);
+    if (R.svdws) k_ws_init<<<R.sgrid(), 128, 0, sm>>>(a, P.svd_ws_gate);
+    if (P.inner_solver == 1) k_adm_init<<<R.sgrid(), 128, 0, sm>>>(a);
+    R.launched(2);
+  }
+  k_sc_denom<<<R.sgrid(), 128, 0, sm>>>(a);
+  R.launched(5);
+  if (R.check("inner setup")) return true;
+  // sigma_1(D) by the same Jacobi (Z3); its V warm-starts the first SVT
+  k_copy_plane<<<R.egrid(L.plane), ENT, 0, sm>>>(a, L.oS, L.oD);
+  R.launched();
+  if (R.svt_core(nullptr, 2, 0, false)) return true;
+  k_sc_mu0<<<R.sgrid(), 128, 0, sm>>>(a);
+  R.launched();
+  const bool warm = P.svd_warm != 0;
+  if (P.inner_solver == 1) {  // ADM baseline (reading Z24): cold start A = D, E = Y = J dtau = 0
+    for (int k = 0; k < a.niter; ++k) {
+      if (!warm) {
+        k_identity<<<R.egrid(L.vplane), ENT, 0, sm>>>(a, a.oV);
+        R.launched();
+      }
+      k_adm_m<<<R.egrid(L.plane), ENT, 0, sm>>>(a);
+      R.launched();
+      if (R.svt_core(nullptr, 0, 1, true)) return true;
+      if (R.gemm(CUBLAS_OP_N, CUBLAS_OP_T, m, n, n, L.oB, L.ldm, a.oV, L.ldn, L.oA, L.ldm)) return true;
+      if (warm && (k % P.ns_period == P.ns_period - 1 || k + 1 == a.niter))
+        if (R.ns_step()) return true;
+      k_adm_e<<<R.egrid(L.plane), ENT, 0, sm>>>(a);
+      k_kt<3><<<R.egrid(L.plane), ENT, 0, sm>>>(a);
+      k_adm_y<<<R.egrid(L.plane), ENT, 0, sm>>>(a);
+      R.launched(3);
+      if (R.zero_counter()) return true;
+      k_adm_sc<<<R.sgrid(), 128, 0, sm>>>(a, k);
+      R.launched();
+      if (R.check("adm iteration")) return true;
+      const int act = R.read_counter();
+      if (act < 0) return true;
+      if (act == 0) break;
+    }
+  } else {
+  k_kt<1><<<R.egrid(L.plane), ENT, 0, sm>>>(a);
+  k_m0<<<R.egrid(L.plane), ENT, 0, sm>>>(a);
+  R.launched(2);
+  for (int k = 0; k < a.niter; ++k) {
+    if (!warm) {
+      k_identity<<<R.egrid(L.vplane), ENT, 0, sm>>>(a, a.oV);
+      R.launched();
+    }
+    int nwarm = 0, K = 0;
+    if (R.svdws && k > 0) {  // Alg. 2 gate, then the warm step's first half for the gated problems
+      if (R.zero_counter()) return true;
+      k_ws_diff<<<R.egrid(L.plane), ENT, 0, sm>>>(a);
+      k_ws_gate<<<R.sgrid(), 128, 0, sm>>>(a, k);
+      R.launched(2);
+      int c[3];
+      if (!R.read_counters(c)) return true;
+      if (c[1] > 0) {
+        if (R.ws_subset(c[1])) return true;
+        if (R.ws_part1()) return true;
+        R.nsub = 0;
+        if (!R.read_counters(c)) return true;
+        nwarm = c[1];
+        K = c[2];
+      }
+    }
+    if (R.svt_core(nullptr, 0, 1, true, R.svdws)) return true;
+    if (nwarm > 0) {
+      if (R.ws_subset(nwarm)) return true;
+      if (R.ws_part2(K)) return true;
+      R.nsub = 0;
+    }
+    if (R.gemm(CUBLAS_OP_N, CUBLAS_OP_T, m, n, n, L.oB, L.ldm, a.oV, L.ldn, L.oAn, L.ldm)) return true;
+    if (warm && (k % P.ns_period == P.ns_period - 1 || k + 1 == a.niter))
+      if (R.ns_step()) return true;
+    if (R.svdws) {
+      k_ws_after<<<R.egrid(L.plane), ENT, 0, sm>>>(a);
+      R.launched();
+    }
+    k_kt<2><<<R.egrid(L.plane), ENT, 0, sm>>>(a);
+    k_estep<<<R.egrid(L.plane), ENT, 0, sm>>>(a);
+    k_sc1<<<R.sgrid(), 128, 0, sm>>>(a, k);
+    k_ystep<<<R.egrid(L.plane), ENT, 0, sm>>>(a);
+    if (R.zero_counter()) return true;
+    k_sc2<<<R.sgrid(), 128, 0, sm>>>(a, k);
+    R.launched(5);
+    if (R.check("ladmap iteration")) return true;
+    const int act = R.read_counter();
+    if (act < 0) return true;
+    if (act == 0) break;
+  }
+  }
+  return false;
+}
+
 tilt_status inner(Ctx& ctx, const float* D, const float* J, const float* Q, int l, int B, int m, int n, int p,
                   const DevParams& P, float* A, float* E, float* Y, tilt_report* rep) {
   tilt_status s0 = ensure(ctx, ws_need(B, m, n, p, P.svd_mode == 1), B);
@@ -1576,107 +1999,8 @@ tilt_status inner(Ctx& ctx, const float* D, const float* J, const float* Q, int 
   k_to_plane<<<tg, dim3(32, 8), 0, sm>>>(D, 1, a, L.oD);
   k_to_plane<<<tgj, dim3(32, 8), 0, sm>>>(J, p, a, L.oK);
   k_init<<<R.sgrid(), 128, 0, sm>>>(a);
-  k_gram<<<R.egrid(L.plane), ENT, 0, sm>>>(a);
-  k_chol<<<R.sgrid(), 128, 0, sm>>>(a, Q, l);
-  k_apply_linv<<<R.egrid(L.plane), ENT, 0, sm>>>(a);
-  R.launched(6);
-  // A_0 = D, E_0 = Y_0 = 0 (memset), V = I; ||W^TW D||
-  k_copy_plane<<<R.egrid(L.plane), ENT, 0, sm>>>(a, L.oA, L.oD);
-  k_identity<<<R.egrid(L.vplane), ENT, 0, sm>>>(a, L.oV);
-  k_kt<0><<<R.egrid(L.plane), ENT, 0, sm>>>(a);
-  k_denom<<<R.egrid(L.plane), ENT, 0, sm>>>(a);
-  if (R.svdws || P.inner_solver == 1) {
-    k_dnorm<<<R.egrid(L.plane), ENT, 0, sm>>>(a);
-    if (R.svdws) k_ws_init<<<R.sgrid(), 128, 0, sm>>>(a, P.svd_ws_gate);
-    if (P.inner_solver == 1) k_adm_init<<<R.sgrid(), 128, 0, sm>>>(a);
-    R.launched(2);
-  }
-  k_sc_denom<<<R.sgrid(), 128, 0, sm>>>(a);
-  R.launched(5);
-  if (R.check("inner setup")) return R.st;
-  // sigma_1(D) by the same Jacobi (Z3); its V warm-starts the first SVT
-  k_copy_plane<<<R.egrid(L.plane), ENT, 0, sm>>>(a, L.oS, L.oD);
-  R.launched();
-  if (R.svt_core(nullptr, 2, 0, false)) return R.st;
-  k_sc_mu0<<<R.sgrid(), 128, 0, sm>>>(a);
-  R.launched();
-  const bool warm = P.svd_warm != 0;
-  if (P.inner_solver == 1) {  // ADM baseline (reading Z24): cold start A = D, E = Y = J dtau = 0
-    for (int k = 0; k < a.niter; ++k) {
-      if (!warm) {
-        k_identity<<<R.egrid(L.vplane), ENT, 0, sm>>>(a, a.oV);
-        R.launched();
-      }
-      k_adm_m<<<R.egrid(L.plane), ENT, 0, sm>>>(a);
-      R.launched();
-      if (R.svt_core(nullptr, 0, 1, true)) return R.st;
-      if (R.gemm(CUBLAS_OP_N, CUBLAS_OP_T, m, n, n, L.oB, L.ldm, a.oV, L.ldn, L.oA, L.ldm)) return R.st;
-      if (warm && (k % P.ns_period == P.ns_period - 1 || k + 1 == a.niter))
-        if (R.ns_step()) return R.st;
-      k_adm_e<<<R.egrid(L.plane), ENT, 0, sm>>>(a);
-      k_kt<3><<<R.egrid(L.plane), ENT, 0, sm>>>(a);
-      k_adm_y<<<R.egrid(L.plane), ENT, 0, sm>>>(a);
-      R.launched(3);
-      if (R.zero_counter()) return R.st;
-      k_adm_sc<<<R.sgrid(), 128, 0, sm>>>(a, k);
-      R.launched();
-      if (R.check("adm iteration")) return R.st;
-      const int act = R.read_counter();
-      if (act < 0) return R.st;
-      if (act == 0) break;
-    }
-  } else {
-  k_kt<1><<<R.egrid(L.plane), ENT, 0, sm>>>(a);
-  k_m0<<<R.egrid(L.plane), ENT, 0, sm>>>(a);
-  R.launched(2);
-  for (int k = 0; k < a.niter; ++k) {
-    if (!warm) {
-      k_identity<<<R.egrid(L.vplane), ENT, 0, sm>>>(a, a.oV);
-      R.launched();
-    }
-    int nwarm = 0, K = 0;
-    if (R.svdws && k > 0) {  // Alg. 2 gate, then the warm step's first half for the gated problems
-      if (R.zero_counter()) return R.st;
-      k_ws_diff<<<R.egrid(L.plane), ENT, 0, sm>>>(a);
-      k_ws_gate<<<R.sgrid(), 128, 0, sm>>>(a, k);
-      R.launched(2);
-      int c[3];
-      if (!R.read_counters(c)) return R.st;
-      if (c[1] > 0) {
-        if (R.ws_subset(c[1])) return R.st;
-        if (R.ws_part1()) return R.st;
-        R.nsub = 0;
-        if (!R.read_counters(c)) return R.st;
-        nwarm = c[1];
-        K = c[2];
-      }
-    }
-    if (R.svt_core(nullptr, 0, 1, true, R.svdws)) return R.st;
-    if (nwarm > 0) {
-      if (R.ws_subset(nwarm)) return R.st;
-      if (R.ws_part2(K)) return R.st;
-      R.nsub = 0;
-    }
-    if (R.gemm(CUBLAS_OP_N, CUBLAS_OP_T, m, n, n, L.oB, L.ldm, a.oV, L.ldn, L.oAn, L.ldm)) return R.st;
-    if (warm && (k % P.ns_period == P.ns_period - 1 || k + 1 == a.niter))
-      if (R.ns_step()) return R.st;
-    if (R.svdws) {
-      k_ws_after<<<R.egrid(L.plane), ENT, 0, sm>>>(a);
-      R.launched();
-    }
-    k_kt<2><<<R.egrid(L.plane), ENT, 0, sm>>>(a);
-    k_estep<<<R.egrid(L.plane), ENT, 0, sm>>>(a);
-    k_sc1<<<R.sgrid(), 128, 0, sm>>>(a, k);
-    k_ystep<<<R.egrid(L.plane), ENT, 0, sm>>>(a);
-    if (R.zero_counter()) return R.st;
-    k_sc2<<<R.sgrid(), 128, 0, sm>>>(a, k);
-    R.launched(5);
-    if (R.check("ladmap iteration")) return R.st;
-    const int act = R.read_counter();
-    if (act < 0) return R.st;
-    if (act == 0) break;
-  }
-  }
+  R.launched(3);
+  if (inner_core(R, P, Q, l, 0, true)) return R.st;
   k_l1<<<R.egrid(L.plane), ENT, 0, sm>>>(a);
   k_report<<<R.sgrid(), 128, 0, sm>>>(a, rep);
   const dim3 og((n + 31) / 32, (m + 31) / 32, B);
@@ -1688,6 +2012,76 @@ tilt_status inner(Ctx& ctx, const float* D, const float* J, const float* Q, int 
     R.launched();
   }
   R.check("inner outputs");
+  return R.st;
+}
+
+tilt_status solve(Ctx& ctx, const float* images, int n_images, int H, int W, const int32_t* patch_image,
+                  const int32_t* boxes, const float* tau0, int B, int m, int n, int kind, const DevParams& P,
+                  float* tau_out, float* A, float* E, float* Y, tilt_report* rep) {
+  const int p = kind == TILT_HOMOGRAPHY ? 8 : 6;
+  if (P.inner_solver != 0) return TILT_E_ARG;  // the ADM's own dtau step is the CTA kernels' (k_solve)
+  tilt_status s0 = ensure(ctx, ws_need(B, m, n, p, P.svd_mode == 1), B);
+  if (s0 != TILT_OK) return s0;
+  Run R(ctx);
+  R.setup(B, m, n, p, P);
+  Args& a = R.a;
+  const Lay& L = a.L;
+  a.tol = P.jacobi_tol > 0.f ? P.jacobi_tol : default_jacobi_tol(m);
+  a.big2 = a.tol / (float)n;
+  a.max_sweeps = P.jacobi_max_sweeps;
+  a.niter = P.fixed_inner > 0 ? P.fixed_inner : P.max_inner;
+  a.rep_outer = P.max_outer;
+  a.images = images;
+  a.n_images = n_images;
+  a.H = H;
+  a.W = W;
+  a.kind = kind;
+  a.patch_image = patch_image;
+  a.boxes = boxes;
+  cudaStream_t sm = ctx.stream;
+  if (R.fail_cuda(cudaMemsetAsync(ctx.ws, 0, (size_t)B * L.stride * sizeof(float), sm), "memset(ws)")) return R.st;
+  k_init<<<R.sgrid(), 128, 0, sm>>>(a);
+  k_solve_init<<<R.sgrid(), 128, 0, sm>>>(a, tau0);
+  R.launched(2);
+  const int n_outer = P.fixed_outer > 0 ? P.fixed_outer : P.max_outer;
+  for (int it = 0; it < n_outer; ++it) {
+    a.cur_outer = it;
+    // Step 1: D_hat, J (two passes), Q
+    k_lwarp<<<R.egrid(L.plane), ENT, 0, sm>>>(a);
+    k_lwarp_status<<<R.sgrid(), 128, 0, sm>>>(a);
+    k_lwarp_norm<<<R.egrid(L.plane), ENT, 0, sm>>>(a);
+    k_qrows<<<R.sgrid(), 128, 0, sm>>>(a);
+    k_outer_begin<<<R.sgrid(), 128, 0, sm>>>(a);
+    R.launched(5);
+    if (R.check("warp")) return R.st;
+    // Step 2: orthonormalise, warm start, inner loop
+    if (inner_core(R, P, nullptr, 3, 1, it == 0)) return R.st;
+    // Steps 3-4, outer stop
+    k_dtau_red<<<R.egrid(L.plane), ENT, 0, sm>>>(a);
+    if (R.zero_counter()) return R.st;
+    k_dtau<<<R.sgrid(), 128, 0, sm>>>(a, it, n_outer);
+    R.launched(2);
+    if (R.check("dtau")) return R.st;
+    const int act = R.read_counter();
+    if (act < 0) return R.st;
+    if (act == 0) break;
+  }
+  k_report_solve<<<R.sgrid(), 128, 0, sm>>>(a, rep, tau_out);
+  const dim3 og((n + 31) / 32, (m + 31) / 32, B);
+  R.launched();
+  if (A) {
+    k_from_plane<<<og, dim3(32, 8), 0, sm>>>(A, a, L.oA, m, n, L.ldm, 2);
+    R.launched();
+  }
+  if (E) {
+    k_from_plane<<<og, dim3(32, 8), 0, sm>>>(E, a, L.oE, m, n, L.ldm, 2);
+    R.launched();
+  }
+  if (Y) {
+    k_from_plane<<<og, dim3(32, 8), 0, sm>>>(Y, a, L.oY, m, n, L.ldm, 2);
+    R.launched();
+  }
+  R.check("solve outputs");
   return R.st;
 }
 
