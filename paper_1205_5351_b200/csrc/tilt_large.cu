@@ -493,10 +493,12 @@ __global__ void __launch_bounds__(ENT) k_identity(Args a, size_t off) {
   }
 }
 
-// T <- 1.5 I - 0.5 T (Newton-Schulz, Z14)
+// T <- 1.5 I - 0.5 T (Newton-Schulz, Z14). Applied to every problem, also those whose inner loop has
+// ended: the batched GEMMs around it run for all of them, and skipping this step would turn their
+// V <- V (1.5 I - 0.5 V^T V) into V <- V (V^T V), which grows the column norms without bound over
+// the remaining iterations of the batch -- and V warm-starts the next outer iteration.
 __global__ void __launch_bounds__(ENT) k_ns_mid(Args a) {
   const int b = blockIdx.y;
-  if (state(a, b)->done) return;
   float* T = slot(a, b) + a.L.oT;
   const int ldn = a.L.ldn;
   FOR_ELEMS(a.L.vplane) {
