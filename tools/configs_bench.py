@@ -22,6 +22,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--configs", default="1,2,3,4,5")
 ap.add_argument("--cap", type=int, default=8192)
 ap.add_argument("--pyramid-warm", type=int, default=0, help="tilt_params.pyramid_warm (config 3; reading Z26)")
+ap.add_argument("--kernel-path", type=int, default=0, help="tilt_params.kernel_path (0 auto, 1 CTA, 3 multi-CTA)")
 a = ap.parse_args()
 for cid in [int(c) for c in a.configs.split(",")]:
     cfg = ts.CONFIGS[cid]
@@ -29,7 +30,8 @@ for cid in [int(c) for c in a.configs.split(",")]:
     b = bench.gen_shard(cid, 0, B)
     m, n, p = cfg.m, cfg.n, cfg.p
     s = T.TiltSolver(0, max_batch=B, max_m=m, max_n=n, max_p=p, max_image_elems=int(b["images"].size))
-    prm = T.default_params(win_h=m, win_w=n, pyramid_levels=cfg.pyramid_levels, pyramid_warm=a.pyramid_warm)
+    prm = T.default_params(win_h=m, win_w=n, pyramid_levels=cfg.pyramid_levels, pyramid_warm=a.pyramid_warm,
+                           kernel_path=a.kernel_path)
     imgs = torch.as_tensor(b["images"], device="cuda")
     args = (imgs, torch.as_tensor(b["patch_image"], device="cuda"), torch.as_tensor(b["boxes"], device="cuda"),
             torch.as_tensor(b["tau0"], device="cuda"), cfg.kind, prm)
@@ -44,7 +46,7 @@ for cid in [int(c) for c in a.configs.split(",")]:
     conv = int(np.sum(rep["status"] == T.CONVERGED))
     it = float(np.sum(rep["inner_iters"]))
     row = {"config": cid, "batch": B, "window": f"{m}x{n}", "p": p, "pyramid": cfg.pyramid_levels,
-           "pyramid_warm": a.pyramid_warm, "seconds": t,
+           "pyramid_warm": a.pyramid_warm, "kernel_path": a.kernel_path, "seconds": t,
            "converged_patches_per_s": conv / t, "converged_fraction": conv / B, "inner_iters_per_s": it / t,
            "mean_inner_iters": it / B, "sweeps_per_svt": float(np.sum(rep["jacobi_sweeps"]) / max(it, 1)),
            "model_tflops": bench.flops_per_launch(rep, m, n, p, int(prm.ns_period)) / t / 1e12}
