@@ -519,7 +519,7 @@ static tilt_status solve_level(tilt_handle* h, const float* images, int32_t n_im
       return TILT_E_ARG;
     }
     return tilt::lp::solve(lp_ctx(h), images, n_images, H, W, patch_image, boxes, tau0, B, m, n, kind, to_dev(prm),
-                           tau_out, A_out, E_out, Y_out, rep);
+                           tau_out, A_out, E_out, Y_out, rep, rep_prev);
   }
   const bool rj_ok = tilt::rjh::fits(m, n);
   if (prm->kernel_path == 2 && !rj_ok) {

@@ -1523,7 +1523,7 @@ __global__ void k_dtau(Args a, int it, int n_outer) {
   if (!st->outer_done) atomicAdd(a.counter, 1);
 }
 
-__global__ void k_report_solve(Args a, tilt_report* rep, float* tau_out) {
+__global__ void k_report_solve(Args a, tilt_report* rep, float* tau_out, const tilt_report* rep_prev) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= a.B) return;
   const St* st = state(a, b);
@@ -1551,6 +1551,15 @@ __global__ void k_report_solve(Args a, tilt_report* rep, float* tau_out) {
   r.jacobi_rotations = st->rotations;
   r.kernel_path = 3;
   r.svd_warm_steps = st->warm_steps;
+  if (rep_prev) {  // pyramid: the coarse level's counters (as solve_patch)
+    const tilt_report& pr = rep_prev[b];
+    r.outer_iters += pr.outer_iters;
+    r.inner_iters += pr.inner_iters;
+    r.jacobi_sweeps += pr.jacobi_sweeps;
+    r.aux_sweeps += pr.aux_sweeps;
+    r.sweep_cap_hits += pr.sweep_cap_hits;
+    r.jacobi_rotations += pr.jacobi_rotations;
+  }
   rep[b] = r;
 }
 
@@ -2019,7 +2028,7 @@ tilt_status inner(Ctx& ctx, const float* D, const float* J, const float* Q, int 
 
 tilt_status solve(Ctx& ctx, const float* images, int n_images, int H, int W, const int32_t* patch_image,
                   const int32_t* boxes, const float* tau0, int B, int m, int n, int kind, const DevParams& P,
-                  float* tau_out, float* A, float* E, float* Y, tilt_report* rep) {
+                  float* tau_out, float* A, float* E, float* Y, tilt_report* rep, const tilt_report* rep_prev) {
   const int p = kind == TILT_HOMOGRAPHY ? 8 : 6;
   if (P.inner_solver != 0) return TILT_E_ARG;  // the ADM's own dtau step is the CTA kernels' (k_solve)
   tilt_status s0 = ensure(ctx, ws_need(B, m, n, p, P.svd_mode == 1), B);
@@ -2068,7 +2077,7 @@ tilt_status solve(Ctx& ctx, const float* images, int n_images, int H, int W, con
     if (act < 0) return R.st;
     if (act == 0) break;
   }
-  k_report_solve<<<R.sgrid(), 128, 0, sm>>>(a, rep, tau_out);
+  k_report_solve<<<R.sgrid(), 128, 0, sm>>>(a, rep, tau_out, rep_prev);
   const dim3 og((n + 31) / 32, (m + 31) / 32, B);
   R.launched();
   if (A) {

@@ -297,3 +297,21 @@ def test_solve_multi_cta_fixed_count(solver_img, T, cfg_id, m, K, outer):
         bar = 1e-4 if outer == 1 else 1e-3
         assert ra < bar and re < bar, (cfg_id, k, ra, re)
         assert rep["objective"][k] == pytest.approx(refs[k]["objective"], rel=bar)
+
+
+def test_pyramid_large_window_fixed_count(solver_img, T):
+    """2-level pyramid (Z18) on a 300x300 window: the 150x150 coarse level and the fine level both run
+    on the multi-CTA path (auto above 128); fixed counts with the oracle's tilt_pyramid."""
+    cfg = ts.SynthConfig(98, 1, 300, 300, O.AFFINE, 2, 3, 8.0, 0.1, 0.0, 0.05, 0.0, 2)
+    b = ts.gen_batch(cfg, 0, 1)
+    K = 10
+    prm_o = O.Params(fixed_inner_iters=K, fixed_outer_iters=1, max_inner=K, max_outer=1)
+    ref = O.tilt_pyramid(b["images"][0], b["boxes"][0], b["tau0"][0], cfg.kind, prm_o, levels=2)
+    prm = T.default_params(fixed_inner_iters=K, fixed_outer_iters=1, max_inner=K, max_outer=1, pyramid_levels=2)
+    out = solver_img.solve(b["images"], b["patch_image"], b["boxes"], b["tau0"], cfg.kind, prm)
+    rep = T.reports_to_numpy(out["rep"])
+    assert rep["kernel_path"][0] == 3
+    assert rep["outer_iters"][0] == 2 and rep["inner_iters"][0] == 2 * K  # coarse + fine counters
+    assert np.max(np.abs(out["tau"][0].double().cpu().numpy() - ref["tau"])) < 1e-3
+    a = out["A"][0].double().cpu().numpy()
+    assert np.linalg.norm(a - ref["A"]) / np.linalg.norm(ref["A"]) < 1e-3
