@@ -315,3 +315,29 @@ def test_pyramid_large_window_fixed_count(solver_img, T):
     assert np.max(np.abs(out["tau"][0].double().cpu().numpy() - ref["tau"])) < 1e-3
     a = out["A"][0].double().cpu().numpy()
     assert np.linalg.norm(a - ref["A"]) / np.linalg.norm(ref["A"]) < 1e-3
+
+
+# ---------------------------------------------------------------------------------------------
+# Edge cases of the multi-CTA path
+# ---------------------------------------------------------------------------------------------
+def test_multi_cta_edge_cases(solver, T):
+    # zero matrix: A = 0, sigma = 0, no NaN
+    out = solver.svt(np.zeros((2, 300, 40), np.float32), [0.1, 0.0], path=3)
+    assert float(out["A"].abs().max()) == 0.0 and float(out["sigma"].abs().max()) == 0.0
+    # a single block of columns (n < 16) and a tall matrix
+    rng = np.random.default_rng(3)
+    M = rng.normal(size=(2, 300, 5))
+    o = solver.svt(M.astype(np.float32), [0.5, 0.0], path=3)
+    for k, eps in enumerate([0.5, 0.0]):
+        ref, _ = O.svt(M[k].astype(np.float32).astype(np.float64), eps)
+        assert np.linalg.norm(o["A"][k].double().cpu().numpy() - ref) < 3e-5 * np.linalg.norm(M[k])
+    # rank-deficient J: the Gram is singular -> per-problem SINGULAR_GRAM, zero outputs, others solve
+    insts = [ts.table1_instance(300, 6, s) for s in range(2)]
+    D = np.stack([i["D"] for i in insts]).astype(np.float32)
+    J = np.stack([i["J"] for i in insts]).astype(np.float32)
+    J[1, 5] = J[1, 4]  # two equal columns
+    out = solver.inner(D, J, params=T.default_params(kernel_path=3, fixed_inner_iters=3, max_inner=3))
+    rep = out["rep"]
+    assert rep["status"][1] == T.SINGULAR_GRAM and rep["status"][0] != T.SINGULAR_GRAM
+    assert float(out["A"][1].abs().max()) == 0.0 and float(out["A"][0].abs().max()) > 0.0
+    assert np.all(np.isfinite(out["A"][0].cpu().numpy()))
