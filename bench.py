@@ -280,6 +280,15 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
         traffic = prof.get("k_solve_dram_bytes_per_launch")
     except Exception:
         pass
+    binding = None  # the resource ncu shows binding k_solve (shared-memory wavefronts, not the FMA pipe)
+    try:
+        met = json.load(open(os.path.join(ROOT, "profiles", "r01", "k_solve_s64_full_metrics.json")))
+        binding = {"resource": "shared-memory wavefronts (LSU pipe)",
+                   "frac": float(met["l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed"][0]) / 100,
+                   "fma_pipe_frac": float(met["sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active"][0]) / 100,
+                   "source": "ncu --set full of k_solve (1184 x 30 iterations), profiles/r01/k_solve_s64_full_metrics.json"}
+    except Exception:
+        pass
     line = {
         "metric": "rectified patches/s (converged)", "value": value, "unit": "patches/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * elapsed / args.steps,
@@ -295,7 +304,7 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
                      "unit": "TFLOP/s", "frac": achieved / FP32_PEAK_TFLOPS, "traffic": traffic,
                      "peak_note": "FP32 FMA: 148 SMs x 128 lanes x 2 x 1.965 GHz (sm_max_mhz of MEASURED_PEAKS.json); "
                                   "achieved = SURVEY §8(d) model flops from the device counters / event time",
-                     "flops_per_launch": flops},
+                     "flops_per_launch": flops, "binding": binding},
         "gpu_launches": int(launches),
         "clocks": clk,
     }
