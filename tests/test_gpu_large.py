@@ -341,3 +341,27 @@ def test_multi_cta_edge_cases(solver, T):
     assert rep["status"][1] == T.SINGULAR_GRAM and rep["status"][0] != T.SINGULAR_GRAM
     assert float(out["A"][1].abs().max()) == 0.0 and float(out["A"][0].abs().max()) > 0.0
     assert np.all(np.isfinite(out["A"][0].cpu().numpy()))
+
+
+def test_multi_cta_argument_errors(solver, T):
+    """Call-level validation of the multi-CTA entries (TILT_E_ARG, no launch) and B = 0."""
+    import ctypes
+    from paper_1205_5351_b200 import _abi
+    lib = _abi.lib
+    prm = T.default_params(kernel_path=3, svd_mode=1)
+    null = ctypes.c_void_p()
+    # svd_mode 1 needs m >= n
+    st = lib.tilt_inner_batch(solver._h, null, null, null, 0, 1, 100, 200, 6, ctypes.byref(prm), null, null, null, null)
+    assert st == _abi.TILT_E_ARG
+    # SVDWS is LADMAP's: with the ADM inner solver the parameters are rejected
+    prm2 = T.default_params(kernel_path=3, svd_mode=1, inner_solver=1)
+    st = lib.tilt_inner_batch(solver._h, null, null, null, 0, 1, 200, 200, 6, ctypes.byref(prm2), null, null, null, null)
+    assert st == _abi.TILT_E_ARG
+    # windows beyond the handle's max_m / max_n
+    st = lib.tilt_inner_batch(solver._h, null, null, null, 0, 1, 2000, 200, 6, ctypes.byref(T.default_params()), null,
+                              null, null, null)
+    assert st == _abi.TILT_E_ARG
+    # B = 0 is a no-op
+    st = lib.tilt_inner_batch(solver._h, null, null, null, 0, 0, 300, 300, 6, ctypes.byref(T.default_params()), null,
+                              null, null, null)
+    assert st == _abi.TILT_OK
