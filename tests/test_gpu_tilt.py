@@ -301,3 +301,18 @@ def test_fixed_count_parity_large_configs(solver_big, T, cfg_id):
         re = np.linalg.norm(e - refs[k]["E"]) / np.linalg.norm(refs[k]["E"])
         assert ra < 1e-4 and re < 1e-4, (cfg_id, k, ra, re)
         assert np.max(np.abs(out["tau"][k].double().cpu().numpy() - refs[k]["tau"])) < 1e-3
+
+
+def test_host_buffer_entry_matches_device_entry(solver, T):
+    """tilt_solve_batch_host (the end-to-end entry: host buffers, copies inside) gives the same bits
+    as tilt_solve_batch on device buffers (the persistent kernel is deterministic per patch)."""
+    cfg = ts.CONFIGS[2]
+    b = ts.gen_batch(cfg, 0, 8)
+    prm = T.default_params(fixed_inner_iters=10, fixed_outer_iters=2, max_inner=10, max_outer=2)
+    d = solver.solve(b["images"], b["patch_image"], b["boxes"], b["tau0"], cfg.kind, prm)
+    h = solver.solve_host(b["images"], b["patch_image"], b["boxes"], b["tau0"], cfg.kind, prm)
+    assert np.array_equal(h["tau"], d["tau"].cpu().numpy())
+    assert np.array_equal(h["A"], d["A"].cpu().numpy()) and np.array_equal(h["E"], d["E"].cpu().numpy())
+    rep_d = T.reports_to_numpy(d["rep"])
+    assert np.array_equal(h["rep"]["inner_iters"], rep_d["inner_iters"])
+    assert np.array_equal(h["rep"]["status"], rep_d["status"])
