@@ -78,3 +78,14 @@ def test_no_cpu_fallback_in_product(pkg):
             src = open(os.path.join(pdir, f)).read()
             assert "oracle" not in src.replace("# ", ""), f
             assert "np.linalg.svd" not in src, f
+
+
+def test_missing_library_fails_loudly():
+    """No CPU fallback: importing the package without its CUDA library raises instead of degrading."""
+    import subprocess
+    import sys
+    env = dict(os.environ, TILT_LIB="/nonexistent/libtilt.so")
+    r = subprocess.run([sys.executable, "-c", "import paper_1205_5351_b200"], cwd=ROOT, env=env,
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode != 0
+    assert "libtilt" in (r.stderr + r.stdout)

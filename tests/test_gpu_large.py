@@ -31,7 +31,8 @@ def solver(T):
     s.close()
 
 
-LARGE_SVT = [(50, 50), (100, 100), (130, 70), (70, 130), (300, 300), (257, 300), (600, 520), (1000, 1000)]
+LARGE_SVT = [(50, 50), (100, 100), (130, 70), (70, 130), (300, 300), (257, 300), (600, 520), (777, 333), (1000, 1000),
+             (1024, 1024)]
 
 
 @pytest.mark.parametrize("m,n", LARGE_SVT)
