@@ -1,3 +1,5 @@
+"""Config 1 (one 32x32 affine patch, BASELINE.json configs[0]) solve latency on the CTA-per-patch
+and warp-per-patch kernels. Usage: python tools/config1_latency.py"""
 import sys, os
 sys.path.insert(0, os.getcwd())
 import numpy as np, torch

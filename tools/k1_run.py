@@ -1,3 +1,5 @@
+"""K1 (warp/Jacobian) HBM roofline over the bench batch (config 2, 1024 patches), as bench.py
+measures it (cold L2 before each launch, median of 20). Usage: python tools/k1_run.py"""
 import sys, os
 sys.path.insert(0, os.getcwd())
 import bench, json, numpy as np, torch
