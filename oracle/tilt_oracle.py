@@ -737,3 +737,31 @@ def tilt_batch(images, patch_image, boxes, tau0, kind, prm: Params = Params(), l
     ctx = mp.get_context("fork")
     with ctx.Pool(min(n_workers, len(jobs))) as pool:
         return pool.map(_tilt_job, jobs)
+
+
+def tilt_oracle_solve_batch(images, n_images, H, W, patch_image, boxes, tau0, B, kind, prm: Params = Params(),
+                            n_threads=1, levels=1):
+    """The oracle twin of tilt_solve_batch: the same argument meaning on host fp64
+    arrays -- images [n_images][H][W], patch_image [B], boxes [B][4] = (x0, y0, w, h), tau0 [B][p] or
+    None (identity), kind AFFINE / HOMOGRAPHY -- plus n_threads worker processes. Returns (tau [B][p],
+    A [B][m][n], E [B][m][n], reports: list of dicts with status, stop_rule, outer_iters, inner_iters,
+    objective, rank, crit1, crit2, patch_norm). A patch without a state (window escape, singular Gram
+    or zero patch in its first outer iteration) gets zero A and E, as the C ABI."""
+    images = np.asarray(images, dtype=np.float64).reshape(n_images, H, W)
+    boxes = np.asarray(boxes, dtype=np.int64).reshape(B, 4)
+    p = 8 if kind == HOMOGRAPHY else 6
+    if tau0 is None:
+        t0 = np.zeros((B, p))
+        t0[:, 0] = 1.0
+        t0[:, 3] = 1.0
+    else:
+        t0 = np.asarray(tau0, dtype=np.float64).reshape(B, p)
+    res = tilt_batch(images, np.asarray(patch_image).reshape(B), boxes, t0, kind, prm, levels=levels,
+                     n_workers=n_threads)
+    m, n = (int(boxes[0, 3]), int(boxes[0, 2])) if B > 0 else (0, 0)
+    tau = np.stack([r["tau"] for r in res]) if B > 0 else np.zeros((0, p))
+    A = np.stack([r["A"] if r["A"] is not None else np.zeros((m, n)) for r in res]) if B > 0 else np.zeros((0, m, n))
+    E = np.stack([r["E"] if r["E"] is not None else np.zeros((m, n)) for r in res]) if B > 0 else np.zeros((0, m, n))
+    keys = ("status", "stop_rule", "outer_iters", "inner_iters", "objective", "rank", "crit1", "crit2", "patch_norm")
+    reps = [{k: r[k] for k in keys} for r in res]
+    return tau, A, E, reps

@@ -96,3 +96,20 @@ def test_pyramid_transfers_tau():
     df2 = O.downsample2x(df)
     corr = np.corrcoef(df2.reshape(-1), dc.reshape(-1))[0, 1]
     assert corr > 0.995
+
+
+def test_oracle_twin_matches_per_patch_tilt():
+    """tilt_oracle_solve_batch (SURVEY.md §8(b) oracle twin) = tilt() per patch, incl. the no-state case."""
+    cfg = ts.CONFIGS[1]
+    b = ts.gen_batch(cfg, 0, 2)
+    prm = O.Params(fixed_inner_iters=5, fixed_outer_iters=1, max_inner=5, max_outer=1)
+    nimg, H, W = b["images"].shape
+    boxes = b["boxes"].copy()
+    boxes[1, 0] = W - 5  # the second window leaves the image: WINDOW_ESCAPE, zero A and E
+    tau, A, E, reps = O.tilt_oracle_solve_batch(b["images"], nimg, H, W, b["patch_image"], boxes, b["tau0"], 2,
+                                                cfg.kind, prm, n_threads=1)
+    r0 = O.tilt(b["images"][b["patch_image"][0]], boxes[0], b["tau0"][0], cfg.kind, prm)
+    np.testing.assert_array_equal(tau[0], r0["tau"])
+    np.testing.assert_array_equal(A[0], r0["A"])
+    assert reps[0]["inner_iters"] == 5
+    assert reps[1]["status"] == O.WINDOW_ESCAPE and not A[1].any() and not E[1].any()
