@@ -240,9 +240,10 @@ tilt_status tilt_project_batch(tilt_handle* h, const float* J, const float* Q, i
  * Uses prm (lambda, mu0_scale, mu_max_ratio, rho0, eps1, eps2, max_inner, fixed_inner_iters,
  * rho_replay [B][max_inner], trace [B][max_inner][4], Jacobi controls). Outputs A, E, Y [B][m][n]
  * (Y may be NULL) and rep [B] (inner_iters, jacobi_sweeps, objective, crit1, crit2, rank...).
- * m, n <= 1024: windows above 256 (or prm->kernel_path = 3) run on the multi-CTA path, which
- * allocates its workspace on first use (B x ~(10 + p) m n floats) and synchronises the handle's
- * stream once per Jacobi sweep and per LADMAP iteration (it reads an active-problem counter). */
+ * m, n <= 1024: windows above 128 (or prm->kernel_path = 3) run on the multi-CTA path, which
+ * synchronises the handle's stream once per Jacobi sweep and per LADMAP iteration (it reads an
+ * active-problem counter). Its workspace (B x ~(10 + p) m n floats, more with svd_mode 1) is made
+ * by tilt_create when max_m or max_n exceeds 128, else on first use. */
 tilt_status tilt_inner_batch(tilt_handle* h, const float* D, const float* J, const float* Q,
                              int32_t l, int32_t B, int32_t m, int32_t n, int32_t p,
                              const tilt_params* prm, float* A, float* E, float* Y,

@@ -438,6 +438,17 @@ tilt_status tilt_create(tilt_handle** out, const tilt_create_opts* o) {
     if ((e = cudaMalloc(&h->ws, h->ws_floats * sizeof(float))) != cudaSuccess) return fail(e, "cudaMalloc(ws)");
   }
   if ((e = cudaMalloc(&h->counter, 64 * sizeof(int))) != cudaSuccess) return fail(e, "cudaMalloc(counter)");
+  // windows above 128 x 128 take the multi-CTA path by default: its workspace and cuBLAS handle are
+  // made here, so the solve entries allocate nothing (SVDWS or a forced kernel_path = 3 at smaller
+  // sizes still allocate on first use, as tilt.h states)
+  if ((h->max_m > 128 || h->max_n > 128) && h->max_batch > 0) {
+    const tilt_status ls = tilt::lp::ensure(lp_ctx(h), tilt::lp::ws_need(h->max_batch, h->max_m, h->max_n, h->max_p),
+                                            h->max_batch);
+    if (ls != TILT_OK) {
+      tilt_destroy(h);
+      return ls;
+    }
+  }
   if (h->max_image_elems > 0) {
     const size_t nb = (size_t)h->max_batch;
     if ((e = cudaMalloc(&h->coarse_images, (size_t)h->max_image_elems / 4 * sizeof(float) + 64)) != cudaSuccess)
