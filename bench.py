@@ -233,9 +233,10 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     stats = torch.tensor([elapsed, float(conv), float(inner), flops, float(np.mean(kern_ms))], dtype=torch.float64,
                          device=dev)
     if world > 1:
-        tmax = stats[0:1].clone()
+        cdev = stats.device if dist.get_backend() == "nccl" else "cpu"  # gloo smoke test: host tensors
+        tmax = stats[0:1].clone().to(cdev)
         dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
-        tot = stats[1:4].clone()
+        tot = stats[1:4].clone().to(cdev)
         dist.all_reduce(tot, op=dist.ReduceOp.SUM)
         elapsed = float(tmax.item())
         conv_all, inner_all, flops_all = (float(x) for x in tot.tolist())
@@ -248,10 +249,11 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
             dist.barrier()
         e2e_line = e2e(solver, batch, kind, prm, args)
         if world > 1:
-            red = torch.tensor([e2e_line["_seconds"]], dtype=torch.float64, device=dev)
+            cdev = dev if dist.get_backend() == "nccl" else "cpu"
+            red = torch.tensor([e2e_line["_seconds"]], dtype=torch.float64, device=cdev)
             dist.all_reduce(red, op=dist.ReduceOp.MAX)
             tot = torch.tensor([float(e2e_line["_conv"]), float(e2e_line["h2d_bytes_per_step"]),
-                                float(e2e_line["d2h_bytes_per_step"])], dtype=torch.float64, device=dev)
+                                float(e2e_line["d2h_bytes_per_step"])], dtype=torch.float64, device=cdev)
             dist.all_reduce(tot, op=dist.ReduceOp.SUM)
             e2e_line["_seconds"] = float(red.item())
             e2e_line["_conv"], h2d_all, d2h_all = (float(x) for x in tot.tolist())
@@ -264,7 +266,8 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     if world > 1:
         t0 = time.perf_counter()
         for key in ("tau", "rep", "A", "E"):
-            D.gather_to_root(out[key], B * world, world, rank)
+            x = out[key] if dist.get_backend() == "nccl" else out[key].cpu()
+            D.gather_to_root(x, B * world, world, rank)
         torch.cuda.synchronize()
         gather_ms = 1e3 * (time.perf_counter() - t0)
     if rank != 0:
@@ -414,6 +417,9 @@ def main():
     ap.add_argument("--ref-warmup", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-k1", action="store_true")
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
+                    help="process-group backend (gloo: a smoke test of the N > 1 code path on fewer GPUs "
+                         "than ranks; never a measurement)")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -424,8 +430,13 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if args.backend == "gloo":  # smoke test: ranks may share a GPU
+            local_rank = local_rank % max(1, torch.cuda.device_count())
+            torch.cuda.set_device(local_rank)
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local_rank)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
         run_ours(args, rank, world, local_rank)
     finally:
