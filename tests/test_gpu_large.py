@@ -300,10 +300,12 @@ def test_solve_multi_cta_fixed_count(solver_img, T, cfg_id, m, K, outer):
         assert rep["objective"][k] == pytest.approx(refs[k]["objective"], rel=bar)
 
 
-def test_pyramid_large_window_fixed_count(solver_img, T):
-    """2-level pyramid (Z18) on a 300x300 window: the 150x150 coarse level and the fine level both run
-    on the multi-CTA path (auto above 128); fixed counts with the oracle's tilt_pyramid."""
-    cfg = ts.SynthConfig(98, 1, 300, 300, O.AFFINE, 2, 3, 8.0, 0.1, 0.0, 0.05, 0.0, 2)
+@pytest.mark.parametrize("m", [300, 200])
+def test_pyramid_large_window_fixed_count(solver_img, T, m):
+    """2-level pyramid (Z18): at 300x300 both levels (150, 300) run on the multi-CTA path (auto above
+    128); at 200x200 the coarse 100x100 level runs on the CTA kernel and the fine level on the
+    multi-CTA path. Fixed counts against the oracle's tilt_pyramid."""
+    cfg = ts.SynthConfig(98, 1, m, m, O.AFFINE, 2, 3, 8.0, 0.1, 0.0, 0.05, 0.0, 2)
     b = ts.gen_batch(cfg, 0, 1)
     K = 10
     prm_o = O.Params(fixed_inner_iters=K, fixed_outer_iters=1, max_inner=K, max_outer=1)
