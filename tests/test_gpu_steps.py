@@ -59,6 +59,25 @@ def test_warp_jacobian_parity(solver, kind):
             assert err < 1e-5, (k, q, err)
 
 
+def test_warp_full_batch_sampled(T):
+    """K1 at the bench's full size and launch configuration (config 2: 1024 patches at tau0, the
+    roofline_k1 call of bench.py), sampled patches against the oracle's warp."""
+    cfg = ts.CONFIGS[2]
+    b = ts.gen_batch(cfg, 0, cfg.batch)
+    s = T.TiltSolver(0, max_batch=cfg.batch, max_m=50, max_n=50, max_p=8, max_image_elems=int(b["images"].size))
+    out = s.warp(b["images"], b["patch_image"], b["boxes"], b["tau0"], cfg.kind)
+    dh = out["Dhat"].double().cpu().numpy()
+    J = out["J"].double().cpu().numpy()
+    assert np.all(out["status"].cpu().numpy() == O.CONVERGED)
+    for k in (0, 511, 1023):
+        d, jraw, st = O.warp(b["images"][k], b["boxes"][k], b["tau0"][k].astype(np.float64), cfg.kind)
+        rdh, rj, nd = O.normalise(d, jraw)
+        np.testing.assert_allclose(dh[k], rdh, atol=2e-6 * np.abs(rdh).max())
+        for q in range(cfg.p):
+            assert np.linalg.norm(J[k, q] - rj[q]) < 1e-5 * np.linalg.norm(rj[q]), (k, q)
+    s.close()
+
+
 def test_warp_escape_and_zero(solver):
     cfg = ts.CONFIGS[1]
     b = ts.gen_batch(cfg, 0, 2)
