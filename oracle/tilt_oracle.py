@@ -401,12 +401,13 @@ class SvdWarm:
     """The SVD warm start of LADMAP+SVDWS (Algorithm 2): keeps the previous (approximate) SVD and
     M_{k-1}; S_eps(M_k) uses one ``svd_warm_start`` step when ||M_k - M_{k-1}||_F < eps_svd, else a
     full SVD ("Else do full svd"). m < n is handled on the transpose (S_eps(M^T) = S_eps(M)^T).
-    Reading Z27: a step without a descent model (f''(0) <= 0, t* = 0) or whose Cayley generators are
-    not small, ||(t*/2) P_U||_F >= 0.5 or ||(t*/2) P_V||_F >= 0.5, is rejected (full SVD instead) --
-    the GPU solves the Cayley systems by Richardson iteration, which needs them below 1. ``decisions`` logs 1 (warm step) / 0 (full SVD)
-    per call."""
-
-    CAYLEY_MAX = 0.5
+    Reading Z27: a gated step is rejected (full SVD instead) only when f''(0) <= 0. Eq. ft
+     replaces f by its quadratic model f(0) + f'(0) t + f''(0) t^2 / 2, whose stationary
+    point t~* = -f'(0)/f''(0) is its minimiser only when f''(0) > 0 (for f''(0) <= 0 the model has no
+    minimiser and the paper's bound ||U(t~*)Sigma(t~*)V(t~*)^T - M_k|| <= ||M_{k-1} - M_k||, P:921-935,
+    has nothing to stand on). Any other t* is taken as printed: (I + t/2 P) is invertible for every
+    skew P and the Cayley curve is feasible for every t, so no step-size rule applies.
+    ``decisions`` logs 1 (warm step) / 0 (full SVD) per call."""
 
     def __init__(self, eps_svd):
         self.eps_svd = eps_svd
@@ -423,10 +424,7 @@ class SvdWarm:
         step = None
         if self.prev is not None and np.linalg.norm(x - self.m_prev) < self.eps_svd:
             u, sig, v, t = svd_warm_start(x, *self.prev)
-            w = (self.prev[0] * self.prev[1]) @ self.prev[2].T
-            p_u = w @ x.T - x @ w.T
-            p_v = w.T @ x - x.T @ w
-            if t != 0.0 and max(np.linalg.norm(0.5 * t * p_u), np.linalg.norm(0.5 * t * p_v)) < self.CAYLEY_MAX:
+            if t != 0.0:
                 step = (u, sig, v)
         if step is not None:
             u, sig, v = step
