@@ -62,7 +62,9 @@ typedef enum {
   TILT_PATCH_WINDOW_ESCAPE = 2, /* a bilinear 4-tap stencil left the image (reading Z2) */
   TILT_PATCH_SINGULAR_GRAM = 3, /* Cholesky of J^TJ + Q^TQ failed (J not full rank) */
   TILT_PATCH_ZERO_PATCH = 4,    /* ||D o tau||_F = 0 (normalisation of Alg. 1 Step 1 undefined) */
-  TILT_PATCH_DIVERGED = 5       /* NaN/Inf or objective > 1e12 */
+  TILT_PATCH_DIVERGED = 5,      /* NaN/Inf or objective > 1e12 */
+  TILT_PATCH_BAD_BOX = 6        /* the patch's box is not win_w x win_h (every box of a call must have
+                                   the call's window size); the patch is not solved, tau_out = tau0 */
 } tilt_patch_status;
 
 typedef enum { TILT_CONSTRAINTS_NONE = 0, TILT_CONSTRAINTS_CENTER_AREA = 1 } tilt_constraint_mode;
@@ -92,8 +94,13 @@ typedef struct {
   const uint8_t* rho_replay;  /* device [B][max_outer][max_inner] or NULL (Z21): bit 0 = rho decision
                                  (1: rho0), bit 1 = end the inner loop after this iteration */
   float* trace;               /* device [B][max_outer][max_inner][4] (mu, crit1, crit2, rho) or NULL */
-  /* window size of the call (all boxes share it). 0: read back from boxes[0] with a stream sync;
-   * > 0: taken as given (no host sync; the call is then graph-capturable). */
+  /* window size of the call (all boxes share it; a patch whose box differs is reported
+   * TILT_PATCH_BAD_BOX and not solved). 0: read back from boxes[0] with a stream sync;
+   * > 0: taken as given. Host syncs: none on the CTA-per-patch kernels when win_h, win_w > 0 (the
+   * call is then graph-capturable); the multi-CTA path (kernel_path 3, windows above 128 x 128 on
+   * auto, svd_mode 1) drives its loops from the host and synchronises the stream to read its
+   * active-problem counter (once per Jacobi sweep and per LADMAP / outer iteration), so it returns
+   * TILT_E_UNSUPPORTED on a capturing stream; the same holds for win_h/win_w = 0. */
   int32_t win_h, win_w;
   /* kernel family: 0 = auto (the CTA-per-patch kernels up to 128 x 128, the multi-CTA path above:
    * at 200 x 200 it is 2.4x faster; the ADM inner entry stays on the CTA kernels up to 256),

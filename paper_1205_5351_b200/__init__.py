@@ -6,7 +6,7 @@ package is the thin binding; ``dist`` adds the multi-GPU sharding. Importing it 
 the CUDA library has not been built.
 """
 from ._abi import (AFFINE, HOMOGRAPHY, CONVERGED, MAX_OUTER, WINDOW_ESCAPE, SINGULAR_GRAM, ZERO_PATCH,  # noqa: F401
-                   DIVERGED, CONSTRAINTS_NONE, CONSTRAINTS_CENTER_AREA, TiltError, TiltParams, default_params,
+                   DIVERGED, BAD_BOX, CONSTRAINTS_NONE, CONSTRAINTS_CENTER_AREA, TiltError, TiltParams, default_params,
                    lib, LIB_PATH, EXPORTS)
 from .solver import TiltSolver, REPORT_DTYPE, reports_to_numpy, p_of  # noqa: F401
 

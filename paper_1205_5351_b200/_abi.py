@@ -14,7 +14,7 @@ LIB_PATH = os.environ.get("TILT_LIB") or os.path.join(_HERE, "libtilt.so")
 
 TILT_OK, TILT_E_ARG, TILT_E_CUDA, TILT_E_OOM, TILT_E_UNSUPPORTED = 0, 1, 2, 3, 4
 AFFINE, HOMOGRAPHY = 0, 1
-CONVERGED, MAX_OUTER, WINDOW_ESCAPE, SINGULAR_GRAM, ZERO_PATCH, DIVERGED = range(6)
+CONVERGED, MAX_OUTER, WINDOW_ESCAPE, SINGULAR_GRAM, ZERO_PATCH, DIVERGED, BAD_BOX = range(7)
 CONSTRAINTS_NONE, CONSTRAINTS_CENTER_AREA = 0, 1
 
 

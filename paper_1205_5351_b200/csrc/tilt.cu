@@ -71,6 +71,7 @@ struct tilt_handle {
   int svt_path = 0;  // tilt_svt_batch kernel family (tilt_set_svt_path): 0/1 CTA-per-patch, 2 warp-per-patch,
                      // 3 multi-CTA
   tilt::lp::Ctx lp;  // multi-CTA path for large windows (workspace on first use)
+  size_t lp_budget = 0;  // bytes of multi-CTA workspace (batches above it run in chunks)
 };
 
 namespace {
@@ -386,6 +387,15 @@ tilt_status tilt_destroy(tilt_handle* h) {
   return TILT_OK;
 }
 
+// the multi-CTA path's batch chunk: its workspace is B x (a few planes + n x n buffers) per problem,
+// so a handle sized for many small patches runs large windows in chunks within lp_budget bytes
+static int lp_chunk(tilt_handle* h, int B, int m, int n, int p, bool svdws) {
+  const size_t per = tilt::lp::ws_need(1, m, n, p, svdws) * sizeof(float);
+  size_t c = per > 0 ? h->lp_budget / per : (size_t)B;
+  if (c < 1) c = 1;
+  return c < (size_t)B ? (int)c : B;
+}
+
 tilt_status tilt_create(tilt_handle** out, const tilt_create_opts* o) {
   if (!out || !o) return TILT_E_ARG;
   *out = nullptr;
@@ -441,9 +451,14 @@ tilt_status tilt_create(tilt_handle** out, const tilt_create_opts* o) {
   // windows above 128 x 128 take the multi-CTA path by default: its workspace and cuBLAS handle are
   // made here, so the solve entries allocate nothing (SVDWS or a forced kernel_path = 3 at smaller
   // sizes still allocate on first use, as tilt.h states)
+  {
+    size_t fr = 0, tot = 0;
+    if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) fr = (size_t)8 << 30;
+    h->lp_budget = fr / 2 < ((size_t)24 << 30) ? fr / 2 : ((size_t)24 << 30);
+  }
   if ((h->max_m > 128 || h->max_n > 128) && h->max_batch > 0) {
-    const tilt_status ls = tilt::lp::ensure(lp_ctx(h), tilt::lp::ws_need(h->max_batch, h->max_m, h->max_n, h->max_p),
-                                            h->max_batch);
+    const int ch = lp_chunk(h, h->max_batch, h->max_m, h->max_n, h->max_p, false);
+    const tilt_status ls = tilt::lp::ensure(lp_ctx(h), tilt::lp::ws_need(ch, h->max_m, h->max_n, h->max_p), ch);
     if (ls != TILT_OK) {
       tilt_destroy(h);
       return ls;
@@ -484,6 +499,11 @@ tilt_status tilt_set_svt_path(tilt_handle* h, int32_t path) {
   if (!h || path < 0 || path > 3) return TILT_E_ARG;
   h->svt_path = path;
   return TILT_OK;
+}
+
+static bool capturing(cudaStream_t s) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  return cudaStreamIsCapturing(s, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone;
 }
 
 static tilt_status solve_level(tilt_handle* h, const float* images, int32_t n_images, int32_t H, int32_t W,
@@ -529,8 +549,28 @@ static tilt_status solve_level(tilt_handle* h, const float* images, int32_t n_im
       g_last_error = "multi-CTA tilt_solve_batch: LADMAP only (svd_mode 1 needs m >= n)";
       return TILT_E_ARG;
     }
-    return tilt::lp::solve(lp_ctx(h), images, n_images, H, W, patch_image, boxes, tau0, B, m, n, kind, to_dev(prm),
-                           tau_out, A_out, E_out, Y_out, rep, rep_prev);
+    if (capturing(h->stream)) {
+      g_last_error = "the multi-CTA path synchronises its stream: not allowed while capturing";
+      return TILT_E_UNSUPPORTED;
+    }
+    const int p = a.p;
+    const int ch = lp_chunk(h, B, m, n, p, prm->svd_mode == 1);
+    const size_t mn = (size_t)m * n, cn = (size_t)B * (m / 2) * (n / 2), cmn = (size_t)(m / 2) * (n / 2);
+    for (int b0 = 0; b0 < B; b0 += ch) {  // bounded workspace: the batch in chunks
+      const int nb = B - b0 < ch ? B - b0 : ch;
+      tilt::DevParams P = a.P;
+      const size_t rows = (size_t)b0 * P.max_outer * P.max_inner;
+      if (P.rho_replay) P.rho_replay += rows;
+      if (P.trace) P.trace += rows * 4;
+      const tilt_status st = tilt::lp::solve(
+          lp_ctx(h), images, n_images, H, W, patch_image + b0, boxes + 4 * (size_t)b0, tau0 ? tau0 + (size_t)b0 * p : nullptr,
+          nb, m, n, kind, P, tau_out + (size_t)b0 * p, A_out ? A_out + b0 * mn : nullptr, E_out ? E_out + b0 * mn : nullptr,
+          Y_out ? Y_out + b0 * mn : nullptr, rep ? rep + b0 : nullptr, rep_prev ? rep_prev + b0 : nullptr,
+          warm_aey ? warm_aey + b0 * cmn : nullptr, warm_aey ? warm_aey + cn + b0 * cmn : nullptr,
+          warm_aey ? warm_aey + 2 * cn + b0 * cmn : nullptr, warm_rep ? warm_rep + b0 : nullptr);
+      if (st != TILT_OK) return st;
+    }
+    return TILT_OK;
   }
   const bool rj_ok = tilt::rjh::fits(m, n);
   if (prm->kernel_path == 2 && !rj_ok) {
@@ -544,6 +584,10 @@ static tilt_status solve_level(tilt_handle* h, const float* images, int32_t n_im
 // All boxes of one call must share (w, h): read from the caller's box array? The boxes live on
 // the device, so the window size is passed through the first box copied to the host.
 static tilt_status first_box(tilt_handle* h, const int32_t* boxes, int* m, int* n) {
+  if (capturing(h->stream)) {
+    g_last_error = "win_h/win_w = 0 reads boxes[0] with a host sync: not allowed on a capturing stream";
+    return TILT_E_UNSUPPORTED;
+  }
   int bx[4];
   TILT_CUDA(cudaMemcpyAsync(bx, boxes, sizeof(bx), cudaMemcpyDeviceToHost, h->stream));
   TILT_CUDA(cudaStreamSynchronize(h->stream));
@@ -706,8 +750,22 @@ tilt_status tilt_svt_batch(tilt_handle* h, const float* M, int32_t B, int32_t m,
   a.sweeps = sweeps;
   a.tol = default_jacobi_tol(m);
   a.max_sweeps = 20;
-  if (h->svt_path == 3 || m > 256 || n > 256)
-    return tilt::lp::svt(lp_ctx(h), M, B, m, n, eps, V_io, A, sigma, sweeps, a.tol, a.max_sweeps);
+  if (h->svt_path == 3 || m > 256 || n > 256) {
+    if (capturing(h->stream)) {
+      g_last_error = "the multi-CTA path synchronises its stream: not allowed while capturing";
+      return TILT_E_UNSUPPORTED;
+    }
+    const int ch = lp_chunk(h, B, m, n, 1, false);
+    for (int b0 = 0; b0 < B; b0 += ch) {  // bounded workspace: the batch in chunks
+      const int nb = B - b0 < ch ? B - b0 : ch;
+      const size_t mn = (size_t)m * n, nn = (size_t)n * n;
+      const tilt_status st = tilt::lp::svt(lp_ctx(h), M + b0 * mn, nb, m, n, eps + b0, V_io ? V_io + b0 * nn : nullptr,
+                                           A + b0 * mn, sigma ? sigma + (size_t)b0 * n : nullptr,
+                                           sweeps ? sweeps + b0 : nullptr, a.tol, a.max_sweeps);
+      if (st != TILT_OK) return st;
+    }
+    return TILT_OK;
+  }
   if (tilt::rjh::fits(m, n) && h->svt_path == 2) return tilt::rjh::svt(h->num_sms, h->ws, h->ws_floats, h->stream, a, &h->launches, &g_last_error);
   return dispatch<SvtF>(size_class(m, n), h, a);
 }
@@ -761,7 +819,23 @@ tilt_status tilt_inner_batch(tilt_handle* h, const float* D, const float* J, con
   if (prm->kernel_path == 3 || m > 256 || n > 256 || prm->svd_mode == 1 ||
       (prm->kernel_path == 0 && prm->inner_solver == 0 && (m > 128 || n > 128))) {
     if (prm->svd_mode == 1 && m < n) return TILT_E_ARG;
-    return tilt::lp::inner(lp_ctx(h), D, J, Q, Q ? l : 0, B, m, n, p, a.P, A, E, Y, rep);
+    if (capturing(h->stream)) {
+      g_last_error = "the multi-CTA path synchronises its stream: not allowed while capturing";
+      return TILT_E_UNSUPPORTED;
+    }
+    const int ch = lp_chunk(h, B, m, n, p, prm->svd_mode == 1);
+    const size_t mn = (size_t)m * n;
+    for (int b0 = 0; b0 < B; b0 += ch) {  // bounded workspace: the batch in chunks
+      const int nb = B - b0 < ch ? B - b0 : ch;
+      tilt::DevParams P = a.P;
+      if (P.rho_replay) P.rho_replay += (size_t)b0 * P.max_inner;
+      if (P.trace) P.trace += (size_t)b0 * P.max_inner * 4;
+      const tilt_status st = tilt::lp::inner(lp_ctx(h), D + b0 * mn, J + b0 * p * mn, Q ? Q + (size_t)b0 * l * p : nullptr,
+                                             Q ? l : 0, nb, m, n, p, P, A + b0 * mn, E + b0 * mn,
+                                             Y ? Y + b0 * mn : nullptr, rep ? rep + b0 : nullptr);
+      if (st != TILT_OK) return st;
+    }
+    return TILT_OK;
   }
   return dispatch<InnerF>(size_class(m, n), h, a);
 }

@@ -442,7 +442,9 @@ __device__ void solve_patch(const SolveArgs& a, Ctx<C>& cx, int b) {
   const float fnan = __int_as_float(0x7fc00000);
   float f = fnan, f_prev = fnan, crit1 = fnan, crit2 = fnan, dtau_inf = fnan, mu_last = fnan, nd = fnan;
   bool have_state = false, have_fprev = false;
-  const int n_outer = P.fixed_outer > 0 ? P.fixed_outer : P.max_outer;
+  const bool box_ok = bx[2] == n && bx[3] == m;  // all boxes of a call share the window size
+  if (!box_ok) status = TILT_PATCH_BAD_BOX;
+  const int n_outer = !box_ok ? 0 : P.fixed_outer > 0 ? P.fixed_outer : P.max_outer;
   for (int it = 0; it < n_outer; ++it) {
     // Step 1: D o tau and the Jacobian factors (fp64 per pixel, stored fp32), escape check
     const WarpGeom g = make_geom(bx, tau, a.kind);

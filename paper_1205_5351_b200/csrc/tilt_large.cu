@@ -141,6 +141,11 @@ struct Args {
   int n_images, H, W, kind;
   const int* patch_image;
   const int* boxes;
+  // pyramid warm start (reading Z26): the coarse level's A, E, Y [B][m/2][n/2] row-major and reports
+  const float* warm_A;
+  const float* warm_E;
+  const float* warm_Y;
+  const tilt_report* warm_rep;
 };
 
 __device__ __forceinline__ float* slot(const Args& a, int b) { return a.ws + (size_t)b * a.L.stride; }
@@ -1299,6 +1304,11 @@ __global__ void k_solve_init(Args a, const float* __restrict__ tau0) {
   st->status = TILT_PATCH_MAX_OUTER;
   st->stop_rule = 0;
   st->f = st->f_prev = st->dtau_inf = st->nd = __int_as_float(0x7fc00000);
+  if (a.boxes[4 * b + 2] != a.L.n || a.boxes[4 * b + 3] != a.L.m) {  // every box has the call's size
+    st->status = TILT_PATCH_BAD_BOX;
+    st->outer_done = 1;
+    st->done = 1;
+  }
 }
 
 // Step 1 (Z2, Z15, Z16), pass 1: d, gx, gy, gz per pixel (fp64 geometry, the CTA
@@ -1417,6 +1427,32 @@ __global__ void __launch_bounds__(ENT) k_cold(Args a) {
     w[a.L.oA + idx] = w[a.L.oD + idx];
     w[a.L.oE + idx] = 0.f;
     w[a.L.oY + idx] = 0.f;
+  }
+}
+
+// first inner loop of the pyramid's fine level (reading Z26): A, E, Y from the coarse level's state
+// replicated 2x2 and halved where the coarse level produced one (CONVERGED or MAX_OUTER), else cold;
+// Y is then projected (k_kty / k_projy) as every warm start
+__global__ void __launch_bounds__(ENT) k_cold_coarse(Args a) {
+  const int b = blockIdx.y;
+  if (state(a, b)->done) return;
+  float* w = slot(a, b);
+  const int st = a.warm_rep[b].status;
+  const bool from = st == TILT_PATCH_CONVERGED || st == TILT_PATCH_MAX_OUTER;
+  const int ldm = a.L.ldm, m = a.L.m, mc = a.L.m / 2, nc = a.L.n / 2;
+  const size_t o = (size_t)b * mc * nc;
+  FOR_ELEMS(a.L.plane) {
+    const int i = (int)(idx % ldm), j = (int)(idx / ldm);
+    if (from && i < m) {
+      const size_t c = o + (size_t)(i / 2) * nc + j / 2;
+      w[a.L.oA + idx] = 0.5f * a.warm_A[c];
+      w[a.L.oE + idx] = 0.5f * a.warm_E[c];
+      w[a.L.oY + idx] = 0.5f * a.warm_Y[c];
+    } else {
+      w[a.L.oA + idx] = w[a.L.oD + idx];
+      w[a.L.oE + idx] = 0.f;
+      w[a.L.oY + idx] = 0.f;
+    }
   }
 }
 
@@ -1807,6 +1843,8 @@ struct Run {
     a.images = nullptr;
     a.boxes = nullptr;
     a.patch_image = nullptr;
+    a.warm_A = a.warm_E = a.warm_Y = nullptr;
+    a.warm_rep = nullptr;
     a.tiny2 = 1e-14f;  // ||b_j|| <= 1e-7 ||M||_F: below fp32 resolution of the SVT output
     a.NB = (n + BW - 1) / BW;
     a.NBp = a.NB + (a.NB & 1);
@@ -1880,7 +1918,14 @@ static bool inner_core(Run& R, const DevParams& P, const float* Q, int l, int q_
   k_apply_linv<<<R.egrid(L.plane), ENT, 0, sm>>>(a);
   R.launched(3);
   // warm start (Eq. warm_start, Eq. Y_new_warmstart) or A_0 = D, E_0 = Y_0 = 0
-  if (first || !P.vws) {
+  if (first && P.vws && a.warm_A) {  // pyramid fine level from the coarse state (Z26)
+    k_cold_coarse<<<R.egrid(L.plane), ENT, 0, sm>>>(a);
+    k_clear_acc<<<R.sgrid(), 128, 0, sm>>>(a);
+    k_kty<<<R.egrid(L.plane), ENT, 0, sm>>>(a);
+    k_projy<<<R.egrid(L.plane), ENT, 0, sm>>>(a);
+    k_clear_acc<<<R.sgrid(), 128, 0, sm>>>(a);
+    R.launched(5);
+  } else if (first || !P.vws) {
     k_cold<<<R.egrid(L.plane), ENT, 0, sm>>>(a);
     R.launched();
   } else {
@@ -2028,7 +2073,8 @@ tilt_status inner(Ctx& ctx, const float* D, const float* J, const float* Q, int 
 
 tilt_status solve(Ctx& ctx, const float* images, int n_images, int H, int W, const int32_t* patch_image,
                   const int32_t* boxes, const float* tau0, int B, int m, int n, int kind, const DevParams& P,
-                  float* tau_out, float* A, float* E, float* Y, tilt_report* rep, const tilt_report* rep_prev) {
+                  float* tau_out, float* A, float* E, float* Y, tilt_report* rep, const tilt_report* rep_prev,
+                  const float* warm_A, const float* warm_E, const float* warm_Y, const tilt_report* warm_rep) {
   const int p = kind == TILT_HOMOGRAPHY ? 8 : 6;
   if (P.inner_solver != 0) return TILT_E_ARG;  // the ADM's own dtau step is the CTA kernels' (k_solve)
   tilt_status s0 = ensure(ctx, ws_need(B, m, n, p, P.svd_mode == 1), B);
@@ -2049,6 +2095,12 @@ tilt_status solve(Ctx& ctx, const float* images, int n_images, int H, int W, con
   a.kind = kind;
   a.patch_image = patch_image;
   a.boxes = boxes;
+  if (warm_A && warm_E && warm_Y && warm_rep) {
+    a.warm_A = warm_A;
+    a.warm_E = warm_E;
+    a.warm_Y = warm_Y;
+    a.warm_rep = warm_rep;
+  }
   cudaStream_t sm = ctx.stream;
   if (R.fail_cuda(cudaMemsetAsync(ctx.ws, 0, (size_t)B * L.stride * sizeof(float), sm), "memset(ws)")) return R.st;
   k_init<<<R.sgrid(), 128, 0, sm>>>(a);

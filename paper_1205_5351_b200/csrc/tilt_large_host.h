@@ -45,7 +45,9 @@ tilt_status inner(Ctx& ctx, const float* D, const float* J, const float* Q, int 
 tilt_status solve(Ctx& ctx, const float* images, int n_images, int H, int W, const int32_t* patch_image,
                   const int32_t* boxes, const float* tau0, int B, int m, int n, int kind, const DevParams& P,
                   float* tau_out, float* A, float* E, float* Y, tilt_report* rep,
-                  const tilt_report* rep_prev = nullptr);
+                  const tilt_report* rep_prev = nullptr, const float* warm_A = nullptr,
+                  const float* warm_E = nullptr, const float* warm_Y = nullptr,
+                  const tilt_report* warm_rep = nullptr);
 // SVT (tilt_svt_batch semantics) on the multi-CTA path
 tilt_status svt(Ctx& ctx, const float* M, int B, int m, int n, const float* eps, float* V_io, float* A,
                 float* sigma, int32_t* sweeps, float tol, int max_sweeps);

@@ -84,7 +84,9 @@ class TiltSolver:
         B = int(boxes_t.shape[0])
         p = p_of(kind)
         tau0_t = _dev(tau0, torch.float32, dev)
-        prm = params if params is not None else default_params()
+        # a private copy: the caller's params object is never written (a reused object must not
+        # carry one call's window size into the next)
+        prm = TiltParams.from_buffer_copy(params) if params is not None else default_params()
         if prm.win_h <= 0 or prm.win_w <= 0:
             bx = np.asarray(boxes.cpu() if isinstance(boxes, torch.Tensor) else boxes)
             if B > 0:

@@ -253,9 +253,12 @@ def test_ragged_sizes_fixed_count(solver, T, m, n, kind):
         assert np.max(np.abs(out["tau"][k].double().cpu().numpy() - refs[k]["tau"])) < 1e-3
 
 
+@pytest.mark.parametrize("path", [1, 3])
 @pytest.mark.parametrize("warm", [0, 1])
-def test_pyramid_config3_small(solver, T, warm):
-    """2-level pyramid (reading Z18); warm = 1: the fine level starts from the coarse A, E, Y (Z26)."""
+def test_pyramid_config3_small(solver, T, warm, path):
+    """2-level pyramid (reading Z18); warm = 1: the fine level starts from the coarse A, E, Y (Z26).
+    path 1: CTA-per-patch kernels; path 3: the multi-CTA path (the auto route above 128 x 128),
+    which must honour the warm start too."""
     cfg = ts.CONFIGS[3]
     B, K = 2, 20
     b = ts.gen_batch(cfg, 0, B)
@@ -263,7 +266,7 @@ def test_pyramid_config3_small(solver, T, warm):
     refs = [O.tilt_pyramid(b["images"][k], b["boxes"][k], b["tau0"][k], cfg.kind, prm_o, levels=2)
             for k in range(B)]
     prm = T.default_params(fixed_inner_iters=K, fixed_outer_iters=2, max_inner=K, max_outer=2, pyramid_levels=2,
-                           pyramid_warm=warm)
+                           pyramid_warm=warm, kernel_path=path)
     out = solver.solve(b["images"], b["patch_image"], b["boxes"], b["tau0"], cfg.kind, prm)
     rep = T.reports_to_numpy(out["rep"])
     for k in range(B):
@@ -316,3 +319,24 @@ def test_host_buffer_entry_matches_device_entry(solver, T):
     rep_d = T.reports_to_numpy(d["rep"])
     assert np.array_equal(h["rep"]["inner_iters"], rep_d["inner_iters"])
     assert np.array_equal(h["rep"]["status"], rep_d["status"])
+
+
+def test_bad_box_and_params_not_mutated(solver, T):
+    """Every box of a call must be win_w x win_h: a patch whose box differs gets TILT_PATCH_BAD_BOX
+    and is not solved (tau_out = tau0), the others are unaffected; the binding never writes the
+    caller's params (a reused object must not carry one call's window size into the next)."""
+    cfg = ts.CONFIGS[2]
+    b = ts.gen_batch(cfg, 0, 3)
+    prm = T.default_params(max_outer=2, fixed_outer_iters=2, fixed_inner_iters=10, max_inner=10)
+    ref = solver.solve(b["images"], b["patch_image"], b["boxes"], b["tau0"], cfg.kind, prm)
+    assert prm.win_h == 0 and prm.win_w == 0
+    boxes = b["boxes"].copy()
+    boxes[1, 2] -= 2
+    prm.win_h, prm.win_w = cfg.m, cfg.n
+    out = solver.solve(b["images"], b["patch_image"], boxes, b["tau0"], cfg.kind, prm)
+    rep = T.reports_to_numpy(out["rep"])
+    assert list(rep["status"]) == [rep["status"][0], T.BAD_BOX, rep["status"][2]]
+    assert rep["status"][0] != T.BAD_BOX
+    np.testing.assert_array_equal(out["tau"][1].cpu().numpy(), b["tau0"][1].astype(np.float32))
+    for k in (0, 2):
+        np.testing.assert_array_equal(out["tau"][k].cpu().numpy(), ref["tau"][k].cpu().numpy())
