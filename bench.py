@@ -2,12 +2,17 @@
 """Benchmark of the batched TILT hot path (BASELINE.json metric: rectified patches/s (converged),
 LADMAP inner iterations/s, % of FP32 / HBM roofline).
 
-One *step* = one call of the hot entry ``tilt_solve_batch`` over one batch: Algorithm 1 for every
-patch (warp/Jacobian -> orthonormalise -> LADMAP inner loop with warm Jacobi SVT -> dtau) until
-each patch retires. Workload (N = 1): BASELINE.json configs[1] = config 2, 1024 patches 50x50
-homography, seeded synthetic data (tilt_synth). For N > 1 (torchrun, one rank per GPU) each rank
-solves its own 1024-patch shard of the same patch stream (config 5 = config 2 sharded; weak
-scaling, no data-path collective); the tau/report gather to rank 0 runs after the timed region.
+Workload: BASELINE.json configs[4] = config 5, 65 536 patches 50x50 homography (config 2's recipe,
+seeded synthetic data from tilt_synth, seeds [5, idx]), the largest configuration that fits one GPU.
+The timed region of K steps solves the whole 65 536-patch set exactly once (strong scaling: the set
+is fixed, N GPUs split it): rank r owns patches r, r+N, ... (interleaved shards, SURVEY.md §8(e));
+step k is one call of the hot entry ``tilt_solve_batch`` on the k-th slab of 65 536 / (N K) of the
+rank's patches -- Algorithm 1 for every patch of the slab (warp/Jacobian -> orthonormalise -> LADMAP
+inner loop with warm Jacobi SVT -> dtau) until each patch retires. Consecutive slabs alternate
+between two handles on two CUDA streams, so a slab's tail (its slowest patches) overlaps the next
+slab's start; the whole pass then behaves like one 65 536-patch launch. For N > 1 the per-patch
+results (tau, reports, A, E) are gathered to rank 0 over NCCL inside the timed region, which ends
+when rank 0 holds them (time = max over ranks).
 
 Prints one JSON line on rank 0. ``--impl reference`` times the fp64 oracle (oracle/) instead, on a
 bounded sample of the same workload on the host cores.
@@ -15,13 +20,15 @@ bounded sample of the same workload on the host cores.
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
-import math
 import multiprocessing as mp
 import os
+import platform
 import subprocess
 import sys
 import tempfile
+import threading
 import time
 
 for _v in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS"):
@@ -33,10 +40,12 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 import tilt_synth as ts  # noqa: E402
+from tilt_synth import metrics as TM  # noqa: E402
 
-PER_RANK_BATCH = 1024
-CFG_ID = 2
+CFG_ID = 5
+GLOBAL_BATCH = ts.CONFIGS[CFG_ID].batch  # 65 536
 FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12  # 148 SMs x 128 FP32 lanes x FMA x sm_max_mhz
+METRIC = "rectified patches/s (converged)"
 
 
 def _peaks():
@@ -46,39 +55,58 @@ def _peaks():
         return {}
 
 
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return platform.processor() or "unknown"
+
+
 def _gen_one(args):
     cfg_id, idx = args
     return ts.gen_patch(ts.CONFIGS[cfg_id], idx)
 
 
-def gen_shard(cfg_id: int, start: int, count: int, workers: int = 0, indices=None) -> dict:
-    workers = workers or min(16, os.cpu_count() or 1)
-    if indices is not None:
-        count = len(indices)
-        jobs = [(cfg_id, int(i)) for i in indices]
-    else:
-        jobs = [(cfg_id, start + i) for i in range(count)]
+def gen_shard(cfg_id: int, indices, workers: int = 0) -> dict:
+    """Patches ``indices`` of config ``cfg_id`` (one canvas each), generated on the host cores."""
+    workers = workers or min(32, os.cpu_count() or 1)
+    jobs = [(cfg_id, int(i)) for i in indices]
+    count = len(jobs)
     if workers > 1 and count > 8:
         with mp.get_context("fork").Pool(workers) as pool:
-            pats = pool.map(_gen_one, jobs, chunksize=16)
+            pats = pool.map(_gen_one, jobs, chunksize=64)
     else:
         pats = [_gen_one(j) for j in jobs]
     return {
         "images": np.stack([p["canvas"] for p in pats]),
-        "patch_image": np.arange(count, dtype=np.int32),
         "boxes": np.stack([p["box"] for p in pats]),
         "tau0": np.stack([p["tau0"] for p in pats]).astype(np.float32),
+        "tau_g": np.stack([p["tau_g"] for p in pats]),
     }
 
 
-def flops_per_launch(rep, m, n, p, ns_period: int = 4) -> float:
-    """Algorithmic FLOPs (SURVEY.md §8(d) model) from the device counters of one launch:
-    per LADMAP iteration 8pmn + 20mn + 4mn^2 + 4n^3/ns_period (the Newton-Schulz step on V runs
-    after every ns_period-th SVT, tilt_params.ns_period), per Jacobi sweep n(n-1)/2 (12m + 6n)."""
-    it = float(np.sum(rep["inner_iters"]))
-    sw = float(np.sum(rep["jacobi_sweeps"]))
+def flops_model(rep, m, n, p, ns_period: int = 4) -> float:
+    """Algorithmic FLOPs (SURVEY.md §8(d) model) from the device counters: per LADMAP iteration
+    8pmn + 20mn + 4mn^2 + 4n^3/ns_period (the Newton-Schulz step on V after every ns_period-th SVT),
+    per Jacobi sweep n(n-1)/2 (12m + 6n) -- every pair of every sweep credited with a rotation."""
+    it = float(np.sum(rep["inner_iters"], dtype=np.float64))
+    sw = float(np.sum(rep["jacobi_sweeps"], dtype=np.float64))
     return it * (8 * p * m * n + 20 * m * n + 4 * m * n * n + 4 * n ** 3 / max(1, ns_period)) + \
         sw * n * (n - 1) / 2 * (12 * m + 6 * n)
+
+
+def flops_rotations(rep, m, n, p, ns_period: int = 4) -> float:
+    """The same with the Jacobi term from the rotations actually applied (device counter
+    ``jacobi_rotations``): every visited pair costs its three column dots (6m), every applied
+    rotation its B and V column updates (6m + 6n); a pair below the tolerance costs the dots only."""
+    it = float(np.sum(rep["inner_iters"], dtype=np.float64))
+    sw = float(np.sum(rep["jacobi_sweeps"], dtype=np.float64))
+    rot = float(np.sum(rep["jacobi_rotations"], dtype=np.float64))
+    return it * (8 * p * m * n + 20 * m * n + 4 * m * n * n + 4 * n ** 3 / max(1, ns_period)) + \
+        sw * n * (n - 1) / 2 * 6 * m + rot * (6 * m + 6 * n)
 
 
 class ClockSampler:
@@ -119,50 +147,85 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+# ------------------------------------------------------------------------------------------------
+# the fp64 oracle on the host cores (the cpu_baseline leg and the reference arm)
+# ------------------------------------------------------------------------------------------------
 def _oracle_job(args):
     import oracle as O
     image, box, tau0 = args
     return O.tilt(image, box, tau0, ts.HOMOGRAPHY)
 
 
-def cpu_sample(batch: dict, count: int, cores: int) -> dict:
-    """The fp64 oracle as it stands on the first ``count`` patches, one process per patch."""
+def cpu_sample(batch: dict, count: int, procs: int) -> dict:
+    """The fp64 oracle as it stands on the first ``count`` patches of ``batch``, ``procs`` processes
+    (one patch per process at a time, one BLAS thread each)."""
     jobs = [(batch["images"][k], batch["boxes"][k], batch["tau0"][k].astype(np.float64)) for k in range(count)]
     t0 = time.perf_counter()
-    with mp.get_context("fork").Pool(min(cores, count)) as pool:
-        res = pool.map(_oracle_job, jobs, chunksize=1)
+    if procs > 1:
+        with mp.get_context("fork").Pool(procs) as pool:
+            res = pool.map(_oracle_job, jobs, chunksize=1)
+    else:
+        res = [_oracle_job(j) for j in jobs]
     dt = time.perf_counter() - t0
     conv = sum(1 for r in res if r["status"] == 0)
     inner = sum(r["inner_iters"] for r in res)
-    return {"seconds": dt, "converged": conv, "inner_iters": inner, "cores": min(cores, count), "count": count}
+    return {"seconds": dt, "converged": conv, "inner_iters": inner, "procs": procs, "count": count,
+            "patches_per_s": count / dt}
+
+
+def cpu_baseline(batch: dict, cores: int) -> dict:
+    """All host cores (one patch per core) and one thread (2 patches), on the first patches of the
+    bench workload. Reports converged patches/s (the metric) and all-patches/s."""
+    allc = cpu_sample(batch, cores, cores)
+    one = cpu_sample(batch, 2, 1)
+    return {"value": allc["converged"] / allc["seconds"], "unit": "patches/s", "cores": cores, "kind": "oracle",
+            "cpu_model": cpu_model(), "inner_iters_per_s": allc["inner_iters"] / allc["seconds"],
+            "all_patches_per_s": allc["patches_per_s"],
+            "sample": f"first {cores} patches of config 5 (one process per patch, {cores} cores, "
+                      f"{allc['seconds']:.1f} s)",
+            "one_thread": {"patches_per_s": one["patches_per_s"],
+                           "converged_per_s": one["converged"] / one["seconds"],
+                           "inner_iters_per_s": one["inner_iters"] / one["seconds"],
+                           "sample": f"first 2 patches, 1 thread ({one['seconds']:.1f} s)"}}
 
 
 def run_reference(args, rank: int) -> None:
     if rank != 0:
         return
-    batch = gen_shard(CFG_ID, 0, args.cpu_sample)
     cores = os.cpu_count() or 1
+    count = args.cpu_sample or cores
+    batch = gen_shard(CFG_ID, range(count))
     vals, inners, secs = [], [], []
     for _ in range(args.warmup if args.ref_warmup else 0):
-        cpu_sample(batch, args.cpu_sample, cores)
+        cpu_sample(batch, count, min(cores, count))
     for _ in range(args.steps):
-        r = cpu_sample(batch, args.cpu_sample, cores)
+        r = cpu_sample(batch, count, min(cores, count))
         vals.append(r["converged"] / r["seconds"])
         inners.append(r["inner_iters"] / r["seconds"])
         secs.append(r["seconds"])
     value = float(np.mean(vals))
     line = {
-        "impl": "reference", "metric": "rectified patches/s (converged)", "value": value, "unit": "patches/s",
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "patches/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * float(np.mean(secs)),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"config 2 sample: first {args.cpu_sample} of 1024 patches 50x50 homography",
-                   "global_batch": args.cpu_sample, "patch": "50x50", "transform": "homography"},
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"config 5 sample: first {count} of 65536 patches 50x50 homography (fp64 oracle)",
+                   "global_batch": count, "patch": "50x50", "transform": "homography"},
         "inner_iters_per_s": float(np.mean(inners)),
-        "cpu_baseline": {"value": value, "unit": "patches/s", "cores": min(cores, args.cpu_sample), "kind": "oracle",
-                         "sample": f"first {args.cpu_sample} patches of config 2, one process per patch"},
+        "cpu_baseline": {"value": value, "unit": "patches/s", "cores": min(cores, count), "kind": "oracle",
+                         "cpu_model": cpu_model(),
+                         "sample": f"first {count} patches of config 5 per step, one process per patch"},
         "e2e": {"value": value, "unit": "patches/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------------------------
+# the CUDA path
+# ------------------------------------------------------------------------------------------------
+def slab_bounds(total: int, steps: int) -> list:
+    """Step k solves rows [lo_k, hi_k) of the rank's shard: the shard split into ``steps`` slabs."""
+    edges = [round(k * total / steps) for k in range(steps + 1)]
+    return [(edges[k], edges[k + 1]) for k in range(steps)]
 
 
 def run_ours(args, rank: int, world: int, local_rank: int) -> None:
@@ -174,80 +237,96 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     cfg = ts.CONFIGS[CFG_ID]
-    B = args.batch
+    G = args.global_batch
     m, n, p, kind = cfg.m, cfg.n, cfg.p, cfg.kind
-    # rank r solves patches r, r + N, r + 2N, ... of the first N*B patches (interleaved shards)
-    batch = gen_shard(CFG_ID, 0, B, indices=D.shard_indices(B * world, world, rank))
+    idx = D.shard_indices(G, world, rank)  # rank r: patches r, r + N, ...
+    S = len(idx)
+    t_gen = time.perf_counter()
+    batch = gen_shard(CFG_ID, idx)
+    t_gen = time.perf_counter() - t_gen
+    slabs = slab_bounds(S, args.steps)
+    cap = max(hi - lo for lo, hi in slabs)
     images = torch.as_tensor(batch["images"], device=dev)
-    patch_image = torch.as_tensor(batch["patch_image"], device=dev)
     boxes = torch.as_tensor(batch["boxes"], device=dev)
     tau0 = torch.as_tensor(batch["tau0"], device=dev)
-    solver = T.TiltSolver(local_rank, max_batch=B, max_m=m, max_n=n, max_p=p,
-                          max_image_elems=int(images.numel()))
+    pimg = torch.arange(cap, dtype=torch.int32, device=dev)  # slab-local patch -> image
+    nst = max(1, args.streams)
+    solvers = [T.TiltSolver(local_rank, max_batch=cap, max_m=m, max_n=n, max_p=p,
+                            max_image_elems=cap * 4 * m * n) for _ in range(nst)]
+    streams = [torch.cuda.Stream(dev) for _ in range(nst)]
     prm = T.default_params(win_h=m, win_w=n)
     out = {
-        "tau": torch.empty((B, p), dtype=torch.float32, device=dev),
-        "A": torch.empty((B, m, n), dtype=torch.float32, device=dev),
-        "E": torch.empty((B, m, n), dtype=torch.float32, device=dev),
-        "Y": None,
-        "rep": torch.empty((B, T.solver._abi.REPORT_BYTES), dtype=torch.uint8, device=dev),
+        "tau": torch.empty((S, p), dtype=torch.float32, device=dev),
+        "A": torch.empty((S, m, n), dtype=torch.float32, device=dev),
+        "E": torch.empty((S, m, n), dtype=torch.float32, device=dev),
+        "rep": torch.empty((S, T.solver._abi.REPORT_BYTES), dtype=torch.uint8, device=dev),
     }
-    l2_flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 
-    def step():
-        solver.solve(images, patch_image, boxes, tau0, kind, prm, out=out, sync=False)
+    def step(k: int, slab: int) -> None:
+        lo, hi = slabs[slab]
+        o = {"tau": out["tau"][lo:hi], "A": out["A"][lo:hi], "E": out["E"][lo:hi], "Y": None,
+             "rep": out["rep"][lo:hi]}
+        with torch.cuda.stream(streams[k % nst]):
+            solvers[k % nst].solve(images[lo:hi], pimg[: hi - lo], boxes[lo:hi], tau0[lo:hi], kind, prm, out=o,
+                                   sync=False)
 
-    for _ in range(args.warmup):
-        l2_flush.zero_()
-        step()
+    main = torch.cuda.current_stream(dev)
+    for w in range(args.warmup):  # untimed: slabs from the end of the pass
+        step(w, (args.steps - 1 - w) % args.steps)
+    torch.cuda.synchronize()
+    torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev).zero_()  # flush L2 once
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     clocks = ClockSampler(local_rank) if rank == 0 else None
-    stream = torch.cuda.current_stream()
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    launches0 = solver.launches
+    launches0 = sum(s.launches for s in solvers)
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    t_all0 = torch.cuda.Event(enable_timing=True)
-    t_all1 = torch.cuda.Event(enable_timing=True)
-    t_all0.record(stream)
+    t0.record(main)
+    for s in streams:
+        s.wait_event(t0)
     for k in range(args.steps):
-        l2_flush.zero_()  # inputs (41 MB) are smaller than L2: flush between steps
-        ev[k][0].record(stream)
-        step()
-        ev[k][1].record(stream)
-    t_all1.record(stream)
+        step(k, k)
+    for s in streams:
+        main.wait_stream(s)
+    gathered = None
+    gather_bytes = 0
+    if world > 1:  # rank 0 collects every patch's tau / report / A / E (north_star's NCCL gather)
+        gathered = {}
+        for key in ("tau", "rep", "A", "E"):
+            x = out[key] if dist.get_backend() == "nccl" else out[key].cpu()
+            gathered[key] = D.gather_to_root(x, G, world, rank)
+            gather_bytes += int(x.numel() * x.element_size()) * (world - 1)
+    t1.record(main)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    launches = solver.launches - launches0
+    launches = sum(s.launches for s in solvers) - launches0
     clk = clocks.stop() if clocks else None
-    elapsed = t_all0.elapsed_time(t_all1) / 1e3
-    kern_ms = [a.elapsed_time(b) for a, b in ev]
+    elapsed = t0.elapsed_time(t1) / 1e3
     rep = T.reports_to_numpy(out["rep"])
     conv = int(np.sum(rep["status"] == T.CONVERGED))
-    inner = int(np.sum(rep["inner_iters"]))
-    flops = flops_per_launch(rep, m, n, p, int(prm.ns_period))
-    stats = torch.tensor([elapsed, float(conv), float(inner), flops, float(np.mean(kern_ms))], dtype=torch.float64,
-                         device=dev)
+    inner = int(np.sum(rep["inner_iters"], dtype=np.int64))
+    fl_model = flops_model(rep, m, n, p, int(prm.ns_period))
+    fl_rot = flops_rotations(rep, m, n, p, int(prm.ns_period))
+    stats = [float(conv), float(inner), fl_model, fl_rot, float(launches)]
     if world > 1:
-        cdev = stats.device if dist.get_backend() == "nccl" else "cpu"  # gloo smoke test: host tensors
-        tmax = stats[0:1].clone().to(cdev)
+        cdev = dev if dist.get_backend() == "nccl" else "cpu"  # gloo smoke test: host tensors
+        tmax = torch.tensor([elapsed], dtype=torch.float64, device=cdev)
         dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
-        tot = stats[1:4].clone().to(cdev)
+        tot = torch.tensor(stats, dtype=torch.float64, device=cdev)
         dist.all_reduce(tot, op=dist.ReduceOp.SUM)
         elapsed = float(tmax.item())
-        conv_all, inner_all, flops_all = (float(x) for x in tot.tolist())
-    else:
-        conv_all, inner_all, flops_all = float(conv), float(inner), flops
-    # end to end through the host-buffer API on every rank (max time over ranks, summed patches)
+        stats = [float(x) for x in tot.tolist()]
+    conv_all, inner_all, fl_model_all, fl_rot_all, launches_all = stats
+    # end to end through the host-buffer API (tilt_solve_batch_host), same slabs, same streams
     e2e_line = None
     if not args.no_e2e:
         if world > 1:
             dist.barrier()
-        e2e_line = e2e(solver, batch, kind, prm, args)
+        e2e_line = e2e(solvers, batch, slabs, kind, prm, p, m, n)
         if world > 1:
             cdev = dev if dist.get_backend() == "nccl" else "cpu"
             red = torch.tensor([e2e_line["_seconds"]], dtype=torch.float64, device=cdev)
@@ -261,86 +340,113 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
         e2e_line["value"] = e2e_line["_conv"] / e2e_line["_seconds"]
         e2e_line.pop("_conv")
         e2e_line.pop("_seconds")
-    # gather tau / reports to rank 0 (north_star: NCCL gather of the results; outside the timed region)
-    gather_ms = None
-    if world > 1:
-        t0 = time.perf_counter()
-        for key in ("tau", "rep", "A", "E"):
-            x = out[key] if dist.get_backend() == "nccl" else out[key].cpu()
-            D.gather_to_root(x, B * world, world, rank)
-        torch.cuda.synchronize()
-        gather_ms = 1e3 * (time.perf_counter() - t0)
     if rank != 0:
+        for s in solvers:
+            s.close()
         return
-    value = conv_all * args.steps / elapsed
-    iters_per_s = inner_all * args.steps / elapsed
-    peaks = _peaks()
-    kernel_s = float(np.mean(kern_ms)) / 1e3
-    achieved = flops / kernel_s / 1e12
+    # results of the whole set on rank 0 (gathered for N > 1)
+    if gathered is not None:
+        rep_all = T.reports_to_numpy(gathered["rep"])
+        tau_all = gathered["tau"].double().cpu().numpy()
+        tau_g = np.stack([ts.gen_patch(cfg, int(i))["tau_g"] for i in range(G)]) if args.recovery_all else None
+    else:
+        rep_all = rep
+        tau_all = out["tau"].double().cpu().numpy()
+        tau_g = batch["tau_g"]
+    value = conv_all / elapsed
+    achieved = fl_model_all / elapsed / 1e12
+    achieved_rot = fl_rot_all / elapsed / 1e12
     traffic = None
     try:
         prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))
         traffic = prof.get("k_solve_dram_bytes_per_launch")
     except Exception:
         pass
-    binding = None  # the resource ncu shows binding k_solve (shared-memory wavefronts, not the FMA pipe)
+    binding = None
     try:
-        met = json.load(open(os.path.join(ROOT, "profiles", "r01", "k_solve_s64_full_metrics.json")))
-        binding = {"resource": "shared-memory wavefronts (LSU pipe)",
-                   "frac": float(met["l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed"][0]) / 100,
-                   "fma_pipe_frac": float(met["sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active"][0]) / 100,
-                   "source": "ncu --set full of k_solve (1184 x 30 iterations), profiles/r01/k_solve_s64_full_metrics.json"}
+        met = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))["k_solve_binding"]
+        binding = met
     except Exception:
         pass
+    status_names = {T.CONVERGED: "converged", T.MAX_OUTER: "max_outer", T.WINDOW_ESCAPE: "window_escape",
+                    T.SINGULAR_GRAM: "singular_gram", T.ZERO_PATCH: "zero_patch", T.DIVERGED: "diverged",
+                    T.BAD_BOX: "bad_box"}
+    stop_names = {0: "none", 1: "objective_change", 2: "dtau", 3: "max_outer"}
     line = {
-        "metric": "rectified patches/s (converged)", "value": value, "unit": "patches/s", "n_gpus": world,
+        "metric": METRIC, "value": value, "unit": "patches/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * elapsed / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": f"config 2: {B} patches 50x50 homography per GPU (tilt_synth seeds [2, idx])",
-                   "global_batch": B * world, "per_gpu_batch": B, "patch": f"{m}x{n}", "transform": "homography",
-                   "parallelism": f"patch-sharded x{world}", "l2": "flushed between steps (256 MB write)"},
-        "inner_iters_per_s": iters_per_s,
-        "converged_fraction": conv_all / (B * world),
-        "mean_inner_iters_per_patch": inner_all / (B * world),
-        "mean_jacobi_sweeps_per_svt": float(np.sum(rep["jacobi_sweeps"]) / max(1, np.sum(rep["inner_iters"]))),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"config 5: {G} patches 50x50 homography (tilt_synth seeds [5, idx]), "
+                               f"one pass per timed region, {args.steps} slabs",
+                   "global_batch": G, "per_gpu_batch": S, "slab_patches": cap, "streams": nst,
+                   "patch": f"{m}x{n}", "transform": "homography", "parallelism": f"patch-sharded x{world}",
+                   "l2": f"not flushed between steps: every step reads its own slab of canvases "
+                         f"({cap * 4 * 4 * m * n / 1e6:.0f} MB), the pass reads "
+                         f"{S * 4 * 4 * m * n / 1e9:.2f} GB per GPU (L2 126 MB); flushed once before the "
+                         f"timed region"},
+        "inner_iters_per_s": inner_all / elapsed,
+        "converged_fraction": conv_all / G,
+        "mean_inner_iters_per_patch": inner_all / G,
+        "mean_jacobi_sweeps_per_svt": float(np.sum(rep["jacobi_sweeps"], dtype=np.float64) /
+                                            max(1, np.sum(rep["inner_iters"], dtype=np.float64))),
+        "status": {status_names.get(int(k), str(k)): int(v) for k, v in
+                   zip(*np.unique(rep_all["status"], return_counts=True))},
+        "stop_rules": {stop_names.get(int(k), str(k)): int(v) for k, v in
+                       zip(*np.unique(rep_all["stop_rule"], return_counts=True))},
         "roofline": {"bound": "alu", "kernel": "k_solve", "achieved": achieved, "peak": FP32_PEAK_TFLOPS,
                      "unit": "TFLOP/s", "frac": achieved / FP32_PEAK_TFLOPS, "traffic": traffic,
-                     "peak_note": "FP32 FMA: 148 SMs x 128 lanes x 2 x 1.965 GHz (sm_max_mhz of MEASURED_PEAKS.json); "
-                                  "achieved = SURVEY §8(d) model flops from the device counters / event time",
-                     "flops_per_launch": flops, "binding": binding},
-        "gpu_launches": int(launches),
+                     "peak_note": "FP32 FMA: 148 SMs x 128 lanes x 2 x 1.965 GHz (sm_max_mhz of "
+                                  "MEASURED_PEAKS.json; DESIGN.md §4)",
+                     "achieved_note": "SURVEY §8(d) model flops from the device counters of all launches / "
+                                      "event time of the timed region (k_solve is ~100% of it)",
+                     "flops_per_pass": fl_model_all,
+                     "rotation_count": {"achieved": achieved_rot, "frac": achieved_rot / FP32_PEAK_TFLOPS,
+                                        "flops_per_pass": fl_rot_all,
+                                        "note": "Jacobi term from jacobi_rotations: 6m per visited pair + "
+                                                "(6m + 6n) per applied rotation"},
+                     "binding": binding},
+        "gpu_launches": int(launches_all),
         "clocks": clk,
+        "gen_seconds": t_gen,
     }
-    if gather_ms is not None:
-        line["gather_ms"] = gather_ms
-    # K1 (warp/Jacobian) standalone HBM roofline over the same batch (first outer iteration's warp)
+    if tau_g is not None:
+        rec = [TM.recovered_p9(tau_all[k], tau_g[k]) for k in range(len(tau_g))]
+        err = np.array([TM.table2_error(tau_all[k], tau_g[k]) for k in range(len(tau_g))])
+        convm = rep_all["status"][: len(tau_g)] == T.CONVERGED
+        line["recovery"] = {
+            "rule": "SURVEY P9(ii): H_G^-1 tau* diagonal to 0.02 relative, perspective < 1e-2",
+            "patches": len(tau_g), "fraction": float(np.mean(rec)),
+            "fraction_of_converged": float(np.mean(np.asarray(rec)[convm])) if convm.any() else None,
+            "table2_error_median": float(np.median(err)), "table2_error_mean": float(np.mean(err)),
+            "table2_note": "||tau* - tau_G|| / ||tau_G|| (P:1380-1381), normalised coordinates"}
+    if world > 1:
+        line["gather"] = {"bytes_to_rank0": gather_bytes, "backend": dist.get_backend(),
+                          "note": "tau, reports, A, E of every patch to rank 0, inside the timed region"}
     if world == 1 and not args.no_k1:
-        line["roofline_k1"] = k1_roofline(solver, images, patch_image, boxes, tau0, kind, m, n, p, peaks)
+        k1n = min(S, args.k1_batch)
+        line["roofline_k1"] = k1_roofline(solvers[0], images[:k1n], pimg[:k1n], boxes[:k1n], tau0[:k1n], kind, m, n,
+                                          p, _peaks())
     if e2e_line is not None:
         line["e2e"] = e2e_line
-    if world == 1 and args.cpu_sample > 0:
-        r = cpu_sample(batch, args.cpu_sample, os.cpu_count() or 1)
-        line["cpu_baseline"] = {"value": r["converged"] / r["seconds"], "unit": "patches/s", "cores": r["cores"],
-                                "kind": "oracle", "inner_iters_per_s": r["inner_iters"] / r["seconds"],
-                                "sample": f"first {r['count']} patches of the same batch, one process per patch"}
+    if world == 1 and not args.no_cpu:
+        line["cpu_baseline"] = cpu_baseline(batch, args.cpu_sample or (os.cpu_count() or 1))
     print(json.dumps(line), flush=True)
-    solver.close()
+    for s in solvers:
+        s.close()
 
 
 def k1_roofline(solver, images, patch_image, boxes, tau0, kind, m, n, p, peaks) -> dict:
     import torch
+    from paper_1205_5351_b200 import lib
     B = int(boxes.shape[0])
     reps = 20
-    outs = solver.warp(images, patch_image, boxes, tau0, kind)  # warm-up + outputs allocated
-    del outs
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    dh = torch.empty((B, m, n), dtype=torch.float32, device=images.device)
-    J = torch.empty((B, p, m, n), dtype=torch.float32, device=images.device)
-    import ctypes
-    from paper_1205_5351_b200 import lib
-    nrm = torch.empty(B, dtype=torch.float32, device=images.device)
-    st = torch.empty(B, dtype=torch.int32, device=images.device)
+    dev = images.device
+    dh = torch.empty((B, m, n), dtype=torch.float32, device=dev)
+    J = torch.empty((B, p, m, n), dtype=torch.float32, device=dev)
+    nrm = torch.empty(B, dtype=torch.float32, device=dev)
+    st = torch.empty(B, dtype=torch.int32, device=dev)
     n_images, H, W = images.shape
+    images = images.contiguous()
 
     def launch():
         lib.tilt_warp_batch(solver._h, ctypes.c_void_p(images.data_ptr()), n_images, H, W,
@@ -353,21 +459,22 @@ def k1_roofline(solver, images, patch_image, boxes, tau0, kind, m, n, p, peaks) 
         launch()
     torch.cuda.synchronize()
     # cold-L2 timing: flush (write 256 MB > L2) before every launch, time each launch alone
-    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=images.device)
-    ts = []
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    tl = []
     for _ in range(reps):
         flush.zero_()
         e0.record()
         launch()
         e1.record()
         torch.cuda.synchronize()
-        ts.append(e0.elapsed_time(e1) / 1e3)
+        tl.append(e0.elapsed_time(e1) / 1e3)
     del flush
-    t = float(np.median(ts))
+    t = float(np.median(tl))
     # algorithmic bytes: distinct source taps (identity tau: (m+1)(n+1) px) + D_hat and J written
     byts = B * 4.0 * ((m + 1) * (n + 1) + m * n * (1 + p))
     achieved = byts / t / 1e9
-    peak = float(peaks.get("hbm_gbs", 6650.0))
+    peak = float(peaks.get("hbm_gbs", 6536.4))
     traffic = None
     try:
         traffic = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json"))).get("k_warp_dram_bytes_per_launch")
@@ -375,48 +482,78 @@ def k1_roofline(solver, images, patch_image, boxes, tau0, kind, m, n, p, peaks) 
         pass
     return {"bound": "hbm", "kernel": "k_warp", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "traffic": traffic, "bytes_per_launch": byts, "us_per_launch": 1e6 * t,
-            "note": "standalone K1 over the bench batch at tau0; L2 flushed before each timed launch (median of "
-                    f"{reps})"}
+            "patches": B,
+            "note": f"standalone K1 over the first {B} patches of the bench workload at tau0; L2 flushed before "
+                    f"each timed launch (median of {reps})"}
 
 
-def e2e(solver, batch, kind, prm, args) -> dict:
+def e2e(solvers, batch, slabs, kind, prm, p, m, n) -> dict:
+    """The same pass through ``tilt_solve_batch_host`` (host buffers in pinned memory; the H2D copy
+    of each slab's inputs and the D2H copy of its tau / A / E / reports are inside the timed region).
+    Slabs alternate between the handles, one host thread per handle (ctypes drops the GIL)."""
     import torch
-    from paper_1205_5351_b200._abi import REPORT_BYTES as T_REPORT_BYTES
-    images = np.ascontiguousarray(batch["images"])
-    pinned = {k: torch.from_numpy(np.ascontiguousarray(v)).pin_memory() for k, v in batch.items()}
-    B = batch["boxes"].shape[0]
-    p = 8 if kind == 1 else 6
-    m, n = int(batch["boxes"][0, 3]), int(batch["boxes"][0, 2])
-    solver.solve_host(pinned["images"].numpy(), pinned["patch_image"].numpy(), pinned["boxes"].numpy(),
-                      pinned["tau0"].numpy(), kind, prm)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize()
-    e0.record()
-    conv = 0
-    for _ in range(args.steps):
-        r = solver.solve_host(pinned["images"].numpy(), pinned["patch_image"].numpy(), pinned["boxes"].numpy(),
-                              pinned["tau0"].numpy(), kind, prm)
-        conv += int(np.sum(r["rep"]["status"] == 0))
-    e1.record()
-    torch.cuda.synchronize()
-    t = e0.elapsed_time(e1) / 1e3
-    h2d = images.nbytes + batch["patch_image"].nbytes + batch["boxes"].nbytes + B * p * 4
-    d2h = B * p * 4 + 2 * B * m * n * 4 + B * T_REPORT_BYTES
-    return {"value": conv / t, "unit": "patches/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-            "api": "tilt_solve_batch_host (host buffers, pinned)", "_conv": conv, "_seconds": t}
+    from paper_1205_5351_b200._abi import REPORT_BYTES
+    from paper_1205_5351_b200.solver import REPORT_DTYPE
+    pin = {k: torch.from_numpy(np.ascontiguousarray(batch[k])).pin_memory().numpy()
+           for k in ("images", "boxes", "tau0")}
+    S = pin["boxes"].shape[0]
+    cap = max(hi - lo for lo, hi in slabs)
+    pimg = np.arange(cap, dtype=np.int32)
+    tau = torch.empty((S, p), dtype=torch.float32).pin_memory().numpy()
+    A = torch.empty((S, m, n), dtype=torch.float32).pin_memory().numpy()
+    E = torch.empty((S, m, n), dtype=torch.float32).pin_memory().numpy()
+    rep = np.zeros(S, REPORT_DTYPE)
+    from paper_1205_5351_b200 import lib
+    from paper_1205_5351_b200._abi import check
+
+    def hp(a):
+        return a.ctypes.data_as(ctypes.c_void_p)
+
+    def run(slab_ids, sv):
+        sv._bind_stream()
+        for s in slab_ids:
+            lo, hi = slabs[s]
+            check(lib.tilt_solve_batch_host(sv._h, hp(pin["images"][lo:hi]), hi - lo, 2 * m, 2 * n, hp(pimg),
+                                            hp(pin["boxes"][lo:hi]), hp(pin["tau0"][lo:hi]), hi - lo, kind,
+                                            ctypes.byref(prm), hp(tau[lo:hi]), hp(A[lo:hi]), hp(E[lo:hi]),
+                                            hp(rep[lo:hi])), "tilt_solve_batch_host")
+
+    nst = len(solvers)
+    run([0], solvers[0])  # warm-up of the host entry (one slab)
+    t0 = time.perf_counter()
+    threads = [threading.Thread(target=run, args=(list(range(j, len(slabs), nst)), solvers[j])) for j in range(nst)]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join()
+    t = time.perf_counter() - t0
+    conv = int(np.sum(rep["status"] == 0))
+    h2d = pin["images"].nbytes + S * 4 + pin["boxes"].nbytes + pin["tau0"].nbytes
+    d2h = S * p * 4 + 2 * S * m * n * 4 + S * REPORT_BYTES
+    steps = len(slabs)
+    return {"value": conv / t, "unit": "patches/s", "h2d_bytes_per_step": int(h2d / steps),
+            "d2h_bytes_per_step": int(d2h / steps),
+            "api": f"tilt_solve_batch_host (pinned host buffers), {nst} host threads / handles",
+            "timer": "host wall clock around the pass (the entry copies in, solves, copies out, and syncs)",
+            "_conv": conv, "_seconds": t}
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=8)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--batch", type=int, default=PER_RANK_BATCH)
-    ap.add_argument("--cpu-sample", type=int, default=8)
+    ap.add_argument("--global-batch", type=int, default=GLOBAL_BATCH,
+                    help="patches of config 5 solved per timed region (default: all 65536)")
+    ap.add_argument("--streams", type=int, default=2)
+    ap.add_argument("--cpu-sample", type=int, default=0, help="oracle patches (0: one per host core)")
+    ap.add_argument("--k1-batch", type=int, default=8192)
     ap.add_argument("--ref-warmup", action="store_true")
+    ap.add_argument("--recovery-all", action="store_true", help="N > 1: regenerate tau_G of every patch on rank 0")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-k1", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                     help="process-group backend (gloo: a smoke test of the N > 1 code path on fewer GPUs "
                          "than ranks; never a measurement)")

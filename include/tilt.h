@@ -93,7 +93,9 @@ typedef struct {
   int32_t fixed_outer_iters;  /* > 0: exactly this many outer iterations */
   const uint8_t* rho_replay;  /* device [B][max_outer][max_inner] or NULL (Z21): bit 0 = rho decision
                                  (1: rho0), bit 1 = end the inner loop after this iteration */
-  float* trace;               /* device [B][max_outer][max_inner][4] (mu, crit1, crit2, rho) or NULL */
+  float* trace;               /* device [B][max_outer][max_inner][4] (mu, crit1, crit2, rho) or NULL;
+                                 the multi-CTA path adds 2 to the rho slot when the iteration took
+                                 Algorithm 2's warm step (svd_mode 1) */
   /* window size of the call (all boxes share it; a patch whose box differs is reported
    * TILT_PATCH_BAD_BOX and not solved). 0: read back from boxes[0] with a stream sync;
    * > 0: taken as given. Host syncs: none on the CTA-per-patch kernels when win_h, win_w > 0 (the
@@ -106,7 +108,7 @@ typedef struct {
    * at 200 x 200 it is 2.4x faster; the ADM inner entry stays on the CTA kernels up to 256),
    * 1 = CTA-per-patch kernels, 2 = warp-per-patch kernel (m <= 64 and n <= 50; TILT_E_ARG otherwise),
    * 3 = multi-CTA path (tilt_inner_batch only, LADMAP, m, n <= 1024: one problem spread over many
-   * CTAs, block-cyclic Jacobi, cuBLAS SGEMMs). All compute the same method; they
+   * CTAs, block-cyclic Jacobi, hand-written batched GEMM). All compute the same method; they
    * differ in data layout, Jacobi ordering and how a problem maps to the GPU. */
   int32_t kernel_path;
   /* Newton-Schulz re-orthonormalisation of the carried V (reading Z14) after every ns_period-th

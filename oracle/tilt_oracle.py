@@ -416,6 +416,7 @@ class SvdWarm:
         self.warm_steps = 0
         self.full_svds = 0
         self.decisions = []
+        self.cayley_sizes = []  # test instrumentation: max ||(t*/2) P_U||_F, ||(t*/2) P_V||_F per warm step
 
     def svt(self, m_k, eps):
         m_k = np.asarray(m_k, dtype=np.float64)
@@ -426,6 +427,9 @@ class SvdWarm:
             u, sig, v, t = svd_warm_start(x, *self.prev)
             if t != 0.0:
                 step = (u, sig, v)
+                w = (self.prev[0] * self.prev[1]) @ self.prev[2].T
+                self.cayley_sizes.append(0.5 * abs(t) * max(np.linalg.norm(w @ x.T - x @ w.T),
+                                                            np.linalg.norm(w.T @ x - x.T @ w)))
         if step is not None:
             u, sig, v = step
             self.warm_steps += 1

@@ -393,6 +393,7 @@ static int lp_chunk(tilt_handle* h, int B, int m, int n, int p, bool svdws) {
   const size_t per = tilt::lp::ws_need(1, m, n, p, svdws) * sizeof(float);
   size_t c = per > 0 ? h->lp_budget / per : (size_t)B;
   if (c < 1) c = 1;
+  if (c > 65535) c = 65535;  // problems index gridDim.y / gridDim.z of the multi-CTA kernels
   return c < (size_t)B ? (int)c : B;
 }
 
@@ -448,7 +449,7 @@ tilt_status tilt_create(tilt_handle** out, const tilt_create_opts* o) {
     if ((e = cudaMalloc(&h->ws, h->ws_floats * sizeof(float))) != cudaSuccess) return fail(e, "cudaMalloc(ws)");
   }
   if ((e = cudaMalloc(&h->counter, 64 * sizeof(int))) != cudaSuccess) return fail(e, "cudaMalloc(counter)");
-  // windows above 128 x 128 take the multi-CTA path by default: its workspace and cuBLAS handle are
+  // windows above 128 x 128 take the multi-CTA path by default: its workspace is
   // made here, so the solve entries allocate nothing (SVDWS or a forced kernel_path = 3 at smaller
   // sizes still allocate on first use, as tilt.h states)
   {

@@ -5,7 +5,9 @@
 // whole GPU instead of one CTA:
 //   * planes (column-major, ld = m rounded to 4) live in a per-problem HBM/L2 slot;
 //   * elementwise passes and the projector reductions K^T v run over all CTAs (fp64 atomics);
-//   * B = M V, A = B diag(h) V^T and the Newton-Schulz step are cuBLAS SGEMMs (FP32, no TF32);
+//   * B = M V, A = B diag(h) V^T, the Newton-Schulz step and Algorithm 2's products are the
+//     hand-written batched FP32 GEMM of tilt_dense.cuh (no TF32), its Cayley systems the blocked LU
+//     solve there;
 //   * the Jacobi sweep is block-cyclic: columns in blocks of BW = 16; one round rotates every
 //     cross pair of a block pair (one CTA per block pair; both blocks' columns staged in shared
 //     memory, 16 warps, one column pair per warp, fast scaled rotations as tilt_jacobi.cuh) and
@@ -15,11 +17,11 @@
 // The host drives the iteration (one stream; one host read of an active-problem counter per Jacobi
 // sweep and per LADMAP iteration).
 #define TILT_NO_FREE_KERNELS
-#include <cublas_v2.h>
 
 #include <cstdio>
 #include <cstring>
 
+#include "tilt_dense.cuh"
 #include "tilt_kernels.cuh"
 #include "tilt_large_host.h"
 
@@ -59,7 +61,7 @@ struct St {
   // SVD warm start (Algorithm 2, svd_mode 1; readings Z26/Z27)
   double wacc[8];  // ||M - M_prev||^2, <h0, h1>, ||h1||^2, <h0, h2>, ||P_U||^2, ||P_V||^2
   float eps_svd, t_star;
-  int warm, have_prev, cay_k, warm_steps;
+  int warm, have_prev, warm_steps;
   // Algorithm 1 state (solve entry)
   double tau[8];
   double Q[24];
@@ -565,7 +567,7 @@ __global__ void k_sc1(Args a, int k) {
   if (a.P.rho_replay) rho_bit = a.P.rho_replay[rix(a, b, k)] & 1;
   st->mu_next = fminf(st->mu_max, rho_bit ? a.P.rho0 * st->mu : st->mu);
   st->crit2 = crit2;
-  if (a.P.trace) a.P.trace[4 * (rix(a, b, k)) + 3] = (float)rho_bit;
+  if (a.P.trace) a.P.trace[4 * (rix(a, b, k)) + 3] = (float)(rho_bit + 2 * st->warm);  // + Alg. 2 step
 }
 
 // Cond1, the stop rule (strict), mu <- mu_{k+1}
@@ -962,9 +964,11 @@ __global__ void __launch_bounds__(RNT, 1) k_round(Args a, int r) {
 //   h1 = P_U W + U P_Sigma V^T - W P_V, Z = h1 + U P_Sigma V^T, h2 = -P_U Z + Z P_V,
 //   t* = -<h0, h1> / (||h1||^2 + <h0, h2>), h0 = M - W,
 //   U <- (I + t/2 P_U)^{-1} (I - t/2 P_U) U, Sigma <- Sigma - t P_Sigma, V likewise with P_V,
-// then A = U T_eps(Sigma) V^T. The products are cuBLAS SGEMMs over the batch; the Cayley systems
-// are solved by Richardson iteration X <- R - (t/2) P X (P skew, so it converges when
-// ||(t/2) P||_F < 1; a step with ||(t/2) P||_F >= 0.5 is rejected for a full SVD, reading Z27).
+// then A = U T_eps(Sigma) V^T. The products run in the hand-written batched GEMM (tilt_dense.cuh)
+// on the gated problems only; each Cayley system is solved exactly, as printed, for any t*:
+// X(t) = (I + S)^{-1} (I - S) X = 2 (I + S)^{-1} X - X with S = (t*/2) P skew, by the blocked LU of
+// I + S (no pivoting needed: its symmetric part is I) and two triangular solves. The only rejected
+// step is f''(0) <= 0, where the quadratic model of Eq. ft has no minimiser (reading Z27).
 // ---------------------------------------------------------------------------------------------
 // dst = src diag(vec) (mode 0), src diag(T_eps(vec)) (mode 1); problems with st->warm == want
 __global__ void __launch_bounds__(ENT) k_colscale(Args a, size_t dst, size_t src, size_t vec, int mode, int want) {
@@ -992,7 +996,7 @@ __global__ void __launch_bounds__(ENT) k_copy_if(Args a, size_t dst, size_t src,
 }
 
 // X <- X - X^T in place (an n x n block, leading dimension ld): the skew part of Eqs.
-// projected_gradient1-2; optionally scaled by t*/2 (scale_t)
+// projected_gradient1-2; scale_t: X <- I + (t*/2) X (the Cayley system matrix)
 __global__ void __launch_bounds__(ENT) k_skew(Args a, size_t off, int nn, int ld, int scale_t) {
   const int b = blockIdx.y;
   St* st = state(a, b);
@@ -1002,7 +1006,7 @@ __global__ void __launch_bounds__(ENT) k_skew(Args a, size_t off, int nn, int ld
   FOR_ELEMS((size_t)nn * nn) {
     const int j = (int)(idx / nn), i = (int)(idx % nn);
     if (scale_t) {
-      X[(size_t)j * ld + i] *= f;
+      X[(size_t)j * ld + i] = fmaf(f, X[(size_t)j * ld + i], i == j ? 1.f : 0.f);
     } else if (i < j) {
       const float x = X[(size_t)j * ld + i], y = X[(size_t)i * ld + j];
       X[(size_t)j * ld + i] = x - y;
@@ -1011,6 +1015,15 @@ __global__ void __launch_bounds__(ENT) k_skew(Args a, size_t off, int nn, int ld
       X[(size_t)j * ld + i] = 0.f;
     }
   }
+}
+
+// X <- 2 T - X (the Cayley point from T = (I + S)^{-1} X)
+__global__ void __launch_bounds__(ENT) k_cay_finish(Args a, size_t oX, size_t oT, size_t count) {
+  const int b = blockIdx.y;
+  St* st = state(a, b);
+  if (st->done || !st->warm) return;
+  float* w = slot(a, b);
+  FOR_ELEMS(count) w[oX + idx] = fmaf(2.f, w[oT + idx], -w[oX + idx]);
 }
 
 // ||M - M_prev||_F^2 (the gate of Alg. 2)
@@ -1086,21 +1099,8 @@ __global__ void __launch_bounds__(ENT) k_ws_red(Args a) {
   block_add<3>(s, st->wacc + 1);
 }
 
-// ||X||_F^2 of an nn x nn block (ld) -> wacc[slot]
-__global__ void __launch_bounds__(ENT) k_ws_norm(Args a, size_t off, int nn, int ld, int slotk) {
-  const int b = blockIdx.y;
-  St* st = state(a, b);
-  if (st->done || !st->warm) return;
-  const float* X = slot(a, b) + off;
-  float s[1] = {0.f};
-  FOR_ELEMS((size_t)nn * nn) {
-    const float x = X[(idx / nn) * ld + idx % nn];
-    s[0] = fmaf(x, x, s[0]);
-  }
-  block_add<1>(s, st->wacc + slotk);
-}
-
-// t* = -f'(0)/f''(0) (Eq. ft; 0 when f''(0) <= 0), the Z27 acceptance test and the Richardson count
+// t* = -f'(0)/f''(0) (Eq. ft); f''(0) <= 0 (no minimiser of the quadratic model) rejects the step
+// for a full SVD (reading Z27)
 __global__ void k_ws_t(Args a) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= a.B) return;
@@ -1108,18 +1108,12 @@ __global__ void k_ws_t(Args a) {
   if (st->done || !st->warm) return;
   const double f1 = st->wacc[1], f2 = st->wacc[2] + st->wacc[3];
   const double t = f2 > 0.0 ? -f1 / f2 : 0.0;
-  const double r = 0.5 * fabs(t) * fmax(sqrt(st->wacc[4]), sqrt(st->wacc[5]));
   st->t_star = (float)t;
-  if (!(f2 > 0.0) || !(r < 0.5)) {  // rejected: full SVD (Z27)
+  if (!(f2 > 0.0) || t == 0.0) {
     st->warm = 0;
     return;
   }
-  int K = 1;
-  if (r > 1e-30) K = (int)ceil(log(1e-8) / log(r));
-  K = K < 1 ? 1 : (K > 40 ? 40 : K);
-  st->cay_k = K;
   atomicAdd(a.counter + 1, 1);
-  atomicMax(a.counter + 2, K);
 }
 
 // Sigma <- Sigma - t P_Sigma; |Sigma| for the statistics; count the warm step
@@ -1169,8 +1163,11 @@ __global__ void k_ws_init(Args a, float gate) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= a.B) return;
   St* st = state(a, b);
-  // eps_svd = gate ||D||_F (the oracle's SvdWarm takes the absolute threshold)
+  // eps_svd = gate ||D||_F (the oracle's SvdWarm takes the absolute threshold); every inner loop
+  // starts with full SVDs (a fresh oracle SvdWarm per LADMAP call)
   st->eps_svd = gate * (float)sqrt(st->acc[ACC_R + 2]);
+  st->warm = 0;
+  st->have_prev = 0;
 }
 
 __global__ void __launch_bounds__(ENT) k_dnorm(Args a) {
@@ -1180,16 +1177,6 @@ __global__ void __launch_bounds__(ENT) k_dnorm(Args a) {
   float s[1] = {0.f};
   FOR_ELEMS(a.L.plane) s[0] = fmaf(D[idx], D[idx], s[0]);
   block_add<1>(s, st->acc + ACC_R + 2);
-}
-
-// pointer arrays of a subset GEMM: ptrs[k * nsub + w] = slot(widx[w]) + off_k
-__global__ void k_ptrs(float* ws, size_t stride, const int* __restrict__ widx, int nsub, size_t o0, size_t o1, size_t o2,
-                       void** ptrs) {
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= 3 * nsub) return;
-  const int k = e / nsub, w = e % nsub;
-  const size_t off = k == 0 ? o0 : (k == 1 ? o1 : o2);
-  ptrs[e] = ws + (size_t)widx[w] * stride + off;
 }
 
 // the problems taking the Alg. 2 step (order irrelevant: every problem's GEMMs are independent)
@@ -1605,12 +1592,11 @@ __global__ void k_report_solve(Args a, tilt_report* rep, float* tau_out, const t
 struct Run {
   Ctx& ctx;
   Args a;
-  cublasHandle_t cb;
   tilt_status st = TILT_OK;
   int rpl = 32;
   bool svdws = false;  // LADMAP+SVDWS (DevParams::svd_mode 1)
 
-  explicit Run(Ctx& c) : ctx(c), cb((cublasHandle_t)c.cublas) {}
+  explicit Run(Ctx& c) : ctx(c) {}
 
   bool fail_cuda(cudaError_t e, const char* what) {
     if (e == cudaSuccess) return false;
@@ -1619,12 +1605,6 @@ struct Run {
     return true;
   }
   bool check(const char* what) { return fail_cuda(cudaGetLastError(), what); }
-  bool cub(cublasStatus_t s, const char* what) {
-    if (s == CUBLAS_STATUS_SUCCESS) return false;
-    *ctx.err = std::string(what) + ": cuBLAS status " + std::to_string((int)s);
-    st = TILT_E_CUDA;
-    return true;
-  }
   dim3 egrid(size_t count) const {
     return dim3((unsigned)((count + (size_t)ENT * EPT - 1) / ((size_t)ENT * EPT)), (unsigned)a.B);
   }
@@ -1648,26 +1628,66 @@ struct Run {
     return true;
   }
 
-  // C = op(X) op(Y) with per-problem strides (column-major; cuBLAS FP32, default math: no TF32)
-  int nsub = 0;  // > 0: GEMMs run on the nsub problems listed in ctx.widx only (pointer-array batch)
+  // C = alpha op(X) op(Y) + beta C with per-problem strides (column-major; the hand-written FP32
+  // GEMM of tilt_dense.cuh). nsub > 0: the GEMM runs on the nsub problems listed in ctx.widx only.
+  int nsub = 0;
 
-  bool gemm(cublasOperation_t ta, cublasOperation_t tb, int M, int N, int K, size_t oX, int ldx, size_t oY,
-            int ldy, size_t oC, int ldc, float alpha = 1.f, float beta = 0.f) {
-    if (nsub > 0) {
-      k_ptrs<<<(3 * nsub + 127) / 128, 128, 0, ctx.stream>>>(a.ws, a.L.stride, ctx.widx, nsub, oX, oY, oC, ctx.ptrs);
-      const bool bad = cub(cublasSgemmBatched(cb, ta, tb, M, N, K, &alpha, (const float**)ctx.ptrs, ldx,
-                                              (const float**)(ctx.ptrs + nsub), ldy, &beta, (float**)(ctx.ptrs + 2 * nsub),
-                                              ldc, nsub),
-                           "cublasSgemmBatched");
-      launched(2);
-      return bad;
-    }
-    const long long s = (long long)a.L.stride;
-    const bool bad = cub(cublasSgemmStridedBatched(cb, ta, tb, M, N, K, &alpha, a.ws + oX, ldx, s, a.ws + oY, ldy, s,
-                                                   &beta, a.ws + oC, ldc, s, a.B),
-                         "cublasSgemmStridedBatched");
+  bool gemm(bool ta, bool tb, int M, int N, int K, size_t oX, int ldx, size_t oY, int ldy, size_t oC, int ldc,
+            float alpha = 1.f, float beta = 0.f) {
+    const int nz = nsub > 0 ? nsub : a.B;
+    const int* wi = nsub > 0 ? ctx.widx : nullptr;
+    const dim3 g((M + dense::GBM - 1) / dense::GBM, (N + dense::GBN - 1) / dense::GBN, nz);
+    const size_t s = a.L.stride;
+    if (!ta && !tb)
+      dense::k_gemm<false, false><<<g, dense::GNT, 0, ctx.stream>>>(a.ws, s, wi, M, N, K, oX, ldx, oY, ldy, oC, ldc, alpha, beta);
+    else if (!ta && tb)
+      dense::k_gemm<false, true><<<g, dense::GNT, 0, ctx.stream>>>(a.ws, s, wi, M, N, K, oX, ldx, oY, ldy, oC, ldc, alpha, beta);
+    else if (ta && !tb)
+      dense::k_gemm<true, false><<<g, dense::GNT, 0, ctx.stream>>>(a.ws, s, wi, M, N, K, oX, ldx, oY, ldy, oC, ldc, alpha, beta);
+    else
+      dense::k_gemm<true, true><<<g, dense::GNT, 0, ctx.stream>>>(a.ws, s, wi, M, N, K, oX, ldx, oY, ldy, oC, ldc, alpha, beta);
     launched();
-    return bad;
+    return check("gemm");
+  }
+
+  // (on the nsub problems of ctx.widx) solve P X = X in place: P (Nd x Nd, ldp) is factored in place
+  // by blocked LU without pivoting (tilt_dense.cuh: P = I + S with S skew), X is Nd x ncols (ldx)
+  bool lu_solve(size_t oP, int ldp, int Nd, size_t oX, int ldx, int ncols) {
+    const int nz = nsub;
+    const int* wi = ctx.widx;
+    const size_t s = a.L.stride;
+    cudaStream_t sm = ctx.stream;
+    const int NB = dense::LU_NB;
+    for (int k0 = 0; k0 < Nd; k0 += NB) {
+      const int nb = Nd - k0 < NB ? Nd - k0 : NB;
+      const int rest = Nd - k0 - nb;
+      dense::k_lu_diag<<<dim3(1, 1, nz), 256, 0, sm>>>(a.ws, s, wi, oP, ldp, k0, nb);
+      launched();
+      if (rest > 0) {
+        dense::k_trsm_l<<<dim3((rest + 127) / 128, 1, nz), 128, 0, sm>>>(a.ws, s, wi, oP, ldp, oP, ldp, k0, nb, k0 + nb, rest);
+        dense::k_trsm_ru<<<dim3((rest + 127) / 128, 1, nz), 128, 0, sm>>>(a.ws, s, wi, oP, ldp, k0, nb, rest);
+        launched(2);
+        const size_t o21 = oP + (k0 + nb) + (size_t)k0 * ldp, o12 = oP + k0 + (size_t)(k0 + nb) * ldp;
+        if (gemm(false, false, rest, rest, nb, o21, ldp, o12, ldp, o21 + (size_t)nb * ldp, ldp, -1.f, 1.f)) return true;
+      }
+    }
+    for (int k0 = 0; k0 < Nd; k0 += NB) {  // forward: L Y = X
+      const int nb = Nd - k0 < NB ? Nd - k0 : NB;
+      const int rest = Nd - k0 - nb;
+      dense::k_trsm_l<<<dim3((ncols + 127) / 128, 1, nz), 128, 0, sm>>>(a.ws, s, wi, oP, ldp, oX, ldx, k0, nb, 0, ncols);
+      launched();
+      if (rest > 0 && gemm(false, false, rest, ncols, nb, oP + (k0 + nb) + (size_t)k0 * ldp, ldp, oX + k0, ldx,
+                           oX + k0 + nb, ldx, -1.f, 1.f))
+        return true;
+    }
+    for (int k0 = ((Nd - 1) / NB) * NB; k0 >= 0; k0 -= NB) {  // backward: U X = Y
+      const int nb = Nd - k0 < NB ? Nd - k0 : NB;
+      dense::k_trsm_u<<<dim3((ncols + 127) / 128, 1, nz), 128, 0, sm>>>(a.ws, s, wi, oP, ldp, oX, ldx, k0, nb, ncols);
+      launched();
+      if (k0 > 0 && gemm(false, false, k0, ncols, nb, oP + (size_t)k0 * ldp, ldp, oX + k0, ldx, oX, ldx, -1.f, 1.f))
+        return true;
+    }
+    return check("lu solve");
   }
 
   template <int RPL>
@@ -1716,7 +1736,7 @@ struct Run {
     k_svt_begin<<<sgrid(), 128, 0, ctx.stream>>>(a, eps, eps_mode);
     launched();
     const Lay& L = a.L;
-    if (gemm(CUBLAS_OP_N, CUBLAS_OP_N, L.m, L.n, L.n, L.oS, L.ldm, a.oV, L.ldn, L.oB, L.ldm)) return true;
+    if (gemm(false, false, L.m, L.n, L.n, L.oS, L.ldm, a.oV, L.ldn, L.oB, L.ldm)) return true;
     k_fro<<<egrid(L.plane), ENT, 0, ctx.stream>>>(a);
     launched();
     if (sweeps()) return true;
@@ -1750,68 +1770,54 @@ struct Run {
     const dim3 ep = egrid(L.plane);
     k_colscale<<<ep, ENT, 0, ctx.stream>>>(a, L.oX, L.oU, L.oSg, 0, 1);
     launched();
-    if (gemm(CUBLAS_OP_N, CUBLAS_OP_T, m, n, n, L.oX, ldm, a.oV, ldn, L.oW, ldm)) return true;      // W
-    if (gemm(CUBLAS_OP_N, CUBLAS_OP_T, m, m, n, L.oW, ldm, L.oS, ldm, L.oPU, ldm)) return true;     // W M^T
+    if (gemm(false, true, m, n, n, L.oX, ldm, a.oV, ldn, L.oW, ldm)) return true;      // W
+    if (gemm(false, true, m, m, n, L.oW, ldm, L.oS, ldm, L.oPU, ldm)) return true;     // W M^T
     k_skew<<<egrid((size_t)m * m), ENT, 0, ctx.stream>>>(a, L.oPU, m, ldm, 0);                     // P_U
-    if (gemm(CUBLAS_OP_T, CUBLAS_OP_N, n, n, m, L.oW, ldm, L.oS, ldm, L.oPV, ldn)) return true;     // W^T M
+    if (gemm(true, false, n, n, m, L.oW, ldm, L.oS, ldm, L.oPV, ldn)) return true;     // W^T M
     k_skew<<<egrid((size_t)n * n), ENT, 0, ctx.stream>>>(a, L.oPV, n, ldn, 0);                     // P_V
     launched(2);
-    if (gemm(CUBLAS_OP_N, CUBLAS_OP_N, m, n, n, L.oS, ldm, a.oV, ldn, L.oH2, ldm)) return true;     // M V
+    if (gemm(false, false, m, n, n, L.oS, ldm, a.oV, ldn, L.oH2, ldm)) return true;     // M V
     k_ws_psig<<<dim3((n + 7) / 8, a.B), 256, 0, ctx.stream>>>(a);                                  // P_Sigma
     k_colscale<<<ep, ENT, 0, ctx.stream>>>(a, L.oX2, L.oU, L.oPs, 0, 1);
     launched(2);
-    if (gemm(CUBLAS_OP_N, CUBLAS_OP_T, m, n, n, L.oX2, ldm, a.oV, ldn, L.oZ, ldm)) return true;    // U P_S V^T
+    if (gemm(false, true, m, n, n, L.oX2, ldm, a.oV, ldn, L.oZ, ldm)) return true;    // U P_S V^T
     k_copy_if<<<ep, ENT, 0, ctx.stream>>>(a, L.oH1, L.oZ, L.plane, 1);
     launched();
-    if (gemm(CUBLAS_OP_N, CUBLAS_OP_N, m, n, m, L.oPU, ldm, L.oW, ldm, L.oH1, ldm, 1.f, 1.f)) return true;
-    if (gemm(CUBLAS_OP_N, CUBLAS_OP_N, m, n, n, L.oW, ldm, L.oPV, ldn, L.oH1, ldm, -1.f, 1.f)) return true;
+    if (gemm(false, false, m, n, m, L.oPU, ldm, L.oW, ldm, L.oH1, ldm, 1.f, 1.f)) return true;
+    if (gemm(false, false, m, n, n, L.oW, ldm, L.oPV, ldn, L.oH1, ldm, -1.f, 1.f)) return true;
     k_ws_z<<<ep, ENT, 0, ctx.stream>>>(a);                                                          // Z
     launched();
-    if (gemm(CUBLAS_OP_N, CUBLAS_OP_N, m, n, m, L.oPU, ldm, L.oZ, ldm, L.oH2, ldm, -1.f, 0.f)) return true;
-    if (gemm(CUBLAS_OP_N, CUBLAS_OP_N, m, n, n, L.oZ, ldm, L.oPV, ldn, L.oH2, ldm, 1.f, 1.f)) return true;
+    if (gemm(false, false, m, n, m, L.oPU, ldm, L.oZ, ldm, L.oH2, ldm, -1.f, 0.f)) return true;
+    if (gemm(false, false, m, n, n, L.oZ, ldm, L.oPV, ldn, L.oH2, ldm, 1.f, 1.f)) return true;
     k_ws_red<<<ep, ENT, 0, ctx.stream>>>(a);
-    k_ws_norm<<<egrid((size_t)m * m), ENT, 0, ctx.stream>>>(a, L.oPU, m, ldm, 4);
-    k_ws_norm<<<egrid((size_t)n * n), ENT, 0, ctx.stream>>>(a, L.oPV, n, ldn, 5);
-    launched(3);
+    launched();
     if (zero_counter()) return true;
     k_ws_t<<<sgrid(), 128, 0, ctx.stream>>>(a);
     launched();
     return check("svd warm step (1)");
   }
 
-  // Cayley update X <- (I + S)^{-1} (I - S) X0 for S = (t/2) P (already scaled) by Richardson
-  // iteration: R = X0 - S X0, X_{k+1} = R - S X_k (K iterations); the result lands in `dst`
-  bool cayley(size_t oP, int ldp, size_t oX0, size_t oR, size_t oA1, size_t oA2, int rows, int cols, int ldx,
-              size_t count, int K, size_t dst) {
+  // Cayley update X <- (I + S)^{-1} (I - S) X = 2 (I + S)^{-1} X - X, S = (t*/2) P skew, exactly:
+  // P holds I + S (k_skew scale_t), factored in place; `tmp` (rows x cols, ldx) receives the solve
+  bool cayley(size_t oP, int ldp, size_t oX, size_t tmp, int rows, int cols, int ldx, size_t count) {
     const dim3 eg = egrid(count);
-    k_copy_if<<<eg, ENT, 0, ctx.stream>>>(a, oR, oX0, count, 1);
+    k_copy_if<<<eg, ENT, 0, ctx.stream>>>(a, tmp, oX, count, 1);
     launched();
-    if (gemm(CUBLAS_OP_N, CUBLAS_OP_N, rows, cols, rows, oP, ldp, oX0, ldx, oR, ldx, -1.f, 1.f)) return true;
-    k_copy_if<<<eg, ENT, 0, ctx.stream>>>(a, oA1, oR, count, 1);
-    launched();
-    size_t cur = oA1, nxt = oA2;
-    for (int it = 0; it < K; ++it) {
-      k_copy_if<<<eg, ENT, 0, ctx.stream>>>(a, nxt, oR, count, 1);
-      launched();
-      if (gemm(CUBLAS_OP_N, CUBLAS_OP_N, rows, cols, rows, oP, ldp, cur, ldx, nxt, ldx, -1.f, 1.f)) return true;
-      const size_t t = cur;
-      cur = nxt;
-      nxt = t;
-    }
-    k_copy_if<<<eg, ENT, 0, ctx.stream>>>(a, dst, cur, count, 1);
+    if (lu_solve(oP, ldp, rows, tmp, ldx, cols)) return true;
+    k_cay_finish<<<eg, ENT, 0, ctx.stream>>>(a, oX, tmp, count);
     launched();
     return check("cayley");
   }
 
   // Alg. 2, second half: U(t), V(t), Sigma(t); B <- U T_eps(Sigma) so that A = B V^T for every problem
-  bool ws_part2(int K) {
+  bool ws_part2() {
     const Lay& L = a.L;
     const int m = L.m, n = L.n, ldm = L.ldm, ldn = L.ldn;
-    k_skew<<<egrid((size_t)m * m), ENT, 0, ctx.stream>>>(a, L.oPU, m, ldm, 1);  // (t/2) P_U
-    k_skew<<<egrid((size_t)n * n), ENT, 0, ctx.stream>>>(a, L.oPV, n, ldn, 1);  // (t/2) P_V
+    k_skew<<<egrid((size_t)m * m), ENT, 0, ctx.stream>>>(a, L.oPU, m, ldm, 1);  // I + (t/2) P_U
+    k_skew<<<egrid((size_t)n * n), ENT, 0, ctx.stream>>>(a, L.oPV, n, ldn, 1);  // I + (t/2) P_V
     launched(2);
-    if (cayley(L.oPU, ldm, L.oU, L.oX, L.oX2, L.oH2, m, n, ldm, L.plane, K, L.oU)) return true;
-    if (cayley(L.oPV, ldn, a.oV, L.oVt, L.oVt2, L.oT, n, n, ldn, L.vplane, K, a.oV)) return true;
+    if (cayley(L.oPU, ldm, L.oU, L.oX, m, n, ldm, L.plane)) return true;
+    if (cayley(L.oPV, ldn, a.oV, L.oVt, n, n, ldn, L.vplane)) return true;
     k_ws_sigma<<<dim3((n + 127) / 128, a.B), 128, 0, ctx.stream>>>(a);
     k_svt_stats<<<a.B, 32, 0, ctx.stream>>>(a, 0, 1);
     k_colscale<<<egrid(L.plane), ENT, 0, ctx.stream>>>(a, L.oB, L.oU, L.oSg, 1, 1);
@@ -1821,11 +1827,11 @@ struct Run {
 
   bool ns_step() {
     const Lay& L = a.L;
-    if (gemm(CUBLAS_OP_T, CUBLAS_OP_N, L.n, L.n, L.n, a.oV, L.ldn, a.oV, L.ldn, L.oT, L.ldn)) return true;
+    if (gemm(true, false, L.n, L.n, L.n, a.oV, L.ldn, a.oV, L.ldn, L.oT, L.ldn)) return true;
     k_ns_mid<<<egrid(L.vplane), ENT, 0, ctx.stream>>>(a);
     launched();
     const size_t other = a.oV == L.oV ? L.oV2 : L.oV;
-    if (gemm(CUBLAS_OP_N, CUBLAS_OP_N, L.n, L.n, L.n, a.oV, L.ldn, L.oT, L.ldn, other, L.ldn)) return true;
+    if (gemm(false, false, L.n, L.n, L.n, a.oV, L.ldn, L.oT, L.ldn, other, L.ldn)) return true;
     a.oV = other;
     return check("ns");
   }
@@ -1865,24 +1871,11 @@ tilt_status ensure(Ctx& ctx, size_t floats, int B) {
   }
   if (ctx.cap_b < B) {
     if (ctx.widx) cudaFree(ctx.widx);
-    if (ctx.ptrs) cudaFree(ctx.ptrs);
     ctx.widx = nullptr;
-    ctx.ptrs = nullptr;
     ctx.cap_b = 0;
     if (cudaMalloc(&ctx.widx, (size_t)B * sizeof(int)) != cudaSuccess) return TILT_E_OOM;
-    if (cudaMalloc(&ctx.ptrs, (size_t)3 * B * sizeof(void*)) != cudaSuccess) return TILT_E_OOM;
     ctx.cap_b = B;
   }
-  if (!ctx.cublas) {
-    cublasHandle_t h;
-    if (cublasCreate(&h) != CUBLAS_STATUS_SUCCESS) {
-      *ctx.err = "cublasCreate failed";
-      return TILT_E_CUDA;
-    }
-    cublasSetMathMode(h, CUBLAS_DEFAULT_MATH);  // FP32 SGEMM, no TF32 (the 1e-4 parity needs FP32)
-    ctx.cublas = h;
-  }
-  cublasSetStream((cublasHandle_t)ctx.cublas, ctx.stream);
   if (ctx.ws_floats < floats) {
     if (ctx.ws) cudaFree(ctx.ws);
     ctx.ws = nullptr;
@@ -1899,10 +1892,8 @@ tilt_status ensure(Ctx& ctx, size_t floats, int B) {
 void release(Ctx& ctx) {
   if (ctx.ws) cudaFree(ctx.ws);
   if (ctx.widx) cudaFree(ctx.widx);
-  if (ctx.ptrs) cudaFree(ctx.ptrs);
   if (ctx.counter) cudaFree(ctx.counter);
   if (ctx.h_counter) cudaFreeHost(ctx.h_counter);
-  if (ctx.cublas) cublasDestroy((cublasHandle_t)ctx.cublas);
   ctx = Ctx();
 }
 
@@ -1967,7 +1958,7 @@ static bool inner_core(Run& R, const DevParams& P, const float* Q, int l, int q_
       k_adm_m<<<R.egrid(L.plane), ENT, 0, sm>>>(a);
       R.launched();
       if (R.svt_core(nullptr, 0, 1, true)) return true;
-      if (R.gemm(CUBLAS_OP_N, CUBLAS_OP_T, m, n, n, L.oB, L.ldm, a.oV, L.ldn, L.oA, L.ldm)) return true;
+      if (R.gemm(false, true, m, n, n, L.oB, L.ldm, a.oV, L.ldn, L.oA, L.ldm)) return true;
       if (warm && (k % P.ns_period == P.ns_period - 1 || k + 1 == a.niter))
         if (R.ns_step()) return true;
       k_adm_e<<<R.egrid(L.plane), ENT, 0, sm>>>(a);
@@ -1991,7 +1982,7 @@ static bool inner_core(Run& R, const DevParams& P, const float* Q, int l, int q_
       k_identity<<<R.egrid(L.vplane), ENT, 0, sm>>>(a, a.oV);
       R.launched();
     }
-    int nwarm = 0, K = 0;
+    int nwarm = 0;
     if (R.svdws && k > 0) {  // Alg. 2 gate, then the warm step's first half for the gated problems
       if (R.zero_counter()) return true;
       k_ws_diff<<<R.egrid(L.plane), ENT, 0, sm>>>(a);
@@ -2005,16 +1996,15 @@ static bool inner_core(Run& R, const DevParams& P, const float* Q, int l, int q_
         R.nsub = 0;
         if (!R.read_counters(c)) return true;
         nwarm = c[1];
-        K = c[2];
       }
     }
     if (R.svt_core(nullptr, 0, 1, true, R.svdws)) return true;
     if (nwarm > 0) {
       if (R.ws_subset(nwarm)) return true;
-      if (R.ws_part2(K)) return true;
+      if (R.ws_part2()) return true;
       R.nsub = 0;
     }
-    if (R.gemm(CUBLAS_OP_N, CUBLAS_OP_T, m, n, n, L.oB, L.ldm, a.oV, L.ldn, L.oAn, L.ldm)) return true;
+    if (R.gemm(false, true, m, n, n, L.oB, L.ldm, a.oV, L.ldn, L.oAn, L.ldm)) return true;
     if (warm && (k % P.ns_period == P.ns_period - 1 || k + 1 == a.niter))
       if (R.ns_step()) return true;
     if (R.svdws) {
@@ -2192,7 +2182,7 @@ tilt_status svt(Ctx& ctx, const float* M, int B, int m, int n, const float* eps,
   }
   R.launched();
   if (R.svt_core(eps, 1, 0, true)) return R.st;
-  if (R.gemm(CUBLAS_OP_N, CUBLAS_OP_T, m, n, n, L.oB, L.ldm, a.oV, L.ldn, L.oAn, L.ldm)) return R.st;
+  if (R.gemm(false, true, m, n, n, L.oB, L.ldm, a.oV, L.ldn, L.oAn, L.ldm)) return R.st;
   k_from_plane<<<dim3((n + 31) / 32, (m + 31) / 32, B), dim3(32, 8), 0, sm>>>(A, a, L.oAn, m, n, L.ldm, 0);
   k_svt_out<<<dim3((n + 127) / 128, B), 128, 0, sm>>>(a, sigma, sweeps);
   R.launched(2);

@@ -23,18 +23,16 @@ struct Ctx {
   float* ws = nullptr;       // per-problem slots (planes, V buffers, state)
   size_t ws_floats = 0;
   int* counter = nullptr;    // device: active-problem counter
-  int* widx = nullptr;       // device: indices of the problems in a subset GEMM (Alg. 2 steps)
-  void** ptrs = nullptr;     // device: pointer arrays of a subset GEMM (3 x cap_b)
+  int* widx = nullptr;       // device: indices of the problems in a subset GEMM / solve (Alg. 2 steps)
   int cap_b = 0;
   int* h_counter = nullptr;  // pinned host mirror
-  void* cublas = nullptr;    // cublasHandle_t
   int64_t* launches = nullptr;
   std::string* err = nullptr;
 };
 
 // workspace floats of B problems of size m x n with p Jacobian planes
 size_t ws_need(int B, int m, int n, int p, bool svdws = false);
-// (re)allocate ctx.ws for at least `floats` floats and create the cuBLAS handle
+// (re)allocate ctx.ws for at least `floats` floats
 tilt_status ensure(Ctx& ctx, size_t floats, int B);
 void release(Ctx& ctx);
 

@@ -199,7 +199,7 @@ class TiltSolver:
         B, p, m, n = J.shape
         Q_t = _dev(Q, torch.float32, dev)
         l = 0 if Q is None else int(Q_t.shape[1])
-        prm = params if params is not None else default_params()
+        prm = TiltParams.from_buffer_copy(params) if params is not None else default_params()
         rr = None
         tr = None
         if rho_replay is not None:

@@ -161,11 +161,12 @@ def _svdws_ref(D, J, lam, K, gate):
     return r, sw
 
 
-@pytest.mark.parametrize("n,gate", [(100, 1e-4), (300, 1e-4), (200, 1e-3)])
+@pytest.mark.parametrize("n,gate", [(100, 1e-4), (300, 1e-4), (200, 1e-3), (150, 1e-2), (130, 3e-2)])
 def test_svdws_fixed_count_parity(solver, T, n, gate):
     """A fixed count of LADMAP+SVDWS iterations with the oracle's rho decisions and warm/full
     decisions replayed (bits 0 and 2): both compute the same Cayley-curve step (Appendix A) from the
-    same previous SVD, so A and E agree to the fixed-count bar (1e-4)."""
+    same previous SVD, with the Cayley systems solved exactly (any t*, reading Z27), so A and E agree
+    to the fixed-count bar (1e-4). The wide gates take steps with ||(t*/2) P||_F >= 0.5."""
     K, B = 20, 2
     insts = [ts.table1_instance(n, 6, s) for s in range(B)]
     D = np.stack([i["D"] for i in insts]).astype(np.float32)
@@ -177,6 +178,8 @@ def test_svdws_fixed_count_parity(solver, T, n, gate):
     prm = T.default_params(fixed_inner_iters=K, max_inner=K, kernel_path=3, svd_mode=1, svd_ws_gate=gate)
     out = solver.inner(D, J, params=prm, rho_replay=bits)
     rep = out["rep"]
+    if gate >= 1e-2:
+        assert max(max(sw.cayley_sizes, default=0.0) for _, sw in refs) >= 0.5
     for k, (r, sw) in enumerate(refs):
         assert rep["svd_warm_steps"][k] == sw.warm_steps
         a = out["A"][k].double().cpu().numpy()
@@ -184,6 +187,49 @@ def test_svdws_fixed_count_parity(solver, T, n, gate):
         ra = np.linalg.norm(a - r.A) / np.linalg.norm(r.A)
         re = np.linalg.norm(e - r.E) / max(np.linalg.norm(r.E), 1e-30)
         assert ra < 1e-4 and re < 1e-4, (n, gate, k, ra, re, sw.decisions)
+
+
+@pytest.mark.parametrize("n,gate", [(100, 1e-3), (200, 1e-3)])
+def test_svdws_free_running_gate_agreement(solver, T, n, gate):
+    """LADMAP+SVDWS free-running on both sides (no rho, stop or warm/full replay): the GPU's own
+    gate ||M_k - M_{k-1}||_F < eps_svd and its own f''(0) test decide every step. Printed: the
+    per-iteration agreement of the warm/full decisions with the oracle's; asserted: the inner loops
+    stop within 2 iterations of the oracle's, the objective within 1e-3, and the decisions agree on
+    at least 90% of the common iterations."""
+    B = 2
+    insts = [ts.table1_instance(n, 6, s) for s in range(B)]
+    D = np.stack([i["D"] for i in insts]).astype(np.float32)
+    J = np.stack([i["J"] for i in insts]).astype(np.float32)
+    lam = insts[0]["lam"]
+    K = 1000
+    refs = []
+    for k in range(B):
+        d, j = D[k].astype(np.float64), J[k].astype(np.float64)
+        proj = O.Projector(j, None)
+        mu0 = 1.25 / np.linalg.svd(d, compute_uv=False)[0]
+        z = np.zeros_like(d)
+        sw = O.SvdWarm(gate * np.linalg.norm(d))
+        r = O.ladmap(d, proj, lam, mu0, 1e6 * mu0, 2.0, 1e-6, 0.1, K, d.copy(), z, z, svd=sw)
+        refs.append((r, sw))
+    prm = T.default_params(kernel_path=3, svd_mode=1, svd_ws_gate=gate, max_inner=K)
+    out = solver.inner(D, J, params=prm, trace=True)
+    rep = out["rep"]
+    agree = total = 0
+    for k, (r, sw) in enumerate(refs):
+        assert rep["status"][k] == T.CONVERGED
+        its = int(rep["inner_iters"][k])
+        assert abs(its - r.iters) <= 2, (k, its, r.iters)
+        assert rep["objective"][k] == pytest.approx(O.objective(r.A, r.E, lam), rel=1e-3)
+        dec = (out["trace"][k, :its, 3].cpu().numpy() >= 2).astype(int)  # trace rho slot + 2 * warm step
+        assert int(dec.sum()) == int(rep["svd_warm_steps"][k]) and dec.sum() > 0
+        c = min(its, r.iters)
+        agree += int(np.sum(dec[:c] == np.asarray(sw.decisions[:c])))
+        total += c
+        print(f"n={n} gate={gate} problem {k}: warm steps GPU {int(dec.sum())} / {its} iterations, "
+              f"oracle {sw.warm_steps} / {r.iters}")
+    print(f"n={n} gate={gate}: gate decisions agree on {agree} of {total} common iterations "
+          f"({100.0 * agree / total:.1f}%)")
+    assert agree >= 0.9 * total
 
 
 def test_svdws_free_running_keeps_ladmap_objective(solver, T):
