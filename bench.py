@@ -244,6 +244,8 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     t_gen = time.perf_counter()
     batch = gen_shard(CFG_ID, idx)
     t_gen = time.perf_counter() - t_gen
+    if rank == 0:
+        print(f"[bench] generated {S} patches in {t_gen:.1f} s", file=sys.stderr, flush=True)
     slabs = slab_bounds(S, args.steps)
     cap = max(hi - lo for lo, hi in slabs)
     images = torch.as_tensor(batch["images"], device=dev)
@@ -306,6 +308,8 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     launches = sum(s.launches for s in solvers) - launches0
     clk = clocks.stop() if clocks else None
     elapsed = t0.elapsed_time(t1) / 1e3
+    if rank == 0:
+        print(f"[bench] timed region {elapsed:.2f} s ({args.steps} steps)", file=sys.stderr, flush=True)
     rep = T.reports_to_numpy(out["rep"])
     conv = int(np.sum(rep["status"] == T.CONVERGED))
     inner = int(np.sum(rep["inner_iters"], dtype=np.int64))
@@ -424,8 +428,8 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
                           "note": "tau, reports, A, E of every patch to rank 0, inside the timed region"}
     if world == 1 and not args.no_k1:
         k1n = min(S, args.k1_batch)
-        line["roofline_k1"] = k1_roofline(solvers[0], images[:k1n], pimg[:k1n], boxes[:k1n], tau0[:k1n], kind, m, n,
-                                          p, _peaks())
+        line["roofline_k1"] = k1_roofline(solvers[0], images[:k1n], torch.arange(k1n, dtype=torch.int32, device=dev),
+                                          boxes[:k1n], tau0[:k1n], kind, m, n, p, _peaks())
     if e2e_line is not None:
         line["e2e"] = e2e_line
     if world == 1 and not args.no_cpu:
@@ -527,6 +531,7 @@ def e2e(solvers, batch, slabs, kind, prm, p, m, n) -> dict:
     for th in threads:
         th.join()
     t = time.perf_counter() - t0
+    print(f"[bench] e2e pass {t:.2f} s", file=sys.stderr, flush=True)
     conv = int(np.sum(rep["status"] == 0))
     h2d = pin["images"].nbytes + S * 4 + pin["boxes"].nbytes + pin["tau0"].nbytes
     d2h = S * p * 4 + 2 * S * m * n * 4 + S * REPORT_BYTES

@@ -62,6 +62,9 @@ class Params:
                                 # 1e-7 reproduces Table 1's ADM counts in fp64, 1e-6 is fp32-resolvable)
     pyramid_warm: bool = False  # 2-level pyramid: the fine level's first inner loop starts from the
                                 # coarse A, E, Y upsampled (reading Z26)
+    crit_noise: float = 0.0     # test instrumentation (reading Z22): Cond1's statistic is compared as
+    noise_seed: int = 0         # crit1 (1 + crit_noise N(0,1)) -- the relative resolution of an fp32
+                                # crit1 near eps1 -- to classify decision-sensitive patches; 0 = exact
 
 
 # ----------------------------------------------------------------------------------------------
@@ -464,7 +467,7 @@ class InnerResult:
 
 
 def ladmap(dh, proj, lam, mu0, mu_max, rho0, eps1, eps2, max_inner, a0, e0, y0,
-           fixed_iters=0, rho_replay=None, svd="lapack"):
+           fixed_iters=0, rho_replay=None, svd="lapack", crit_noise=None):
     """LADMAP for min ||A||_* + lam ||E||_1  s.t.  W^T W (A + E) = W^T W D  (Eq. reformulated_TILT2).
 
     Iteration (Eq. newvars2, with errata E1 (+ sign of the dual step, as Eq. Y)
@@ -480,6 +483,8 @@ def ladmap(dh, proj, lam, mu0, mu_max, rho0, eps1, eps2, max_inner, a0, e0, y0,
     projector applications are made per iteration. Stop when Cond1 and Cond2 hold (P:489-497,
     strict inequalities, reading Z12), unless ``fixed_iters`` > 0 (test mode).
     ``rho_replay`` (sequence of 0/1) overrides the rho decision (parity protocol, reading Z21).
+    ``crit_noise`` = (scale, numpy Generator) perturbs the statistic Cond1 tests (test
+    instrumentation of reading Z22: the stop decision as resolved by fp32 arithmetic); None = exact.
     """
     denom = float(np.linalg.norm(proj.apply(dh)))
     if denom == 0.0:  # D in span(J): the crit denominators degenerate; use 1 (reading R9)
@@ -503,12 +508,13 @@ def ladmap(dh, proj, lam, mu0, mu_max, rho0, eps1, eps2, max_inner, a0, e0, y0,
         crit1 = float(np.linalg.norm(r)) / denom
         crit2 = mu * max(float(np.linalg.norm(a1 - a)), float(np.linalg.norm(e1 - e))) / denom
         a, e = a1, e1
+        c1_test = crit1 if crit_noise is None else crit1 * (1.0 + crit_noise[0] * crit_noise[1].standard_normal())
         rho_bit = 1 if crit2 < eps2 else 0
         if rho_replay is not None and k < len(rho_replay):
             rho_bit = int(rho_replay[k])
         trace.append((mu, crit1, crit2, rho_bit))
         mu_used = mu
-        if crit1 < eps1 and crit2 < eps2:
+        if c1_test < eps1 and crit2 < eps2:
             converged = True
             if fixed_iters <= 0:
                 return InnerResult(a, e, y, k + 1, mu_used, sig, crit1, crit2, trace, True)
@@ -606,6 +612,7 @@ def tilt(image, box, tau0, kind, prm: Params = Params(), rho_replay=None, warm=N
     status = MAX_OUTER
     stop_rule = STOP_NONE
     outer_traces = []
+    tau_path = []       # tau after every outer iteration (test instrumentation)
     inner_iters = 0
     res = None
     nd = float("nan")
@@ -644,13 +651,17 @@ def tilt(image, box, tau0, kind, prm: Params = Params(), rho_replay=None, warm=N
             else:
                 y = proj.apply(y)                      # Eq. Y_new_warmstart
             replay = rho_replay[it] if rho_replay is not None and it < len(rho_replay) else None
+            noise = ((prm.crit_noise, np.random.default_rng([prm.noise_seed, it]))
+                     if prm.crit_noise > 0 else None)
             res = ladmap(dh, proj, lam, mu0, prm.mu_max_ratio * mu0, prm.rho0, prm.eps1, prm.eps2,
-                         prm.max_inner, a, e, y, fixed_iters=prm.fixed_inner_iters, rho_replay=replay, svd=prm.svd)
+                         prm.max_inner, a, e, y, fixed_iters=prm.fixed_inner_iters, rho_replay=replay, svd=prm.svd,
+                         crit_noise=noise)
             a, e, y = res.A, res.E, res.Y
             inner_iters += res.iters
             outer_traces.append(res.trace)
             dtau = proj.delta_tau(a + e - dh)          # Step 3
         tau = tau + dtau                           # Step 4
+        tau_path.append(tau.copy())
         dtau_inf = float(np.max(np.abs(dtau)))
         f = float(shrink(res.sigma_m, 1.0 / res.mu).sum()) + lam * float(np.abs(e).sum())
         it_done = it + 1
@@ -677,7 +688,7 @@ def tilt(image, box, tau0, kind, prm: Params = Params(), rho_replay=None, warm=N
         "rank": rank, "rank_band": band, "svt_rank": int(np.sum(res.sigma_m > 1.0 / res.mu)) if res else 0,
         "crit1": (res.resid if isinstance(res, AdmResult) else res.crit1) if res else float("nan"),
         "crit2": (float("nan") if isinstance(res, AdmResult) else res.crit2) if res else float("nan"),
-        "patch_norm": nd, "dtau_inf": dtau_inf, "traces": outer_traces, "lam": lam,
+        "patch_norm": nd, "dtau_inf": dtau_inf, "traces": outer_traces, "lam": lam, "tau_path": tau_path,
     }
 
 

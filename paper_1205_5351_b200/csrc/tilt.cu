@@ -5,7 +5,9 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <string>
+#include <vector>
 
 #include "tilt_kernels.cuh"
 #include "tilt_large_host.h"
@@ -39,6 +41,91 @@ SizeClass size_class(int m, int n) {
   if (d <= 128) return SC128;
   if (d <= 256) return n <= 216 ? SC256 : SC256G;  // B in shared memory while MAXD x n floats fit
   return SC_NONE;
+}
+
+// Jacobi pair schedule with column reuse (tilt_jacobi.cuh, g_sched): returns the number of rounds,
+// or -1 if a node needs more units than available (then the kernels keep the round-robin order).
+int build_jacobi_schedule(int n, int units, std::vector<uint16_t>& out) {
+  struct Node {
+    int lo, hi;
+  };
+  std::vector<Node> nodes{{0, n}};
+  int rounds = 0;
+  while (true) {
+    std::vector<Node> live;
+    for (const Node& x : nodes)
+      if (x.hi - x.lo >= 2) live.push_back(x);
+    if (live.empty()) break;
+    size_t g0 = 0;
+    while (g0 < live.size()) {  // nodes of one depth side by side, as many as the units allow
+      int used = 0, dur = 0;
+      size_t g1 = g0;
+      while (g1 < live.size()) {
+        const int f = (live[g1].hi - live[g1].lo + 1) / 2;
+        if (used + f > units) break;
+        used += f;
+        dur = f > dur ? f : dur;
+        ++g1;
+      }
+      if (g1 == g0) return -1;
+      for (int r = 0; r < dur; ++r) {
+        out.insert(out.end(), units, (uint16_t)0xFFFF);
+        uint16_t* row = out.data() + out.size() - units;
+        int uo = 0;
+        for (size_t q = g0; q < g1; ++q) {
+          const int lo = live[q].lo, L = live[q].hi - lo, f = (L + 1) / 2, m = L - f;
+          if (r < f)
+            for (int u = 0; u < f; ++u) {
+              const int mi = (u + r) % f;
+              row[uo + u] = (uint16_t)(((lo + u) << 8) | (mi < m ? lo + f + mi : 0xFF));
+            }
+          uo += f;
+        }
+        ++rounds;
+      }
+      g0 = g1;
+    }
+    std::vector<Node> next;
+    for (const Node& x : live) {
+      const int f = (x.hi - x.lo + 1) / 2;
+      next.push_back({x.lo, x.lo + f});
+      next.push_back({x.lo + f, x.hi});
+    }
+    nodes.swap(next);
+  }
+  return rounds;
+}
+
+// upload the schedules for n = 2 .. SCHED_MAXN, 32 and 64 units, once per device
+tilt_status init_schedules(int device) {
+  static std::mutex mu;
+  static bool done[128] = {false};
+  std::lock_guard<std::mutex> lk(mu);
+  if (device < 0 || device >= 128) return TILT_E_ARG;
+  if (done[device]) return TILT_OK;
+  std::vector<uint16_t> tab;
+  int off[2][SCHED_MAXN + 1], rounds[2][SCHED_MAXN + 1];
+  for (int c = 0; c < 2; ++c)
+    for (int n = 0; n <= SCHED_MAXN; ++n) {
+      off[c][n] = (int)tab.size();
+      rounds[c][n] = 0;
+      if (n < 2) continue;
+      std::vector<uint16_t> t;
+      const int r = build_jacobi_schedule(n, c == 0 ? 32 : 64, t);
+      if (r > 0 && n <= (c == 0 ? 64 : 128)) {
+        rounds[c][n] = r;
+        tab.insert(tab.end(), t.begin(), t.end());
+      }
+    }
+  uint16_t* d = nullptr;
+  TILT_CUDA(cudaMalloc(&d, tab.size() * sizeof(uint16_t)));  // one table per device, kept for the process
+  TILT_CUDA(cudaMemcpy(d, tab.data(), tab.size() * sizeof(uint16_t), cudaMemcpyHostToDevice));
+  const uint16_t* dc = d;
+  TILT_CUDA(cudaMemcpyToSymbol(g_sched, &dc, sizeof(dc)));
+  TILT_CUDA(cudaMemcpyToSymbol(c_sched_off, off, sizeof(off)));
+  TILT_CUDA(cudaMemcpyToSymbol(c_sched_rounds, rounds, sizeof(rounds)));
+  done[device] = true;
+  return TILT_OK;
 }
 
 }  // namespace
@@ -423,6 +510,13 @@ tilt_status tilt_create(tilt_handle** out, const tilt_create_opts* o) {
     delete h;
     return s;
   }
+  {
+    const tilt_status ss = init_schedules(h->device);
+    if (ss != TILT_OK) {
+      delete h;
+      return ss;
+    }
+  }
   auto fail = [&](cudaError_t err, const char* what) {
     cuda_fail(err, what);
     tilt_destroy(h);
@@ -706,7 +800,7 @@ tilt_status tilt_warp_batch(tilt_handle* h, const float* images, int32_t n_image
     tilt_status s = first_box(h, boxes, &m, &n);
     if (s != TILT_OK) return s;
   }
-  if (m < 2 || n < 2 || (size_t)m * n * sizeof(float4) > 227 * 1024) return TILT_E_ARG;
+  if (m < 2 || n < 2 || m > tilt::lp::MAX_DIM || n > tilt::lp::MAX_DIM) return TILT_E_ARG;
   WarpArgs a;
   a.images = images;
   a.n_images = n_images;
@@ -725,6 +819,7 @@ tilt_status tilt_warp_batch(tilt_handle* h, const float* images, int32_t n_image
   a.norm = norm;
   a.status = status;
   const size_t k1_smem = (size_t)m * n * sizeof(float4);  // (d, gx, gy, gz) per window pixel
+  if (k1_smem > 227 * 1024) return TILT_E_ARG;
   if (k1_smem > 48 * 1024) TILT_CUDA(cudaFuncSetAttribute((const void*)k_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k1_smem));
   k_warp<<<B, K1_NT, k1_smem, h->stream>>>(a);
   h->launches++;
@@ -839,6 +934,17 @@ tilt_status tilt_inner_batch(tilt_handle* h, const float* D, const float* J, con
     return TILT_OK;
   }
   return dispatch<InnerF>(size_class(m, n), h, a);
+}
+
+// host-side check of the Jacobi pair schedule (no GPU needed): rounds, or -1 / -2 (cap too small)
+int32_t tilt_jacobi_schedule(int32_t n, int32_t units, uint16_t* out, int32_t cap) {
+  if (n < 2 || n > 255 || units < 1) return -1;
+  std::vector<uint16_t> t;
+  const int r = build_jacobi_schedule(n, units, t);
+  if (r < 0) return -1;
+  if ((int64_t)t.size() > cap) return -2;
+  if (out) memcpy(out, t.data(), t.size() * sizeof(uint16_t));
+  return r;
 }
 
 }  // extern "C"

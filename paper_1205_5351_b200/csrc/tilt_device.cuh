@@ -424,30 +424,68 @@ __device__ __forceinline__ WarpGeom make_geom(const int* box, const double* tau,
 // Bilinear sample d and the Jacobian factors (gx, gy, gz) at window pixel (i, j):
 // J_raw = (gx u, gx v, gy u, gy v, gx, gy, gz u, gz v) with gx = s I_X / w, gy = s I_Y / w,
 // gz = -(gx x + gy y) (normalised frame). Returns false on window escape.
-__device__ __forceinline__ bool warp_pixel(const WarpGeom& g, const float* __restrict__ img, int H, int W,
-                                           int i, int j, double& d, double& gx, double& gy, double& gz) {
+// The one Step-1 pixel routine of every kernel (the standalone K1 k_warp, the CTA-per-patch solve,
+// the warp-per-patch and multi-CTA paths): the source coordinate in fp64 (an fp32 coordinate of a
+// 100-pixel canvas would carry ~6e-6 px of rounding into the fractions), the 4 taps, the bilinear
+// value and the exact interpolant gradient (reading Z2) in fp32 from the fp32 fractions.
+struct WarpTap {
+  int off;                    // yi * W + xi of the cell's top-left tap
+  float fx, fy, sw, xn, yn;   // fractions, s / w, normalised source coordinate
+  bool ok;                    // the 4-tap stencil lies inside the image
+};
+
+// fp64 geometry of window pixel (i, j): source coordinate (Z15, Z16), cell by floor, escape test (Z2)
+__device__ __forceinline__ WarpTap warp_tap(const WarpGeom& g, int H, int W, int i, int j) {
   const double du = j - 0.5 * (g.n - 1);
   const double dv = i - 0.5 * (g.m - 1);
   const double w = 1.0 + (g.h31 * du + g.h32 * dv) / g.s;
   const double X = g.cx + (g.h11 * du + g.h12 * dv + g.s * g.h13) / w;
   const double Y = g.cy + (g.h21 * du + g.h22 * dv + g.s * g.h23) / w;
   const double X0 = floor(X), Y0 = floor(Y);
-  if (!(X0 >= 0.0 && X0 + 1.0 <= W - 1 && Y0 >= 0.0 && Y0 + 1.0 <= H - 1)) {
-    d = gx = gy = gz = 0.0;
+  WarpTap t;
+  t.ok = X0 >= 0.0 && X0 + 1.0 <= W - 1 && Y0 >= 0.0 && Y0 + 1.0 <= H - 1;
+  t.off = t.ok ? (int)Y0 * W + (int)X0 : 0;
+  t.fx = (float)(X - X0);
+  t.fy = (float)(Y - Y0);
+  t.sw = (float)(g.s / w);
+  t.xn = (float)((X - g.cx) / g.s);
+  t.yn = (float)((Y - g.cy) / g.s);
+  return t;
+}
+
+// fp32 bilinear value and exact interpolant gradient from the 4 taps (Z2); J_raw factors
+__device__ __forceinline__ void warp_interp(const WarpTap& t, float i00, float i01, float i10, float i11, float& d,
+                                            float& gx, float& gy, float& gz) {
+  const float top = fmaf(t.fx, i01 - i00, i00), bot = fmaf(t.fx, i11 - i10, i10);
+  d = fmaf(t.fy, bot - top, top);
+  const float dX = fmaf(t.fy, (i11 - i10) - (i01 - i00), i01 - i00);  // (1-fy)(I01-I00) + fy(I11-I10)
+  const float dY = bot - top;                                          // (1-fx)(I10-I00) + fx(I11-I01)
+  gx = t.sw * dX;
+  gy = t.sw * dY;
+  gz = -fmaf(gx, t.xn, gy * t.yn);
+}
+
+__device__ __forceinline__ bool warp_pixel_f(const WarpGeom& g, const float* __restrict__ img, int H, int W,
+                                             int i, int j, float& d, float& gx, float& gy, float& gz) {
+  const WarpTap t = warp_tap(g, H, W, i, j);
+  if (!t.ok) {
+    d = gx = gy = gz = 0.f;
     return false;
   }
-  const double fx = X - X0, fy = Y - Y0;
-  const int xi = (int)X0, yi = (int)Y0;
-  const float* r0 = img + (size_t)yi * W + xi;
-  const double i00 = __ldg(r0), i01 = __ldg(r0 + 1), i10 = __ldg(r0 + W), i11 = __ldg(r0 + W + 1);
-  d = (1.0 - fy) * ((1.0 - fx) * i00 + fx * i01) + fy * ((1.0 - fx) * i10 + fx * i11);
-  const double dX = (1.0 - fy) * (i01 - i00) + fy * (i11 - i10);
-  const double dY = (1.0 - fx) * (i10 - i00) + fx * (i11 - i01);
-  const double xn = (X - g.cx) / g.s, yn = (Y - g.cy) / g.s;
-  gx = g.s * dX / w;
-  gy = g.s * dY / w;
-  gz = -(gx * xn + gy * yn);
+  const float* r0 = img + t.off;
+  warp_interp(t, __ldg(r0), __ldg(r0 + 1), __ldg(r0 + W), __ldg(r0 + W + 1), d, gx, gy, gz);
   return true;
+}
+
+__device__ __forceinline__ bool warp_pixel(const WarpGeom& g, const float* __restrict__ img, int H, int W,
+                                           int i, int j, double& d, double& gx, double& gy, double& gz) {
+  float df, gxf, gyf, gzf;
+  const bool ok = warp_pixel_f(g, img, H, W, i, j, df, gxf, gyf, gzf);
+  d = df;
+  gx = gxf;
+  gy = gyf;
+  gz = gzf;
+  return ok;
 }
 
 __device__ __forceinline__ void jraw_row(double gx, double gy, double gz, double u, double v, double (&jr)[8]) {

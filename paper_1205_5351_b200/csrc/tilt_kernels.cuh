@@ -545,7 +545,7 @@ __device__ void solve_patch(const SolveArgs& a, Ctx<C>& cx, int b) {
     for (int q = 0; q < p; ++q) {  // Step 4: tau += dtau
       double dq = 0.0;
       for (int r = q; r < p; ++r) dq += Li[r * 8 + q] * (double)s[r];
-      tau[q] += dq;
+      tau[q] = (double)(float)(tau[q] + dq);  // tau carried in fp32 between outer iterations (Z28)
       dt_inf = fmax(dt_inf, fabs(dq));
       finite = finite && isfinite(tau[q]);
     }
@@ -827,10 +827,11 @@ __global__ void __launch_bounds__(C::NT, 1) k_project(ProjArgs a) {
 }
 
 // ---------------------------------------------------------------------------------------------
-// K1 standalone: Alg. 1 Step 1 over all patches (HBM-bound). One CTA per patch.
+// K1 standalone: Alg. 1 Step 1 over all patches (HBM-bound). One CTA per patch; the per-pixel
+// arithmetic is the solve kernels' (warp_tap + warp_interp = warp_pixel_f).
 //   pass 1: per pixel (fp64 coordinates, 4 bilinear taps) -> d, gx, gy, gz stored fp32 in shared
-//           memory (the same fp32 values the fused solve kernel keeps in its planes), fp64 sums of
-//           ||d||^2 and J_raw^T d; the tap loads of K1_ILP pixels are issued before their math;
+//           memory, fp64 sums of ||d||^2 and J_raw^T d; the tap loads of K1_ILP pixels are issued
+//           before their math;
 //   pass 2: D_hat = d/||d|| and J = (J_raw - D_hat c^T)/||d|| (quotient rule) from shared memory,
 //           written as coalesced row-major planes.
 // Traffic per patch: the window's 4-tap footprint (~(m+1)(n+1) pixels) read, (1+p) m n floats
@@ -853,32 +854,6 @@ struct WarpArgs {
 constexpr int K1_NT = 256;
 constexpr int K1_ILP = 4;
 
-// Geometry of one window pixel: source coordinate, cell and fractions (reading Z2, Z15, Z16)
-struct Tap {
-  int off;            // yi * W + xi
-  float fx, fy, w, xn, yn;  // fractions from the fp64 source coordinate, then rounded to fp32
-  bool ok;
-};
-
-__device__ __forceinline__ Tap tap_geom(const WarpGeom& g, double inv_s, int H, int W, int i, int j) {
-  Tap t;
-  const double du = j - 0.5 * (g.n - 1);
-  const double dv = i - 0.5 * (g.m - 1);
-  const double w = 1.0 + (g.h31 * du + g.h32 * dv) * inv_s;
-  const double iw = g.kind == TILT_HOMOGRAPHY ? 1.0 / w : 1.0;
-  const double X = g.cx + (g.h11 * du + g.h12 * dv + g.s * g.h13) * iw;
-  const double Y = g.cy + (g.h21 * du + g.h22 * dv + g.s * g.h23) * iw;
-  const double X0 = floor(X), Y0 = floor(Y);
-  t.ok = X0 >= 0.0 && X0 + 1.0 <= W - 1 && Y0 >= 0.0 && Y0 + 1.0 <= H - 1;
-  t.fx = (float)(X - X0);
-  t.fy = (float)(Y - Y0);
-  t.w = (float)w;
-  t.off = t.ok ? (int)Y0 * W + (int)X0 : 0;
-  t.xn = (float)((X - g.cx) * inv_s);
-  t.yn = (float)((Y - g.cy) * inv_s);
-  return t;
-}
-
 __global__ void __launch_bounds__(K1_NT, 3) k_warp(WarpArgs a) {
   extern __shared__ float4 k1s[];  // per pixel (d, gx, gy, gz)
   __shared__ double red[K1_NT / 32][9];
@@ -887,7 +862,9 @@ __global__ void __launch_bounds__(K1_NT, 3) k_warp(WarpArgs a) {
   const int m = a.m, n = a.n, p = a.p, mn = m * n;
   const int bx[4] = {a.boxes[4 * b], a.boxes[4 * b + 1], a.boxes[4 * b + 2], a.boxes[4 * b + 3]};
   double tau[8] = {1, 0, 0, 1, 0, 0, 0, 0};
-  for (int q = 0; q < p; ++q) tau[q] = a.tau[b * p + q];
+#pragma unroll
+  for (int q = 0; q < 8; ++q)
+    if (q < p) tau[q] = a.tau[b * p + q];
   const WarpGeom g = make_geom(bx, tau, a.kind);
   const float* img = a.images + (size_t)a.patch_image[b] * a.H * a.W;
   const double inv_s = 1.0 / g.s;
@@ -896,7 +873,7 @@ __global__ void __launch_bounds__(K1_NT, 3) k_warp(WarpArgs a) {
   bool esc = false;
   PixIter it(threadIdx.x, K1_NT, n);  // row-major (j fastest): it.i is the column j, it.j the row i
   for (int o0 = threadIdx.x; o0 < mn; o0 += K1_NT * K1_ILP) {
-    Tap t[K1_ILP];
+    WarpTap t[K1_ILP];
     float v[K1_ILP][4];
     int pi[K1_ILP], pj[K1_ILP];
 #pragma unroll
@@ -906,7 +883,7 @@ __global__ void __launch_bounds__(K1_NT, 3) k_warp(WarpArgs a) {
       pj[u] = it.i;
       it.next(K1_NT);
       const int i = pi[u], j = pj[u];
-      t[u] = tap_geom(g, inv_s, a.H, a.W, o < mn ? i : 0, o < mn ? j : 0);
+      t[u] = warp_tap(g, a.H, a.W, o < mn ? i : 0, o < mn ? j : 0);
       const bool live = o < mn && t[u].ok;
       esc |= (o < mn) && !t[u].ok;
       const float* r0 = img + t[u].off;
@@ -920,15 +897,8 @@ __global__ void __launch_bounds__(K1_NT, 3) k_warp(WarpArgs a) {
       const int o = o0 + u * K1_NT;
       if (o >= mn) break;
       const int i = pi[u], j = pj[u];
-      const float fx = t[u].fx, fy = t[u].fy;
-      const float i00 = v[u][0], i01 = v[u][1], i10 = v[u][2], i11 = v[u][3];
-      const float top = fmaf(fx, i01 - i00, i00), bot = fmaf(fx, i11 - i10, i10);
-      const float d = fmaf(fy, bot - top, top);
-      const float dX = fmaf(fy, (i11 - i10) - (i01 - i00), i01 - i00);
-      const float dY = bot - top;
-      const float sw = (float)g.s / t[u].w;
-      const float gx = sw * dX, gy = sw * dY;
-      const float gz = -fmaf(gx, t[u].xn, gy * t[u].yn);
+      float d, gx, gy, gz;  // the solve kernels' per-pixel routine (warp_pixel_f)
+      warp_interp(t[u], v[u][0], v[u][1], v[u][2], v[u][3], d, gx, gy, gz);
       const float4 px = make_float4(d, gx, gy, gz);
       k1s[o] = px;
       // per-thread partial sums in fp32 (~10 pixels each), combined across threads in fp64

@@ -1514,7 +1514,7 @@ __global__ void k_dtau(Args a, int it, int n_outer) {
   for (int q = 0; q < p; ++q) {
     double dq = 0.0;
     for (int r = q; r < p; ++r) dq += st->Linv[r * 8 + q] * (double)(float)st->acc[ACC_S1 + r];
-    st->tau[q] += dq;
+    st->tau[q] = (double)(float)(st->tau[q] + dq);  // tau carried in fp32 (Z28)
     dt_inf = fmax(dt_inf, fabs(dq));
     finite = finite && isfinite(st->tau[q]);
   }

@@ -1222,7 +1222,7 @@ __device__ void solve_patch_rj(const SolveArgs& a, const W<NC>& w, int b) {
       if (q >= p) continue;
       double dq = 0.0;
       for (int r = q; r < p; ++r) dq += Linv[r * 8 + q] * (double)s[r];
-      tau[q] += dq;
+      tau[q] = (double)(float)(tau[q] + dq);  // tau carried in fp32 between outer iterations (Z28)
       dt_inf = fmax(dt_inf, fabs(dq));
       finite = finite && isfinite(tau[q]);
     }

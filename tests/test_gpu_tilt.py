@@ -283,20 +283,23 @@ def solver_big(T):
     s.close()
 
 
-@pytest.mark.parametrize("cfg_id", [3, 4])
-def test_fixed_count_parity_large_configs(solver_big, T, cfg_id):
-    """Configs 3 (100x100 homography, fine level without the pyramid: the S128 class) and 4
-    (200x200 affine: the S256 class, B in shared memory, V and S in the workspace): one outer
-    iteration of 20 LADMAP iterations with replayed rho, A and E within 1e-4 of the oracle."""
+@pytest.mark.parametrize("cfg_id,path", [(3, 1), (4, 1), (4, 3), (4, 0)])
+def test_fixed_count_parity_large_configs(solver_big, T, cfg_id, path):
+    """Configs 3 (100x100 homography, fine level without the pyramid: the S128 CTA class) and 4
+    (200x200 affine): path 1 forces the CTA-per-patch S256 class (B in shared memory, V and S in the
+    workspace), path 3 the multi-CTA path, path 0 the auto route (multi-CTA above 128 x 128). One
+    outer iteration of 20 LADMAP iterations with replayed rho, A and E within 1e-4 of the oracle."""
     cfg = ts.CONFIGS[cfg_id]
     B, K = 2, 20
     b = ts.gen_batch(cfg, 0, B)
     prm_o = O.Params(fixed_inner_iters=K, fixed_outer_iters=1, max_inner=K, max_outer=1)
     refs = [O.tilt(b["images"][k], b["boxes"][k], b["tau0"][k], cfg.kind, prm_o) for k in range(B)]
     rr = _replay_tensor([r["traces"] for r in refs], 1, K)
-    prm = T.default_params(fixed_inner_iters=K, fixed_outer_iters=1, max_inner=K, max_outer=1)
+    prm = T.default_params(fixed_inner_iters=K, fixed_outer_iters=1, max_inner=K, max_outer=1, kernel_path=path)
     prm.rho_replay = rr.data_ptr()
     out = solver_big.solve(b["images"], b["patch_image"], b["boxes"], b["tau0"], cfg.kind, prm)
+    rep = T.reports_to_numpy(out["rep"])
+    assert np.all(rep["kernel_path"] == (path if path else (3 if cfg.m > 128 else 1)))
     for k in range(B):
         a = out["A"][k].double().cpu().numpy()
         e = out["E"][k].double().cpu().numpy()

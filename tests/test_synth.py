@@ -2,6 +2,7 @@
 import dataclasses
 
 import numpy as np
+import pytest
 
 import tilt_synth as ts
 
@@ -40,3 +41,24 @@ def test_table1_instance_shapes():
     inst = ts.table1_instance(10, 6, 0)
     assert inst["D"].shape == (10, 10) and inst["J"].shape == (6, 10, 10)
     assert np.all(np.abs(inst["D"]) <= 0.5)
+
+
+def test_recovery_metrics():
+    """SURVEY P9(ii) recovery rule and Table 2's error on hand-built transforms:
+    tau* = H_G composed with an axis scaling and a translation is recovered (TILT's null
+    directions, reading Z10); an extra 3-degree rotation or a perspective error is not."""
+    from tilt_synth import metrics as M
+    hg = ts.planted_transform(0.3, 0.2, 0.01, -0.02)
+    tg = ts.tau_from_h(hg, ts.HOMOGRAPHY)
+    assert M.recovered_p9(tg, tg) and M.table2_error(tg, tg) == 0.0
+    s = np.diag([1.2, 0.85, 1.0])
+    s[0, 2], s[1, 2] = 0.05, -0.03
+    assert M.recovered_p9(ts.tau_from_h(hg @ s, ts.HOMOGRAPHY), tg)
+    r = ts.planted_transform(np.radians(3.0), 0.0)
+    assert not M.recovered_p9(ts.tau_from_h(hg @ r, ts.HOMOGRAPHY), tg)
+    p = np.eye(3)
+    p[2, 0] = 0.05
+    assert not M.recovered_p9(ts.tau_from_h(hg @ p, ts.HOMOGRAPHY), tg)
+    t2 = tg.copy()
+    t2[0] += 0.1
+    assert M.table2_error(t2, tg) == pytest.approx(0.1 / np.linalg.norm(tg))
