@@ -297,10 +297,11 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     gather_bytes = 0
     if world > 1:  # rank 0 collects every patch's tau / report / A / E (north_star's NCCL gather)
         gathered = {}
-        for key in ("tau", "rep", "A", "E"):
-            x = out[key] if dist.get_backend() == "nccl" else out[key].cpu()
-            gathered[key] = D.gather_to_root(x, G, world, rank)
-            gather_bytes += int(x.numel() * x.element_size()) * (world - 1)
+        with torch.cuda.nvtx.range("K5 gather tau/reports/A/E to rank 0"):
+            for key in ("tau", "rep", "A", "E"):
+                x = out[key] if dist.get_backend() == "nccl" else out[key].cpu()
+                gathered[key] = D.gather_to_root(x, G, world, rank)
+                gather_bytes += int(x.numel() * x.element_size()) * (world - 1)
     t1.record(main)
     torch.cuda.synchronize()
     if world > 1:

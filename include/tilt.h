@@ -266,13 +266,6 @@ tilt_status tilt_set_svt_path(tilt_handle* h, int32_t path);
 /* Number of kernel launches issued by this handle since creation (for bench accounting). */
 int64_t tilt_launch_count(const tilt_handle* h);
 
-/* Host-side view of the Jacobi pair schedule the CTA-per-patch SVT uses for n columns on `units`
- * pair units (32 for windows up to 64, 64 up to 128): a recursive F x M ordering in which a unit
- * keeps one column in registers while the partners rotate past it (tilt_jacobi.cuh). Writes
- * rounds x units entries (i << 8 | j; j = 0xFF: no partner this round; 0xFFFF: idle unit) to `out`
- * (caller-owned host memory, cap entries) and returns the number of rounds; -1 for an invalid
- * n (< 2 or > 255) or a schedule that needs more units, -2 if cap is too small. No GPU needed. */
-int32_t tilt_jacobi_schedule(int32_t n, int32_t units, uint16_t* out, int32_t cap);
 
 #ifdef __cplusplus
 }

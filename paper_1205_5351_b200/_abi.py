@@ -98,7 +98,7 @@ EXPORTS = [
     "tilt_abi_version", "tilt_status_string", "tilt_patch_status_string", "tilt_last_error",
     "tilt_default_params", "tilt_create", "tilt_destroy", "tilt_set_stream", "tilt_solve_batch",
     "tilt_solve_batch_host", "tilt_warp_batch", "tilt_svt_batch", "tilt_project_batch",
-    "tilt_inner_batch", "tilt_launch_count", "tilt_set_svt_path", "tilt_jacobi_schedule",
+    "tilt_inner_batch", "tilt_launch_count", "tilt_set_svt_path",
 ]
 
 _P = ctypes.c_void_p
@@ -144,8 +144,6 @@ def _load():
     lib.tilt_launch_count.argtypes = [_P]
     lib.tilt_set_svt_path.restype = _I
     lib.tilt_set_svt_path.argtypes = [_P, _I]
-    lib.tilt_jacobi_schedule.restype = _I
-    lib.tilt_jacobi_schedule.argtypes = [_I, _I, _P, _I]
     return lib
 
 

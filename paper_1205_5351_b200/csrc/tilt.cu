@@ -11,6 +11,7 @@
 
 #include "tilt_kernels.cuh"
 #include "tilt_large_host.h"
+#include "tilt_nvtx.h"
 #include "tilt_rj_host.h"
 
 using namespace tilt;
@@ -41,91 +42,6 @@ SizeClass size_class(int m, int n) {
   if (d <= 128) return SC128;
   if (d <= 256) return n <= 216 ? SC256 : SC256G;  // B in shared memory while MAXD x n floats fit
   return SC_NONE;
-}
-
-// Jacobi pair schedule with column reuse (tilt_jacobi.cuh, g_sched): returns the number of rounds,
-// or -1 if a node needs more units than available (then the kernels keep the round-robin order).
-int build_jacobi_schedule(int n, int units, std::vector<uint16_t>& out) {
-  struct Node {
-    int lo, hi;
-  };
-  std::vector<Node> nodes{{0, n}};
-  int rounds = 0;
-  while (true) {
-    std::vector<Node> live;
-    for (const Node& x : nodes)
-      if (x.hi - x.lo >= 2) live.push_back(x);
-    if (live.empty()) break;
-    size_t g0 = 0;
-    while (g0 < live.size()) {  // nodes of one depth side by side, as many as the units allow
-      int used = 0, dur = 0;
-      size_t g1 = g0;
-      while (g1 < live.size()) {
-        const int f = (live[g1].hi - live[g1].lo + 1) / 2;
-        if (used + f > units) break;
-        used += f;
-        dur = f > dur ? f : dur;
-        ++g1;
-      }
-      if (g1 == g0) return -1;
-      for (int r = 0; r < dur; ++r) {
-        out.insert(out.end(), units, (uint16_t)0xFFFF);
-        uint16_t* row = out.data() + out.size() - units;
-        int uo = 0;
-        for (size_t q = g0; q < g1; ++q) {
-          const int lo = live[q].lo, L = live[q].hi - lo, f = (L + 1) / 2, m = L - f;
-          if (r < f)
-            for (int u = 0; u < f; ++u) {
-              const int mi = (u + r) % f;
-              row[uo + u] = (uint16_t)(((lo + u) << 8) | (mi < m ? lo + f + mi : 0xFF));
-            }
-          uo += f;
-        }
-        ++rounds;
-      }
-      g0 = g1;
-    }
-    std::vector<Node> next;
-    for (const Node& x : live) {
-      const int f = (x.hi - x.lo + 1) / 2;
-      next.push_back({x.lo, x.lo + f});
-      next.push_back({x.lo + f, x.hi});
-    }
-    nodes.swap(next);
-  }
-  return rounds;
-}
-
-// upload the schedules for n = 2 .. SCHED_MAXN, 32 and 64 units, once per device
-tilt_status init_schedules(int device) {
-  static std::mutex mu;
-  static bool done[128] = {false};
-  std::lock_guard<std::mutex> lk(mu);
-  if (device < 0 || device >= 128) return TILT_E_ARG;
-  if (done[device]) return TILT_OK;
-  std::vector<uint16_t> tab;
-  int off[2][SCHED_MAXN + 1], rounds[2][SCHED_MAXN + 1];
-  for (int c = 0; c < 2; ++c)
-    for (int n = 0; n <= SCHED_MAXN; ++n) {
-      off[c][n] = (int)tab.size();
-      rounds[c][n] = 0;
-      if (n < 2) continue;
-      std::vector<uint16_t> t;
-      const int r = build_jacobi_schedule(n, c == 0 ? 32 : 64, t);
-      if (r > 0 && n <= (c == 0 ? 64 : 128)) {
-        rounds[c][n] = r;
-        tab.insert(tab.end(), t.begin(), t.end());
-      }
-    }
-  uint16_t* d = nullptr;
-  TILT_CUDA(cudaMalloc(&d, tab.size() * sizeof(uint16_t)));  // one table per device, kept for the process
-  TILT_CUDA(cudaMemcpy(d, tab.data(), tab.size() * sizeof(uint16_t), cudaMemcpyHostToDevice));
-  const uint16_t* dc = d;
-  TILT_CUDA(cudaMemcpyToSymbol(g_sched, &dc, sizeof(dc)));
-  TILT_CUDA(cudaMemcpyToSymbol(c_sched_off, off, sizeof(off)));
-  TILT_CUDA(cudaMemcpyToSymbol(c_sched_rounds, rounds, sizeof(rounds)));
-  done[device] = true;
-  return TILT_OK;
 }
 
 }  // namespace
@@ -510,13 +426,7 @@ tilt_status tilt_create(tilt_handle** out, const tilt_create_opts* o) {
     delete h;
     return s;
   }
-  {
-    const tilt_status ss = init_schedules(h->device);
-    if (ss != TILT_OK) {
-      delete h;
-      return ss;
-    }
-  }
+
   auto fail = [&](cudaError_t err, const char* what) {
     cuda_fail(err, what);
     tilt_destroy(h);
@@ -699,6 +609,7 @@ tilt_status tilt_solve_batch(tilt_handle* h, const float* images, int32_t n_imag
   if (B < 0 || B > h->max_batch) return TILT_E_ARG;
   if (B == 0) return TILT_OK;
   if (!images || !patch_image || !boxes || !tau_out || n_images < 1 || H < 2 || W < 2) return TILT_E_ARG;
+  tilt::NvtxRange nv("tilt_solve_batch (K1-K4: persistent Algorithm 1)");
   if (kind != TILT_AFFINE && kind != TILT_HOMOGRAPHY) return TILT_E_ARG;
   const int p = kind == TILT_HOMOGRAPHY ? 8 : 6;
   if (p > h->max_p) return TILT_E_ARG;
@@ -761,6 +672,7 @@ tilt_status tilt_solve_batch_host(tilt_handle* h, const float* images, int32_t n
     g_last_error = "host entry needs max_image_elems >= n_images*H*W at tilt_create";
     return TILT_E_ARG;
   }
+  tilt::NvtxRange nv("tilt_solve_batch_host (H2D, solve, D2H)");
   const int p = kind == TILT_HOMOGRAPHY ? 8 : 6;
   const int m = boxes[3], n = boxes[2];
   if (m < 2 || n < 2 || m > h->max_m || n > h->max_n) return TILT_E_ARG;
@@ -794,6 +706,7 @@ tilt_status tilt_warp_batch(tilt_handle* h, const float* images, int32_t n_image
   if (B == 0) return TILT_OK;
   if (!images || !patch_image || !boxes || !tau || !Dhat) return TILT_E_ARG;
   if (kind != TILT_AFFINE && kind != TILT_HOMOGRAPHY) return TILT_E_ARG;
+  tilt::NvtxRange nv("K1 tilt_warp_batch");
   TILT_CUDA(cudaSetDevice(h->device));
   int m = win_h, n = win_w;
   if (m <= 0 || n <= 0) {
@@ -832,6 +745,7 @@ tilt_status tilt_svt_batch(tilt_handle* h, const float* M, int32_t B, int32_t m,
   if (!h || B < 0 || m < 1 || n < 1 || m > h->max_m || n > h->max_n) return TILT_E_ARG;
   if (B == 0) return TILT_OK;
   if (!M || !eps || !A) return TILT_E_ARG;
+  tilt::NvtxRange nv("K3 tilt_svt_batch");
   TILT_CUDA(cudaSetDevice(h->device));
   SvtArgs a;
   memset(&a, 0, sizeof(a));
@@ -872,6 +786,7 @@ tilt_status tilt_project_batch(tilt_handle* h, const float* J, const float* Q, i
   if (p < 1 || p > 8 || p > h->max_p || (Q && (l < 1 || l > 3))) return TILT_E_ARG;
   if (B == 0) return TILT_OK;
   if (!J || !v || !Pv) return TILT_E_ARG;
+  tilt::NvtxRange nv("K2 tilt_project_batch");
   TILT_CUDA(cudaSetDevice(h->device));
   ProjArgs a;
   memset(&a, 0, sizeof(a));
@@ -896,6 +811,7 @@ tilt_status tilt_inner_batch(tilt_handle* h, const float* D, const float* J, con
   if (p < 1 || p > 8 || p > h->max_p || (Q && (l < 1 || l > 3))) return TILT_E_ARG;
   if (B == 0) return TILT_OK;
   if (!D || !J || !A || !E) return TILT_E_ARG;
+  tilt::NvtxRange nv("K3 tilt_inner_batch");
   TILT_CUDA(cudaSetDevice(h->device));
   InnerArgs a;
   memset(&a, 0, sizeof(a));
@@ -934,17 +850,6 @@ tilt_status tilt_inner_batch(tilt_handle* h, const float* D, const float* J, con
     return TILT_OK;
   }
   return dispatch<InnerF>(size_class(m, n), h, a);
-}
-
-// host-side check of the Jacobi pair schedule (no GPU needed): rounds, or -1 / -2 (cap too small)
-int32_t tilt_jacobi_schedule(int32_t n, int32_t units, uint16_t* out, int32_t cap) {
-  if (n < 2 || n > 255 || units < 1) return -1;
-  std::vector<uint16_t> t;
-  const int r = build_jacobi_schedule(n, units, t);
-  if (r < 0) return -1;
-  if ((int64_t)t.size() > cap) return -2;
-  if (out) memcpy(out, t.data(), t.size() * sizeof(uint16_t));
-  return r;
 }
 
 }  // extern "C"

@@ -84,6 +84,7 @@ struct Scal {
   int flag;
   int patch;
   int rot_acc;       // Jacobi rotations of the current SVT
+  int svt_comp;      // 1: the current SVT is formed as M - P_eps(M) (Moreau form, svt())
 };
 
 // --------------------------------------------------------------------------------------------
@@ -296,6 +297,44 @@ __device__ __forceinline__ void transpose_nn(float* __restrict__ Ym, const float
 #include "tilt_jacobi.cuh"
 
 // sigma_j = sqrt(ns_j.x) stats after the final pass: nuclear norm of S_eps, ranks (Z19), sigma_1.
+// Scale B for the SVT product: column j by h_j / ||v_j||^2 (A = B V^T), or by (1 - h_j) / ||v_j||^2
+// when sum_j min(sigma_j, eps)^2 < sum_j max(sigma_j - eps, 0)^2 (the Moreau form M - B V^T)
+template <class C>
+__device__ __forceinline__ void col_scale(Ctx<C>& cx, float eps) {
+  const int n = cx.n;
+  if (threadIdx.x < 32) {
+    float kept = 0.f, disc = 0.f;
+    for (int j = threadIdx.x; j < n; j += 32) {
+      const float sg = sqrtf(cx.ns[j].x);
+      const float a = fmaxf(sg - eps, 0.f), c = fminf(sg, eps);
+      kept = fmaf(a, a, kept);
+      disc = fmaf(c, c, disc);
+    }
+#pragma unroll
+    for (int off = 16; off; off >>= 1) {
+      kept += __shfl_xor_sync(FULL, kept, off);
+      disc += __shfl_xor_sync(FULL, disc, off);
+    }
+    if (threadIdx.x == 0) cx.sc->svt_comp = disc < kept ? 1 : 0;
+  }
+  __syncthreads();
+  const bool comp = cx.sc->svt_comp != 0;
+  const int lds = cx.lds, rows = round4(cx.m);
+  for (int e = threadIdx.x; e < n * (rows >> 2); e += C::NT) {
+    const int j = e / (rows >> 2), i0 = (e - j * (rows >> 2)) * 4;
+    const float h = cx.hv[j];
+    const float f = (comp ? 1.f - h : h) * cx.ns[j].y;
+    float4* bp = reinterpret_cast<float4*>(cx.B + j * lds + i0);
+    float4 b = *bp;
+    b.x *= f;
+    b.y *= f;
+    b.z *= f;
+    b.w *= f;
+    *bp = b;
+  }
+  __syncthreads();
+}
+
 template <class C>
 __device__ __forceinline__ void svt_stats(Ctx<C>& cx, float eps) {
   const int n = cx.n;
@@ -388,9 +427,24 @@ __device__ SvtOut svt(Ctx<C>& cx, const float* X, float eps, float tol, int max_
   } else {
     r.sweeps = jacobi_sweeps<C>(cx, tol, max_sweeps, &r.capped);
   }
-  col_pass<C, 2>(cx, eps);  // sigma_j, h_j, B <- B diag(h / ||v||^2)
+  col_pass<C, 2>(cx, eps);  // sigma_j, h_j, 1 / ||v_j||^2
   svt_stats<C>(cx, eps);
-  if constexpr (DO_OUT) gemm_bvt<C>(cx.B, cx.V, cx.lds, cx.m, cx.n, out);  // A = B diag(h) V^T
+  if constexpr (DO_OUT) {
+    // S_eps(M) = B diag(h) V^T, or, when the shrunk-away part is the smaller one, the Moreau form
+    // M - B diag(1 - h) V^T = M - P_eps(M) (P_eps: projection onto the spectral ball of radius eps;
+    // the same matrix in exact arithmetic). At large mu the correction is O(eps) and the fp32 error
+    // of A falls from the SVT's (~1e-6 ||A||, which put a floor of mu 1e-6 under crit2) to ~ulp(M).
+    col_scale<C>(cx, eps);
+    const bool comp = cx.sc->svt_comp != 0;
+    const int lds = cx.lds;
+    gemm_bvt<C>(cx.B, cx.V, cx.lds, cx.m, cx.n, [&](int i0, int j, float4 p) {
+      if (comp) {
+        const float4 x = *reinterpret_cast<const float4*>(X + j * lds + i0);
+        p = make_float4(x.x - p.x, x.y - p.y, x.z - p.z, x.w - p.w);
+      }
+      out(i0, j, p);
+    });
+  }
   __syncthreads();
   if (ns_after) ns_step<C>(cx);
   return r;
@@ -401,7 +455,7 @@ __device__ SvtOut svt(Ctx<C>& cx, const float* X, float eps, float tol, int max_
 // --------------------------------------------------------------------------------------------
 
 struct WarpGeom {
-  double s, cx, cy, h11, h12, h13, h21, h22, h23, h31, h32;
+  double s, inv_s, cx, cy, h11, h12, h13, h21, h22, h23, h31, h32;
   int m, n, p, kind;
 };
 
@@ -411,6 +465,7 @@ __device__ __forceinline__ WarpGeom make_geom(const int* box, const double* tau,
   g.n = box[2];
   g.m = box[3];
   g.s = 0.5 * (double)max(g.m, g.n);
+  g.inv_s = 1.0 / g.s;
   g.cx = x0 + 0.5 * (g.n - 1);
   g.cy = y0 + 0.5 * (g.m - 1);
   g.h11 = tau[0]; g.h12 = tau[1]; g.h21 = tau[2]; g.h22 = tau[3]; g.h13 = tau[4]; g.h23 = tau[5];
@@ -428,6 +483,14 @@ __device__ __forceinline__ WarpGeom make_geom(const int* box, const double* tau,
 // the warp-per-patch and multi-CTA paths): the source coordinate in fp64 (an fp32 coordinate of a
 // 100-pixel canvas would carry ~6e-6 px of rounding into the fractions), the 4 taps, the bilinear
 // value and the exact interpolant gradient (reading Z2) in fp32 from the fp32 fractions.
+// a + e - d of three fp32 values, exact up to the final rounding (fp64 sum): the LADMAP residual
+// A + E - D_hat cancels O(1e-2) entries down to O(1e-9), so summed in fp32 its rounding (~ulp(a + e)
+// per entry, ~2e-7 in norm at 50 x 50) was the crit1 floor (Z7) and, through Y += mu R, put a floor
+// of ~mu 1e-6 under crit2: fp32 inner loops that the fp64 oracle ends at mu ~ 2e5 ran to max_inner
+__device__ __forceinline__ float res3(float a, float e, float d) {
+  return (float)(((double)a + (double)e) - (double)d);
+}
+
 struct WarpTap {
   int off;                    // yi * W + xi of the cell's top-left tap
   float fx, fy, sw, xn, yn;   // fractions, s / w, normalised source coordinate
@@ -438,18 +501,19 @@ struct WarpTap {
 __device__ __forceinline__ WarpTap warp_tap(const WarpGeom& g, int H, int W, int i, int j) {
   const double du = j - 0.5 * (g.n - 1);
   const double dv = i - 0.5 * (g.m - 1);
-  const double w = 1.0 + (g.h31 * du + g.h32 * dv) / g.s;
-  const double X = g.cx + (g.h11 * du + g.h12 * dv + g.s * g.h13) / w;
-  const double Y = g.cy + (g.h21 * du + g.h22 * dv + g.s * g.h23) / w;
+  const double w = 1.0 + (g.h31 * du + g.h32 * dv) * g.inv_s;
+  const double iw = g.kind == TILT_HOMOGRAPHY ? 1.0 / w : 1.0;  // the one fp64 division per pixel
+  const double X = g.cx + (g.h11 * du + g.h12 * dv + g.s * g.h13) * iw;
+  const double Y = g.cy + (g.h21 * du + g.h22 * dv + g.s * g.h23) * iw;
   const double X0 = floor(X), Y0 = floor(Y);
   WarpTap t;
   t.ok = X0 >= 0.0 && X0 + 1.0 <= W - 1 && Y0 >= 0.0 && Y0 + 1.0 <= H - 1;
   t.off = t.ok ? (int)Y0 * W + (int)X0 : 0;
   t.fx = (float)(X - X0);
   t.fy = (float)(Y - Y0);
-  t.sw = (float)(g.s / w);
-  t.xn = (float)((X - g.cx) / g.s);
-  t.yn = (float)((Y - g.cy) / g.s);
+  t.sw = (float)(g.s * iw);
+  t.xn = (float)((X - g.cx) * g.inv_s);
+  t.yn = (float)((Y - g.cy) * g.inv_s);
   return t;
 }
 

@@ -60,14 +60,6 @@ struct Col {
           : "+f"(v[4 * q]), "+f"(v[4 * q + 1]), "+f"(v[4 * q + 2]), "+f"(v[4 * q + 3])
           : "r"(a + 16 * q * L), "r"((int)(cm >> q & 1u)));
   }
-  __device__ __forceinline__ void sload_keep(uint32_t a, uint32_t cm) {  // predicated, others unchanged
-#pragma unroll
-    for (int q = 0; q < NCH; ++q)
-      asm volatile(
-          "{\n .reg .pred p;\n setp.ne.b32 p, %5, 0;\n @p ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];\n}"
-          : "+f"(v[4 * q]), "+f"(v[4 * q + 1]), "+f"(v[4 * q + 2]), "+f"(v[4 * q + 3])
-          : "r"(a + 16 * q * L), "r"((int)(cm >> q & 1u)));
-  }
   __device__ __forceinline__ void sload_full(uint32_t a) {  // every chunk exists
 #pragma unroll
     for (int q = 0; q < NCH; ++q)
@@ -156,8 +148,8 @@ __device__ __forceinline__ Rot rot_params(float4 ni, float4 nj, float gam, bool 
 // Re-normalisation passes
 // MODE 0: ns_j = (||x_j||^2, 1, 1) (no scaling applied)
 // MODE 1: apply the scales to B and V columns, ns_j = (fresh ||x_j||^2, 1, 1)
-// MODE 2: as 1, then sigma_j = ||b_j|| / ||v_j||, h_j = max(sigma_j - eps, 0)/sigma_j and
-//         B <- B diag(h_j / ||v_j||^2) (ready for A = B V^T); hv_j = h_j.
+// MODE 2: as 1, then sigma_j = ||b_j|| / ||v_j||, h_j = max(sigma_j - eps, 0)/sigma_j;
+//         ns_j = (sigma_j^2, 1/||v_j||^2, 1), hv_j = h_j (B is scaled for the product by svt()).
 // ---------------------------------------------------------------------------------------------
 template <class C, int MODE>
 __device__ __forceinline__ void col_pass(Ctx<C>& cx, float eps) {
@@ -182,19 +174,20 @@ __device__ __forceinline__ void col_pass(Ctx<C>& cx, float eps) {
       y.gload(vp, cm);
       y.scale(s);
     }
+    float ivv = 1.f;
     if (MODE == 2) {
       const float vv = unit_sum<L>(y.sq());
       ss = vv > 0.f ? ss / vv : 0.f;
+      ivv = vv > 0.f ? 1.f / vv : 0.f;
       const float sg = sqrtf(ss);
       h = (sg > eps) ? (sg - eps) / sg : 0.f;
-      x.scale(vv > 0.f ? h / vv : 0.f);
     }
     if (valid && MODE != 0) {
       x.gstore(bp, cm);
       y.gstore(vp, cm);
     }
     if (valid && lu == 0) {
-      cx.ns[j] = make_float4(ss, 1.f, 1.f, 0.f);
+      cx.ns[j] = make_float4(ss, ivv, 1.f, 0.f);
       if (MODE == 2) cx.hv[j] = h;
     }
   }
@@ -325,21 +318,6 @@ __device__ int jacobi_sweeps(Ctx<C>& cx, float tol, int max_sweeps, bool* capped
 }
 
 // ---------------------------------------------------------------------------------------------
-// Pair schedules with column reuse (built on the host by tilt.cu: build_jacobi_schedule). A node
-// [lo, hi) of columns pairs its first half F (ceil) with its second half M in |F| rounds: unit u
-// keeps F_u in registers while the M columns rotate past it (every F x M pair once), then both
-// halves recurse; nodes of one depth run side by side. Every pair is visited once per sweep, as in
-// the round-robin ordering (any cyclic ordering is a valid one-sided Jacobi sweep), but per pair a
-// unit loads one column instead of two and writes the kept column back once per phase.
-// Entry (round r, unit u) = (i << 8) | j: i the kept column, j its partner (0xFF: none this round;
-// 0xFFFF: unit idle). Per unit class (0: 32 units, 1: 64 units) and column count n <= SCHED_MAXN.
-// ---------------------------------------------------------------------------------------------
-constexpr int SCHED_MAXN = 128;
-static __device__ const uint16_t* g_sched = nullptr;
-static __constant__ int c_sched_off[2][SCHED_MAXN + 1];
-static __constant__ int c_sched_rounds[2][SCHED_MAXN + 1];
-
-// ---------------------------------------------------------------------------------------------
 // Shared-memory specialisation (S32/S64/S128: B, V in shared memory, n/2 <= UNITS): 32-bit shared
 // addresses with predicated vector ld/st.shared, the circle-method pair advanced incrementally
 // (i, j <- i+1, j+1 mod q), __noinline__ so the caller's live state does not crowd its registers.
@@ -364,89 +342,6 @@ __device__ __noinline__ int jacobi_sweeps_smem(float* Bp, float* Vp, float4* nsp
   col_pass_smem<C, 0>(sB, sV, sNS, n, ld);
   int sweeps = 0;
   int any = 0;
-  constexpr int cls = C::UNITS == 64 ? 1 : 0;
-  const int nrounds = (C::UNITS == 32 || C::UNITS == 64) && n <= SCHED_MAXN ? c_sched_rounds[cls][n] : 0;
-  if (nrounds > 0) {  // column-reuse schedule
-    const uint16_t* __restrict__ sched = g_sched + c_sched_off[cls][n];
-    while (sweeps < max_sweeps) {
-      int rot = 0, big = 0;
-      int ci = -1;                         // column held in xi (and yi once loaded)
-      bool bdirty = false, vdirty = false, vload = false;
-      Col<RPL, L> xi, xj, yi, yj;
-      uint32_t code = __ldg(sched + k);
-      for (int r = 0; r < nrounds; ++r) {
-        const uint32_t nxt = r + 1 < nrounds ? __ldg(sched + (r + 1) * C::UNITS + k) : 0xFFFFu;
-        const bool has_i = code != 0xFFFFu;
-        const int i = has_i ? (int)(code >> 8) : 0;
-        const bool valid = has_i && (code & 0xFFu) != 0xFFu;
-        const int j = valid ? (int)(code & 0xFFu) : 0;
-        const uint32_t ai = sB + i * colb + lane_off, aj = sB + j * colb + lane_off;
-        if (has_i && i != ci) {  // a new kept column (unit-uniform branch)
-          xi.sload_full(ai);
-          ci = i;
-          bdirty = vdirty = vload = false;
-        }
-        if (valid) xj.sload_full(aj);
-        const float4 ni = lds4(sNS + 16 * i), nj = lds4(sNS + 16 * j);  // (alpha, d, 1/d, -)
-        const float g = unit_sum<L>(valid ? xi.dot(xj) : 0.f);
-        const float gam = g * ni.y * nj.y;
-        const float ab = ni.x * nj.x;
-        const bool doit = valid && ni.x > 0.f && nj.x > 0.f && gam * gam > tol2 * ab;
-        if (__any_sync(FULL, doit)) {  // warp-uniform branch
-          const Rot rp = rot_params(ni, nj, gam, doit);
-          const uint32_t vi = sV + i * colb + lane_off, vj = sV + j * colb + lane_off;
-          const uint32_t cmr = doit ? cm : 0u;
-#pragma unroll
-          for (int e = 0; e < RPL; ++e) {
-            const float o = xi.v[e];
-            xi.v[e] = fmaf(-rp.ca, xj.v[e], o);
-            xj.v[e] = fmaf(rp.cb, o, xj.v[e]);
-          }
-          xj.sstore(aj, cmr);  // the partner leaves after this round
-          yi.sload_keep(vi, (doit && !vload) ? cm : 0u);  // the kept V column, loaded on its first rotation
-          vload = vload || doit;
-          yj.sload(vj, cmr);
-#pragma unroll
-          for (int e = 0; e < RPL; ++e) {
-            const float o = yi.v[e];
-            yi.v[e] = fmaf(-rp.ca, yj.v[e], o);
-            yj.v[e] = fmaf(rp.cb, o, yj.v[e]);
-          }
-          yj.sstore(vj, cmr);
-          bdirty = bdirty || doit;
-          vdirty = vdirty || doit;
-          const float sx = rp.c * fmaf(rp.t, rp.t, 1.f);  // sqrt(1 + t^2)
-          sts4(sNS + 16 * i, make_float4(fmaxf(fmaf(-rp.t, gam, ni.x), 0.f), rp.c * ni.y, sx * ni.z, 0.f),
-               doit && lu == 0);
-          sts4(sNS + 16 * j, make_float4(fmaf(rp.t, gam, nj.x), rp.c * nj.y, sx * nj.z, 0.f), doit && lu == 0);
-          rot |= doit ? 1 : 0;
-          nrot += (doit && lu == 0) ? 1 : 0;
-          big |= (doit && gam * gam > big2 * ab) ? 1 : 0;
-        }
-        // the kept column goes back to shared memory when it leaves this unit
-        const int inext = nxt != 0xFFFFu ? (int)(nxt >> 8) : -1;
-        if (ci >= 0 && inext != ci) {
-          xi.sstore(sB + ci * colb + lane_off, bdirty ? cm : 0u);
-          yi.sstore(sV + ci * colb + lane_off, vdirty ? cm : 0u);
-          ci = -1;
-        }
-        __syncthreads();
-        code = nxt;
-      }
-      ++sweeps;
-      any = __syncthreads_or(rot);
-      const int more = __syncthreads_or(big);
-      col_pass_smem<C, 1>(sB, sV, sNS, n, ld);  // re-normalise (apply scales, fresh norms)
-      if (!more) {
-        any = 0;
-        break;
-      }
-    }
-    if (rot_acc && nrot) atomicAdd(rot_acc, nrot);
-    __syncthreads();
-    *capped = any;
-    return sweeps;
-  }
   while (sweeps < max_sweeps) {
     int rot = 0, big = 0;
     int i = k == 0 ? q : k, j = k == 0 ? 0 : q - k;  // round 0 of the circle method

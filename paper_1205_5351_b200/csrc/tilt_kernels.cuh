@@ -140,7 +140,7 @@ __device__ InnerOut ladmap_inner(Ctx<C>& cx, const DevParams& P, float lam, floa
   float mu = mu0;
   o.mu = mu;
   const bool warm = P.svd_warm != 0;
-  auto vres = [&](int idx) { return Ap[idx] + Ep[idx] - Dp[idx]; };
+  auto vres = [&](int idx) { return res3(Ap[idx], Ep[idx], Dp[idx]); };
   for (int k = 0; k < niter; ++k) {
     // ---- A step: A_{k+1} = S_{1/mu}(M_k), M_k in S ------------------------------------------
     float dA2 = 0.f;
@@ -170,7 +170,7 @@ __device__ InnerOut ladmap_inner(Ctx<C>& cx, const DevParams& P, float lam, floa
     for (PixIter pi(threadIdx.x, C::NT, ld); pi.idx < pl; pi.next(C::NT)) {
       const int idx = pi.idx;
       const float e = Ep[idx];
-      const float v = Ap[idx] + e - Dp[idx];
+      const float v = res3(Ap[idx], e, Dp[idx]);
       const float pv = v - PR::apply(cx, idx, pi.i, pi.j, z);
       const float nk = e - pv - Yp[idx] * inv_mu;
       const float en = copysignf(fmaxf(fabsf(nk) - thr, 0.f), nk);
@@ -192,7 +192,7 @@ __device__ InnerOut ladmap_inner(Ctx<C>& cx, const DevParams& P, float lam, floa
     for (PixIter pi(threadIdx.x, C::NT, ld); pi.idx < pl; pi.next(C::NT)) {
       const int idx = pi.idx;
       const float a = Ap[idx];
-      const float v = a + Ep[idx] - Dp[idx];
+      const float v = res3(a, Ep[idx], Dp[idx]);
       const float r = v - PR::apply(cx, idx, pi.i, pi.j, z);
       const float y = fmaf(mu, r, Yp[idx]);
       Yp[idx] = y;
@@ -347,12 +347,12 @@ __device__ __forceinline__ void write_m0(Ctx<C>& cx, float mu0) {
   const float* Ap = cx.A;
   const float* Ep = cx.E;
   const float* Dp = cx.D;
-  PR::reduce(cx, [&](int idx) { return Ap[idx] + Ep[idx] - Dp[idx]; }, s);
+  PR::reduce(cx, [&](int idx) { return res3(Ap[idx], Ep[idx], Dp[idx]); }, s);
   PR::coeffs(cx, s, z);
   const float inv = 1.f / mu0;
   for (PixIter pi(threadIdx.x, C::NT, cx.ld); pi.idx < cx.pl; pi.next(C::NT)) {
     const int idx = pi.idx;
-    const float v = Ap[idx] + Ep[idx] - Dp[idx];
+    const float v = res3(Ap[idx], Ep[idx], Dp[idx]);
     const float r = v - PR::apply(cx, idx, pi.i, pi.j, z);
     cx.S[pi.j * cx.lds + pi.i] = Ap[idx] - r - cx.Y[idx] * inv;
   }

@@ -24,6 +24,7 @@
 #include "tilt_dense.cuh"
 #include "tilt_kernels.cuh"
 #include "tilt_large_host.h"
+#include "tilt_nvtx.h"
 
 namespace tilt {
 namespace lp {
@@ -55,6 +56,7 @@ struct St {
   float inv_nd;  // ADM: 1 / ||D||_F
   int svt_rank, relrank, band;
   int iters, done, status, conv;
+  int comp;        // the current SVT is formed as M - P_eps(M) (Moreau form; k_svt_stats)
   int svt_done, big_any, rot_any, sw_cur, cap_cur, rot_cur;
   int sweeps, caps, rotations, aux_sweeps;
   double fro2;  // ||B||_F^2 at the start of the current SVT (negligible-column threshold)
@@ -398,7 +400,7 @@ __global__ void __launch_bounds__(ENT) k_m0(Args a) {
   const float inv = 1.f / st->mu;
   FOR_ELEMS(L.plane) {
     const float av = w[L.oA + idx];
-    const float v = av + w[L.oE + idx] - w[L.oD + idx];
+    const float v = res3(av, w[L.oE + idx], w[L.oD + idx]);
     const float r = v - kdot(w + L.oK, L.plane, idx, L.p, s);
     w[L.oS + idx] = av - r - w[L.oY + idx] * inv;
   }
@@ -422,13 +424,13 @@ __global__ void __launch_bounds__(ENT) k_estep(Args a) {
   for (int q = 0; q < 9; ++q) o[q] = 0.f;
   FOR_ELEMS(L.plane) {
     const float an = w[L.oAn + idx], e = w[L.oE + idx], dv = w[L.oD + idx];
-    const float pv = (an + e - dv) - kdot(K, L.plane, idx, L.p, s);
+    const float pv = res3(an, e, dv) - kdot(K, L.plane, idx, L.p, s);
     const float nk = e - pv - w[L.oY + idx] * inv_mu;
     const float en = copysignf(fmaxf(fabsf(nk) - thr, 0.f), nk);
     const float d = en - e;
     o[8] = fmaf(d, d, o[8]);
     w[L.oE + idx] = en;
-    const float v2 = an + en - dv;
+    const float v2 = res3(an, en, dv);
 #pragma unroll
     for (int q = 0; q < 8; ++q)
       if (q < L.p) o[q] = fmaf(K[q * L.plane + idx], v2, o[q]);
@@ -450,7 +452,7 @@ __global__ void __launch_bounds__(ENT) k_ystep(Args a) {
   float c1[1] = {0.f};
   FOR_ELEMS(L.plane) {
     const float an = w[L.oAn + idx];
-    const float r = (an + w[L.oE + idx] - w[L.oD + idx]) - kdot(w + L.oK, L.plane, idx, L.p, s);
+    const float r = res3(an, w[L.oE + idx], w[L.oD + idx]) - kdot(w + L.oK, L.plane, idx, L.p, s);
     const float y = fmaf(mu, r, w[L.oY + idx]);
     w[L.oY + idx] = y;
     c1[0] = fmaf(r, r, c1[0]);
@@ -694,15 +696,17 @@ __global__ void __launch_bounds__(32) k_svt_stats(Args a, int count_sweeps, int 
   const float* sig = slot(a, b) + a.L.oSig;
   const float eps = st->eps;
   const int lane = threadIdx.x, n = a.L.n;
-  float nuc = 0.f, smax = 0.f, amax = 0.f;
+  float nuc = 0.f, smax = 0.f, amax = 0.f, kept = 0.f, disc = 0.f;
   int cnt = 0;
   for (int j = lane; j < n; j += 32) {
     const float sg = sig[j];
-    const float x = fmaxf(sg - eps, 0.f);
+    const float x = fmaxf(sg - eps, 0.f), c = fminf(sg, eps);
     nuc += x;
     smax = fmaxf(smax, sg);
     amax = fmaxf(amax, x);
     cnt += (sg > eps);
+    kept = fmaf(x, x, kept);
+    disc = fmaf(c, c, disc);
   }
 #pragma unroll
   for (int off = 16; off; off >>= 1) {
@@ -710,6 +714,8 @@ __global__ void __launch_bounds__(32) k_svt_stats(Args a, int count_sweeps, int 
     smax = fmaxf(smax, __shfl_xor_sync(0xffffffffu, smax, off));
     amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, off));
     cnt += __shfl_xor_sync(0xffffffffu, cnt, off);
+    kept += __shfl_xor_sync(0xffffffffu, kept, off);
+    disc += __shfl_xor_sync(0xffffffffu, disc, off);
   }
   int rel = 0, band = 0;
   for (int j = lane; j < n; j += 32) {
@@ -726,6 +732,7 @@ __global__ void __launch_bounds__(32) k_svt_stats(Args a, int count_sweeps, int 
     band |= __shfl_xor_sync(0xffffffffu, band, off);
   }
   if (lane == 0) {
+    st->comp = which == 0 && disc < kept ? 1 : 0;  // the Moreau form when the shrunk part is smaller
     st->nuc = nuc;
     st->sig1 = smax;
     st->svt_rank = cnt;
@@ -754,8 +761,18 @@ __global__ void __launch_bounds__(ENT) k_svt_scale(Args a) {
     if (j >= a.L.n) continue;
     const float sg = sig[j], v2 = vv[j];
     const float h = sg > eps ? (sg - eps) / sg : 0.f;
-    w[a.L.oB + idx] *= v2 > 0.f ? h / v2 : 0.f;
+    w[a.L.oB + idx] *= v2 > 0.f ? (st->comp ? 1.f - h : h) / v2 : 0.f;
   }
+}
+
+// the Moreau form of the SVT (svt() in tilt_device.cuh): dst = M - B diag(1 - h) V^T = M - P_eps(M)
+// for the problems whose shrunk-away part is the smaller one (st->comp); M is in S
+__global__ void __launch_bounds__(ENT) k_svt_moreau(Args a, size_t dst) {
+  const int b = blockIdx.y;
+  St* st = state(a, b);
+  if (st->done || st->warm || !st->comp) return;
+  float* w = slot(a, b);
+  FOR_ELEMS(a.L.plane) w[dst + idx] = w[a.L.oS + idx] - w[dst + idx];
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -1493,7 +1510,7 @@ __global__ void __launch_bounds__(ENT) k_dtau_red(Args a) {
   for (int q = 0; q < 9; ++q) s[q] = 0.f;
   FOR_ELEMS(L.plane) {
     const float e = w[L.oE + idx];
-    const float v = w[L.oA + idx] + e - w[L.oD + idx];
+    const float v = res3(w[L.oA + idx], e, w[L.oD + idx]);
 #pragma unroll
     for (int q = 0; q < 8; ++q)
       if (q < L.p) s[q] = fmaf(w[L.oK + q * L.plane + idx], v, s[q]);
@@ -1959,6 +1976,8 @@ static bool inner_core(Run& R, const DevParams& P, const float* Q, int l, int q_
       R.launched();
       if (R.svt_core(nullptr, 0, 1, true)) return true;
       if (R.gemm(false, true, m, n, n, L.oB, L.ldm, a.oV, L.ldn, L.oA, L.ldm)) return true;
+      k_svt_moreau<<<R.egrid(L.plane), ENT, 0, sm>>>(a, L.oA);
+      R.launched();
       if (warm && (k % P.ns_period == P.ns_period - 1 || k + 1 == a.niter))
         if (R.ns_step()) return true;
       k_adm_e<<<R.egrid(L.plane), ENT, 0, sm>>>(a);
@@ -2005,6 +2024,8 @@ static bool inner_core(Run& R, const DevParams& P, const float* Q, int l, int q_
       R.nsub = 0;
     }
     if (R.gemm(false, true, m, n, n, L.oB, L.ldm, a.oV, L.ldn, L.oAn, L.ldm)) return true;
+    k_svt_moreau<<<R.egrid(L.plane), ENT, 0, sm>>>(a, L.oAn);
+    R.launched();
     if (warm && (k % P.ns_period == P.ns_period - 1 || k + 1 == a.niter))
       if (R.ns_step()) return true;
     if (R.svdws) {
@@ -2099,16 +2120,23 @@ tilt_status solve(Ctx& ctx, const float* images, int n_images, int H, int W, con
   const int n_outer = P.fixed_outer > 0 ? P.fixed_outer : P.max_outer;
   for (int it = 0; it < n_outer; ++it) {
     a.cur_outer = it;
+    NvtxRange nv_outer("multi-CTA outer iteration");
     // Step 1: D_hat, J (two passes), Q
-    k_lwarp<<<R.egrid(L.plane), ENT, 0, sm>>>(a);
-    k_lwarp_status<<<R.sgrid(), 128, 0, sm>>>(a);
-    k_lwarp_norm<<<R.egrid(L.plane), ENT, 0, sm>>>(a);
-    k_qrows<<<R.sgrid(), 128, 0, sm>>>(a);
-    k_outer_begin<<<R.sgrid(), 128, 0, sm>>>(a);
-    R.launched(5);
+    {
+      NvtxRange nv_k1("K1 warp + Jacobian");
+      k_lwarp<<<R.egrid(L.plane), ENT, 0, sm>>>(a);
+      k_lwarp_status<<<R.sgrid(), 128, 0, sm>>>(a);
+      k_lwarp_norm<<<R.egrid(L.plane), ENT, 0, sm>>>(a);
+      k_qrows<<<R.sgrid(), 128, 0, sm>>>(a);
+      k_outer_begin<<<R.sgrid(), 128, 0, sm>>>(a);
+      R.launched(5);
+    }
     if (R.check("warp")) return R.st;
     // Step 2: orthonormalise, warm start, inner loop
-    if (inner_core(R, P, nullptr, 3, 1, it == 0)) return R.st;
+    {
+      NvtxRange nv_k3("K2-K3 orthonormalise + LADMAP inner loop");
+      if (inner_core(R, P, nullptr, 3, 1, it == 0)) return R.st;
+    }
     // Steps 3-4, outer stop
     k_dtau_red<<<R.egrid(L.plane), ENT, 0, sm>>>(a);
     if (R.zero_counter()) return R.st;
@@ -2183,6 +2211,8 @@ tilt_status svt(Ctx& ctx, const float* M, int B, int m, int n, const float* eps,
   R.launched();
   if (R.svt_core(eps, 1, 0, true)) return R.st;
   if (R.gemm(false, true, m, n, n, L.oB, L.ldm, a.oV, L.ldn, L.oAn, L.ldm)) return R.st;
+  k_svt_moreau<<<R.egrid(L.plane), ENT, 0, sm>>>(a, L.oAn);
+  R.launched();
   k_from_plane<<<dim3((n + 31) / 32, (m + 31) / 32, B), dim3(32, 8), 0, sm>>>(A, a, L.oAn, m, n, L.ldm, 0);
   k_svt_out<<<dim3((n + 127) / 128, B), 128, 0, sm>>>(a, sigma, sweeps);
   R.launched(2);

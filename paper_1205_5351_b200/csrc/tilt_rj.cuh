@@ -58,6 +58,11 @@ __device__ __forceinline__ u64 add2(u64 a, u64 b) {
   asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
   return d;
 }
+// packed a + e - d, each half exact up to the final rounding (res3 of tilt_device.cuh)
+__device__ __forceinline__ u64 res3_2(u64 a, u64 e, u64 d) {
+  const float2 x = up(a), y = up(e), z = up(d);
+  return pk(res3(x.x, y.x, z.x), res3(x.y, y.y, z.y));
+}
 __device__ __forceinline__ u64 sub2(u64 a, u64 b) {
   u64 d;
   asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
@@ -1091,7 +1096,7 @@ __device__ void solve_patch_rj(const SolveArgs& a, const W<NC>& w, int b) {
     const float mu_max = P.mu_max_ratio * mu0;
     // ---- M_0 = A - W^TW(A + E - D) - Y/mu0, B = M_0 V --------------------------------------
     {
-      proj_z<NC>(w, [&](int j) { return sub2(add2(w.ld(Ap, j), w.ld(Ep, j)), w.ld(Dp, j)); }, z);
+      proj_z<NC>(w, [&](int j) { return res3_2(w.ld(Ap, j), w.ld(Ep, j), w.ld(Dp, j)); }, z);
       const float inv = 1.f / mu0;
       build_b<NC>(w, w.Bm(), [&](int k, u64& m0, u64& m1) {
         u64 mk[2];
@@ -1103,7 +1108,7 @@ __device__ void solve_patch_rj(const SolveArgs& a, const W<NC>& w, int b) {
             continue;
           }
           const u64 av = w.ld(Ap, j);
-          const u64 v = sub2(add2(av, w.ld(Ep, j)), w.ld(Dp, j));
+          const u64 v = res3_2(av, w.ld(Ep, j), w.ld(Dp, j));
           const u64 r = sub2(v, proj_apply<NC>(w, j, z));
           mk[h] = fmas2(w.ld(Yp, j), -inv, sub2(av, r));
         }
@@ -1134,7 +1139,7 @@ __device__ void solve_patch_rj(const SolveArgs& a, const W<NC>& w, int b) {
       const float inv_mu = 1.f / mu;
       const float thr = lam * inv_mu;
       const float *__restrict__ GXp = w.GX(), *__restrict__ GYp = w.GY(), *__restrict__ GZp = w.GZ();
-      proj_z<NC>(w, [&](int j) { return sub2(add2(w.ld(Ap, j), w.ld(Ep, j)), w.ld(Dp, j)); }, z);
+      proj_z<NC>(w, [&](int j) { return res3_2(w.ld(Ap, j), w.ld(Ep, j), w.ld(Dp, j)); }, z);
       float dE2 = 0.f;
       u64 acc[9];
 #pragma unroll
@@ -1143,14 +1148,14 @@ __device__ void solve_patch_rj(const SolveArgs& a, const W<NC>& w, int b) {
       for (int j = 0; j < n; ++j) {
         const ColG cg = load_g<NC>(w, GXp, GYp, GZp, Dp, j);
         const u64 e = w.ld(Ep, j), av = w.ld(Ap, j), yv = w.ld(Yp, j);
-        const u64 v = sub2(add2(av, e), cg.d);
+        const u64 v = res3_2(av, e, cg.d);
         const u64 pv = sub2(v, apply_g<NC>(w, cg, z));
         const u64 nk = fmas2(yv, -inv_mu, sub2(e, pv));
         const u64 en = shrink2(nk, thr);
         const u64 d = sub2(en, e);
         dE2 += hsum(mul2(d, d));
         w.st(Ep, j, en);
-        accum_g(cg, w.vv, sub2(add2(av, en), cg.d), acc);
+        accum_g(cg, w.vv, res3_2(av, en, cg.d), acc);
       }
       dE2 = wsum(dE2);
       const float c2 = mu * sqrtf(fmaxf(sst.dA2, dE2)) * inv_den;
@@ -1172,7 +1177,7 @@ __device__ void solve_patch_rj(const SolveArgs& a, const W<NC>& w, int b) {
           }
           const ColG cg = load_g<NC>(w, GXp, GYp, GZp, Dp, j);
           const u64 av = w.ld(Ap, j);
-          const u64 v = sub2(add2(av, w.ld(Ep, j)), cg.d);
+          const u64 v = res3_2(av, w.ld(Ep, j), cg.d);
           const u64 r = sub2(v, apply_g<NC>(w, cg, z));
           const u64 y = fmas2(r, mu, w.ld(Yp, j));
           w.st(Yp, j, y);
@@ -1207,7 +1212,7 @@ __device__ void solve_patch_rj(const SolveArgs& a, const W<NC>& w, int b) {
     svt_rank = sst.rank;
     // ---- Step 3: dtau = L^{-T} K^T (A + E - D_hat) (Eq. Delta_tau) ---------------------------
     float s[8];
-    proj_s<NC>(w, [&](int j) { return sub2(add2(w.ld(Ap, j), w.ld(Ep, j)), w.ld(Dp, j)); }, s);
+    proj_s<NC>(w, [&](int j) { return res3_2(w.ld(Ap, j), w.ld(Ep, j), w.ld(Dp, j)); }, s);
     float l1 = 0.f;
     for (int j = 0; j < n; ++j) {
       const float2 e2 = up(w.ld(Ep, j));

@@ -89,44 +89,3 @@ def test_missing_library_fails_loudly():
                        capture_output=True, text=True, timeout=300)
     assert r.returncode != 0
     assert "libtilt" in (r.stderr + r.stdout)
-
-
-@pytest.mark.parametrize("n,units", [(2, 32), (3, 32), (32, 32), (33, 32), (50, 32), (63, 32), (64, 32),
-                                     (65, 64), (100, 64), (127, 64), (128, 64)])
-def test_jacobi_schedule_is_a_sweep(n, units):
-    """The column-reuse pair schedule of the CTA-per-patch SVT (host builder in the library, no GPU):
-    every column pair exactly once per sweep, no column twice in a round, at most `units` pairs per
-    round, and a unit keeps its column i across consecutive rounds of a phase (the reuse that halves
-    the shared-memory column loads)."""
-    import ctypes
-    import numpy as np
-    from paper_1205_5351_b200 import lib
-    cap = 4 * n * units + 64
-    buf = (ctypes.c_uint16 * cap)()
-    r = lib.tilt_jacobi_schedule(n, units, buf, cap)
-    assert r > 0
-    tab = np.frombuffer(buf, dtype=np.uint16, count=r * units).reshape(r, units)
-    seen = set()
-    keeps = loads = 0
-    for row_i, row in enumerate(tab):
-        cols = []
-        for u, code in enumerate(row):
-            if code == 0xFFFF:
-                continue
-            i, j = int(code) >> 8, int(code) & 0xFF
-            cols.append(i)
-            if j != 0xFF:
-                cols.append(j)
-                assert i < n and j < n and i != j
-                key = (min(i, j), max(i, j))
-                assert key not in seen
-                seen.add(key)
-            if row_i > 0 and tab[row_i - 1, u] != 0xFFFF and int(tab[row_i - 1, u]) >> 8 == i:
-                keeps += 1
-            else:
-                loads += 1
-        assert len(cols) == len(set(cols))
-    assert len(seen) == n * (n - 1) // 2
-    assert r <= n + 8  # about as many rounds as the round-robin's n - 1
-    if n >= 32:
-        assert keeps > 3 * loads
