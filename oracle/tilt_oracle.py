@@ -587,7 +587,7 @@ def relative_rank(sigma_a):
     return int(np.sum(ratio > 1e-3)), bool(np.any((ratio >= 3e-4) & (ratio <= 3e-3)))
 
 
-def tilt(image, box, tau0, kind, prm: Params = Params(), rho_replay=None, warm=None):
+def tilt(image, box, tau0, kind, prm: Params = Params(), rho_replay=None, warm=None, inner_replay=None):
     """Algorithm 1 for one window; returns a dict (tau, A, E, Y, report fields, traces).
 
     Step 1: normalise D o tau and compute J; Q per reading Z10.
@@ -598,6 +598,9 @@ def tilt(image, box, tau0, kind, prm: Params = Params(), rho_replay=None, warm=N
     Step 4: tau^{i+1} = tau^i + Delta tau* (P:568-570).
     Outer stop ("while not converged", reading Z9).
     ``rho_replay``: optional list (per outer iteration) of 0/1 sequences (reading Z21).
+    ``inner_replay``: optional list (per outer iteration) of inner-iteration counts: the inner loop
+    of outer iteration i runs exactly inner_replay[i] iterations (replaying another run's Cond1 &
+    Cond2 decisions; parity protocol, reading Z21).
     ``warm``: optional (A, E, Y) that replace the first inner loop's cold start A_0 = D_hat,
     E_0 = Y_0 = 0 (then Y_0 <- W^TW Y as every warm start, Eq. Y_new_warmstart); used by
     the pyramid's fine level (reading Z26). Ignored without VWS.
@@ -653,8 +656,11 @@ def tilt(image, box, tau0, kind, prm: Params = Params(), rho_replay=None, warm=N
             replay = rho_replay[it] if rho_replay is not None and it < len(rho_replay) else None
             noise = ((prm.crit_noise, np.random.default_rng([prm.noise_seed, it]))
                      if prm.crit_noise > 0 else None)
+            fixed = prm.fixed_inner_iters
+            if inner_replay is not None and it < len(inner_replay):
+                fixed = int(inner_replay[it])
             res = ladmap(dh, proj, lam, mu0, prm.mu_max_ratio * mu0, prm.rho0, prm.eps1, prm.eps2,
-                         prm.max_inner, a, e, y, fixed_iters=prm.fixed_inner_iters, rho_replay=replay, svd=prm.svd,
+                         prm.max_inner, a, e, y, fixed_iters=fixed, rho_replay=replay, svd=prm.svd,
                          crit_noise=noise)
             a, e, y = res.A, res.E, res.Y
             inner_iters += res.iters

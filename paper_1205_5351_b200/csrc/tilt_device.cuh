@@ -84,7 +84,6 @@ struct Scal {
   int flag;
   int patch;
   int rot_acc;       // Jacobi rotations of the current SVT
-  int svt_comp;      // 1: the current SVT is formed as M - P_eps(M) (Moreau form, svt())
 };
 
 // --------------------------------------------------------------------------------------------
@@ -297,33 +296,13 @@ __device__ __forceinline__ void transpose_nn(float* __restrict__ Ym, const float
 #include "tilt_jacobi.cuh"
 
 // sigma_j = sqrt(ns_j.x) stats after the final pass: nuclear norm of S_eps, ranks (Z19), sigma_1.
-// Scale B for the SVT product: column j by h_j / ||v_j||^2 (A = B V^T), or by (1 - h_j) / ||v_j||^2
-// when sum_j min(sigma_j, eps)^2 < sum_j max(sigma_j - eps, 0)^2 (the Moreau form M - B V^T)
+// Scale B for the SVT product A = B diag(h_j / ||v_j||^2) V^T
 template <class C>
-__device__ __forceinline__ void col_scale(Ctx<C>& cx, float eps) {
-  const int n = cx.n;
-  if (threadIdx.x < 32) {
-    float kept = 0.f, disc = 0.f;
-    for (int j = threadIdx.x; j < n; j += 32) {
-      const float sg = sqrtf(cx.ns[j].x);
-      const float a = fmaxf(sg - eps, 0.f), c = fminf(sg, eps);
-      kept = fmaf(a, a, kept);
-      disc = fmaf(c, c, disc);
-    }
-#pragma unroll
-    for (int off = 16; off; off >>= 1) {
-      kept += __shfl_xor_sync(FULL, kept, off);
-      disc += __shfl_xor_sync(FULL, disc, off);
-    }
-    if (threadIdx.x == 0) cx.sc->svt_comp = disc < kept ? 1 : 0;
-  }
-  __syncthreads();
-  const bool comp = cx.sc->svt_comp != 0;
-  const int lds = cx.lds, rows = round4(cx.m);
+__device__ __forceinline__ void col_scale(Ctx<C>& cx) {
+  const int n = cx.n, lds = cx.lds, rows = round4(cx.m);
   for (int e = threadIdx.x; e < n * (rows >> 2); e += C::NT) {
     const int j = e / (rows >> 2), i0 = (e - j * (rows >> 2)) * 4;
-    const float h = cx.hv[j];
-    const float f = (comp ? 1.f - h : h) * cx.ns[j].y;
+    const float f = cx.hv[j] * cx.ns[j].y;
     float4* bp = reinterpret_cast<float4*>(cx.B + j * lds + i0);
     float4 b = *bp;
     b.x *= f;
@@ -430,20 +409,8 @@ __device__ SvtOut svt(Ctx<C>& cx, const float* X, float eps, float tol, int max_
   col_pass<C, 2>(cx, eps);  // sigma_j, h_j, 1 / ||v_j||^2
   svt_stats<C>(cx, eps);
   if constexpr (DO_OUT) {
-    // S_eps(M) = B diag(h) V^T, or, when the shrunk-away part is the smaller one, the Moreau form
-    // M - B diag(1 - h) V^T = M - P_eps(M) (P_eps: projection onto the spectral ball of radius eps;
-    // the same matrix in exact arithmetic). At large mu the correction is O(eps) and the fp32 error
-    // of A falls from the SVT's (~1e-6 ||A||, which put a floor of mu 1e-6 under crit2) to ~ulp(M).
-    col_scale<C>(cx, eps);
-    const bool comp = cx.sc->svt_comp != 0;
-    const int lds = cx.lds;
-    gemm_bvt<C>(cx.B, cx.V, cx.lds, cx.m, cx.n, [&](int i0, int j, float4 p) {
-      if (comp) {
-        const float4 x = *reinterpret_cast<const float4*>(X + j * lds + i0);
-        p = make_float4(x.x - p.x, x.y - p.y, x.z - p.z, x.w - p.w);
-      }
-      out(i0, j, p);
-    });
+    col_scale<C>(cx);
+    gemm_bvt<C>(cx.B, cx.V, cx.lds, cx.m, cx.n, out);  // A = B diag(h) V^T
   }
   __syncthreads();
   if (ns_after) ns_step<C>(cx);

@@ -56,7 +56,6 @@ struct St {
   float inv_nd;  // ADM: 1 / ||D||_F
   int svt_rank, relrank, band;
   int iters, done, status, conv;
-  int comp;        // the current SVT is formed as M - P_eps(M) (Moreau form; k_svt_stats)
   int svt_done, big_any, rot_any, sw_cur, cap_cur, rot_cur;
   int sweeps, caps, rotations, aux_sweeps;
   double fro2;  // ||B||_F^2 at the start of the current SVT (negligible-column threshold)
@@ -696,17 +695,15 @@ __global__ void __launch_bounds__(32) k_svt_stats(Args a, int count_sweeps, int 
   const float* sig = slot(a, b) + a.L.oSig;
   const float eps = st->eps;
   const int lane = threadIdx.x, n = a.L.n;
-  float nuc = 0.f, smax = 0.f, amax = 0.f, kept = 0.f, disc = 0.f;
+  float nuc = 0.f, smax = 0.f, amax = 0.f;
   int cnt = 0;
   for (int j = lane; j < n; j += 32) {
     const float sg = sig[j];
-    const float x = fmaxf(sg - eps, 0.f), c = fminf(sg, eps);
+    const float x = fmaxf(sg - eps, 0.f);
     nuc += x;
     smax = fmaxf(smax, sg);
     amax = fmaxf(amax, x);
     cnt += (sg > eps);
-    kept = fmaf(x, x, kept);
-    disc = fmaf(c, c, disc);
   }
 #pragma unroll
   for (int off = 16; off; off >>= 1) {
@@ -714,8 +711,6 @@ __global__ void __launch_bounds__(32) k_svt_stats(Args a, int count_sweeps, int 
     smax = fmaxf(smax, __shfl_xor_sync(0xffffffffu, smax, off));
     amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, off));
     cnt += __shfl_xor_sync(0xffffffffu, cnt, off);
-    kept += __shfl_xor_sync(0xffffffffu, kept, off);
-    disc += __shfl_xor_sync(0xffffffffu, disc, off);
   }
   int rel = 0, band = 0;
   for (int j = lane; j < n; j += 32) {
@@ -732,7 +727,6 @@ __global__ void __launch_bounds__(32) k_svt_stats(Args a, int count_sweeps, int 
     band |= __shfl_xor_sync(0xffffffffu, band, off);
   }
   if (lane == 0) {
-    st->comp = which == 0 && disc < kept ? 1 : 0;  // the Moreau form when the shrunk part is smaller
     st->nuc = nuc;
     st->sig1 = smax;
     st->svt_rank = cnt;
@@ -761,19 +755,10 @@ __global__ void __launch_bounds__(ENT) k_svt_scale(Args a) {
     if (j >= a.L.n) continue;
     const float sg = sig[j], v2 = vv[j];
     const float h = sg > eps ? (sg - eps) / sg : 0.f;
-    w[a.L.oB + idx] *= v2 > 0.f ? (st->comp ? 1.f - h : h) / v2 : 0.f;
+    w[a.L.oB + idx] *= v2 > 0.f ? h / v2 : 0.f;
   }
 }
 
-// the Moreau form of the SVT (svt() in tilt_device.cuh): dst = M - B diag(1 - h) V^T = M - P_eps(M)
-// for the problems whose shrunk-away part is the smaller one (st->comp); M is in S
-__global__ void __launch_bounds__(ENT) k_svt_moreau(Args a, size_t dst) {
-  const int b = blockIdx.y;
-  St* st = state(a, b);
-  if (st->done || st->warm || !st->comp) return;
-  float* w = slot(a, b);
-  FOR_ELEMS(a.L.plane) w[dst + idx] = w[a.L.oS + idx] - w[dst + idx];
-}
 
 // ---------------------------------------------------------------------------------------------
 // One Jacobi round over a block pair (CROSS) or within one block (intra): see the header.
@@ -1976,8 +1961,6 @@ static bool inner_core(Run& R, const DevParams& P, const float* Q, int l, int q_
       R.launched();
       if (R.svt_core(nullptr, 0, 1, true)) return true;
       if (R.gemm(false, true, m, n, n, L.oB, L.ldm, a.oV, L.ldn, L.oA, L.ldm)) return true;
-      k_svt_moreau<<<R.egrid(L.plane), ENT, 0, sm>>>(a, L.oA);
-      R.launched();
       if (warm && (k % P.ns_period == P.ns_period - 1 || k + 1 == a.niter))
         if (R.ns_step()) return true;
       k_adm_e<<<R.egrid(L.plane), ENT, 0, sm>>>(a);
@@ -2024,8 +2007,6 @@ static bool inner_core(Run& R, const DevParams& P, const float* Q, int l, int q_
       R.nsub = 0;
     }
     if (R.gemm(false, true, m, n, n, L.oB, L.ldm, a.oV, L.ldn, L.oAn, L.ldm)) return true;
-    k_svt_moreau<<<R.egrid(L.plane), ENT, 0, sm>>>(a, L.oAn);
-    R.launched();
     if (warm && (k % P.ns_period == P.ns_period - 1 || k + 1 == a.niter))
       if (R.ns_step()) return true;
     if (R.svdws) {
@@ -2211,8 +2192,6 @@ tilt_status svt(Ctx& ctx, const float* M, int B, int m, int n, const float* eps,
   R.launched();
   if (R.svt_core(eps, 1, 0, true)) return R.st;
   if (R.gemm(false, true, m, n, n, L.oB, L.ldm, a.oV, L.ldn, L.oAn, L.ldm)) return R.st;
-  k_svt_moreau<<<R.egrid(L.plane), ENT, 0, sm>>>(a, L.oAn);
-  R.launched();
   k_from_plane<<<dim3((n + 31) / 32, (m + 31) / 32, B), dim3(32, 8), 0, sm>>>(A, a, L.oAn, m, n, L.ldm, 0);
   k_svt_out<<<dim3((n + 127) / 128, B), 128, 0, sm>>>(a, sigma, sweeps);
   R.launched(2);
