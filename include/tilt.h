@@ -106,9 +106,9 @@ typedef struct {
   int32_t win_h, win_w;
   /* kernel family: 0 = auto (the CTA-per-patch kernels up to 128 x 128, the multi-CTA path above:
    * at 200 x 200 it is 2.4x faster; the ADM inner entry stays on the CTA kernels up to 256),
-   * 1 = CTA-per-patch kernels, 2 = warp-per-patch kernel (m <= 64 and n <= 50; TILT_E_ARG otherwise),
-   * 3 = multi-CTA path (tilt_inner_batch only, LADMAP, m, n <= 1024: one problem spread over many
-   * CTAs, block-cyclic Jacobi, hand-written batched GEMM). All compute the same method; they
+   * 1 = CTA-per-patch kernels, 3 = multi-CTA path (m, n <= 1024: one problem spread over many
+   * CTAs, block-cyclic Jacobi, hand-written batched GEMM and LU). 2 (a
+   * warp-per-patch kernel, round 1) is retired: TILT_E_ARG. All compute the same method; they
    * differ in data layout, Jacobi ordering and how a problem maps to the GPU. */
   int32_t kernel_path;
   /* Newton-Schulz re-orthonormalisation of the carried V (reading Z14) after every ns_period-th
@@ -119,7 +119,7 @@ typedef struct {
   /* inner solver: 0 = LADMAP (the paper's), 1 = the ADM baseline of Zhang et al. as
    * restated in P:241-264 (three variables, mu_{k+1} = adm_rho mu_k unbounded, cold start every outer
    * iteration, dtau from the ADM). CTA kernels and the multi-CTA path (not the
-   * warp-per-patch kernel; not with svd_mode 1). */
+   * retired warp-per-patch kernel; not with svd_mode 1). */
   int32_t inner_solver;
   float adm_rho;          /* ADM penalty growth (default 1.25) */
   float adm_tol;          /* ADM stop: ||D + J dtau - A - E||_F / ||D||_F < adm_tol (default 1e-6: the
@@ -159,7 +159,7 @@ typedef struct {
   float dtau_inf;         /* ||dtau||_inf of the last outer iteration */
   float mu_last;          /* mu_K of the last SVT */
   int32_t jacobi_rotations; /* Jacobi rotations applied, summed over the LADMAP SVTs */
-  int32_t kernel_path;      /* 1: CTA-per-patch kernel, 2: warp-per-patch kernel, 3: multi-CTA path */
+  int32_t kernel_path;      /* 1: CTA-per-patch kernel, 3: multi-CTA path */
   int32_t svd_warm_steps;   /* SVTs replaced by the Alg. 2 warm step (svd_mode 1) */
 } tilt_report;
 
@@ -259,8 +259,8 @@ tilt_status tilt_inner_batch(tilt_handle* h, const float* D, const float* J, con
                              tilt_report* rep);
 
 /* Kernel family used by tilt_svt_batch: 0 = auto (CTA-per-patch up to 256 x 256, else multi-CTA),
- * 1 = CTA-per-patch, 2 = warp-per-patch (m <= 64, n <= 50), 3 = multi-CTA block-cyclic Jacobi
- * (m, n <= 1024) (step parity of every implementation). */
+ * 1 = CTA-per-patch, 3 = multi-CTA block-cyclic Jacobi (m, n <= 1024) (step parity of both);
+ * 2 (warp-per-patch) is retired: TILT_E_ARG. */
 tilt_status tilt_set_svt_path(tilt_handle* h, int32_t path);
 
 /* Number of kernel launches issued by this handle since creation (for bench accounting). */

@@ -62,6 +62,9 @@ class Params:
                                 # 1e-7 reproduces Table 1's ADM counts in fp64, 1e-6 is fp32-resolvable)
     pyramid_warm: bool = False  # 2-level pyramid: the fine level's first inner loop starts from the
                                 # coarse A, E, Y upsampled (reading Z26)
+    tau_noise: float = 0.0      # test instrumentation (reading Z22): tau <- tau (1 + tau_noise N(0,1))
+                                # after every outer update, seeded by noise_seed -- the chain
+                                # sensitivity of the outer loop to per-step differences; 0 = exact
     crit_noise: float = 0.0     # test instrumentation (reading Z22): Cond1's statistic is compared as
     noise_seed: int = 0         # crit1 (1 + crit_noise N(0,1)) -- the relative resolution of an fp32
                                 # crit1 near eps1 -- to classify decision-sensitive patches; 0 = exact
@@ -667,6 +670,8 @@ def tilt(image, box, tau0, kind, prm: Params = Params(), rho_replay=None, warm=N
             outer_traces.append(res.trace)
             dtau = proj.delta_tau(a + e - dh)          # Step 3
         tau = tau + dtau                           # Step 4
+        if prm.tau_noise > 0:
+            tau = tau * (1.0 + prm.tau_noise * np.random.default_rng([prm.noise_seed, 7, it]).standard_normal(tau.shape))
         tau_path.append(tau.copy())
         dtau_inf = float(np.max(np.abs(dtau)))
         f = float(shrink(res.sigma_m, 1.0 / res.mu).sum()) + lam * float(np.abs(e).sum())

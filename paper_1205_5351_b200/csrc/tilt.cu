@@ -12,7 +12,6 @@
 #include "tilt_kernels.cuh"
 #include "tilt_large_host.h"
 #include "tilt_nvtx.h"
-#include "tilt_rj_host.h"
 
 using namespace tilt;
 
@@ -71,7 +70,7 @@ struct tilt_handle {
   float* h_E = nullptr;
   tilt_report* h_rep = nullptr;
   int64_t launches = 0;
-  int svt_path = 0;  // tilt_svt_batch kernel family (tilt_set_svt_path): 0/1 CTA-per-patch, 2 warp-per-patch,
+  int svt_path = 0;  // tilt_svt_batch kernel family (tilt_set_svt_path): 0/1 CTA-per-patch, (2 retired),
                      // 3 multi-CTA
   tilt::lp::Ctx lp;  // multi-CTA path for large windows (workspace on first use)
   size_t lp_budget = 0;  // bytes of multi-CTA workspace (batches above it run in chunks)
@@ -137,15 +136,13 @@ bool params_ok(const tilt_params* p) {
   if (p->fixed_inner_iters > p->max_inner || p->fixed_outer_iters > p->max_outer) return false;
   if (p->pyramid_levels < 1 || p->pyramid_levels > 2) return false;
   if (p->constraint_mode != TILT_CONSTRAINTS_NONE && p->constraint_mode != TILT_CONSTRAINTS_CENTER_AREA) return false;
-  if (p->kernel_path < 0 || p->kernel_path > 3) return false;
+  if (p->kernel_path < 0 || p->kernel_path > 3 || p->kernel_path == 2) return false;  // 2: retired
   if (p->inner_solver == 1 && p->svd_mode == 1) return false;  // SVDWS is LADMAP's (Table 1's third column)
   if (p->inner_solver < 0 || p->inner_solver > 1) return false;
   if (p->ctas_per_sm < 0) return false;
   if (p->pyramid_warm < 0 || p->pyramid_warm > 1) return false;
-  if (p->pyramid_warm && p->kernel_path == 2) return false;  // the warp-per-patch kernel starts cold
   if (p->svd_mode < 0 || p->svd_mode > 1) return false;
   if (!std::isfinite(p->svd_ws_gate) || p->svd_ws_gate < 0.f) return false;
-  if (p->inner_solver == 1 && p->kernel_path == 2) return false;  // the warp-per-patch kernel runs LADMAP only
   if (!std::isfinite(p->adm_rho) || !std::isfinite(p->adm_tol) || p->adm_rho < 1.f || p->adm_tol <= 0.f) return false;
   return true;
 }
@@ -443,12 +440,6 @@ tilt_status tilt_create(tilt_handle** out, const tilt_create_opts* o) {
     h->ws_slots = h->num_sms * (occ > 0 ? occ : 1);
     h->ws_floats = wsf * h->ws_slots;
   }
-  // the warp-per-patch kernel (m <= 64, n <= 50) needs its own slots; take the larger need
-  {
-    const int mm = h->max_m < 64 ? h->max_m : 64, nn = h->max_n < 50 ? h->max_n : 50;
-    const size_t rjf = tilt::rjh::ws_need(h->num_sms, mm, nn);
-    if (rjf > h->ws_floats) h->ws_floats = rjf;
-  }
   if (h->ws_floats > 0) {
     if ((e = cudaMalloc(&h->ws, h->ws_floats * sizeof(float))) != cudaSuccess) return fail(e, "cudaMalloc(ws)");
   }
@@ -501,7 +492,7 @@ tilt_status tilt_set_stream(tilt_handle* h, void* stream) {
 int64_t tilt_launch_count(const tilt_handle* h) { return h ? h->launches : 0; }
 
 tilt_status tilt_set_svt_path(tilt_handle* h, int32_t path) {
-  if (!h || path < 0 || path > 3) return TILT_E_ARG;
+  if (!h || path < 0 || path > 3 || path == 2) return TILT_E_ARG;  // 2: the retired warp-per-patch family
   h->svt_path = path;
   return TILT_OK;
 }
@@ -577,12 +568,6 @@ static tilt_status solve_level(tilt_handle* h, const float* images, int32_t n_im
     }
     return TILT_OK;
   }
-  const bool rj_ok = tilt::rjh::fits(m, n);
-  if (prm->kernel_path == 2 && !rj_ok) {
-    g_last_error = "kernel_path = 2 (warp-per-patch) needs m <= 64 and n <= 50";
-    return TILT_E_ARG;
-  }
-  if (rj_ok && prm->kernel_path == 2 && prm->inner_solver == 0) return tilt::rjh::solve(h->num_sms, h->ws, h->ws_floats, h->counter, h->stream, a, &h->launches, &g_last_error);
   return dispatch<SolveF>(size_class(m, n), h, a);
 }
 
@@ -776,7 +761,6 @@ tilt_status tilt_svt_batch(tilt_handle* h, const float* M, int32_t B, int32_t m,
     }
     return TILT_OK;
   }
-  if (tilt::rjh::fits(m, n) && h->svt_path == 2) return tilt::rjh::svt(h->num_sms, h->ws, h->ws_floats, h->stream, a, &h->launches, &g_last_error);
   return dispatch<SvtF>(size_class(m, n), h, a);
 }
 

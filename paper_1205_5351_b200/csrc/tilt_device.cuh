@@ -71,8 +71,9 @@ struct Scal {
   double Linv[64];   // L^{-1}, L L^T = G = J^TJ + Q^TQ (row-major p x p, lower)
   double dred[16 * 12];
   double dout[12];
-  float Lp[64];      // L^{-1} / ||d|| (fp32, implicit projector)
-  float cp[8];       // L^{-1} c / ||d||, c = D_hat^T J_raw
+  double sd[8];      // K^T v of the last implicit-projector reduce (fp64)
+  double Lp[64];     // L^{-1} / ||d|| (implicit projector; fp64 so that L'(J_raw^T v) - c'(D_hat^T v)
+  double cp[8];      // does not cancel in fp32);  L^{-1} c / ||d||, c = D_hat^T J_raw
   float fred[32 * 10];
   float fout[12];
   float nd;          // ||D o tau||_F
@@ -114,6 +115,30 @@ __device__ __forceinline__ void block_sum_f(float (&v)[KV], Scal* sc) {
   __syncthreads();
 #pragma unroll
   for (int k = 0; k < KV; ++k) v[k] = sc->fout[k];
+}
+
+// fp32 warp sums, combined across warps in fp64 (the implicit projector's K^T v: partials of a
+// residual cancel across the CTA; a warp's 32 x ~10 pixels are summed by an fp32 tree)
+template <class C, int KV>
+__device__ __forceinline__ void block_sum_fd(const float (&v)[KV], double (&out)[KV], Scal* sc) {
+  static_assert(KV <= 10, "fred holds 10 values per warp");
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < KV; ++k) {
+    float x = v[k];
+#pragma unroll
+    for (int off = 16; off; off >>= 1) x += __shfl_xor_sync(FULL, x, off);
+    if (lane == 0) sc->fred[w * 10 + k] = x;
+  }
+  __syncthreads();
+  if (threadIdx.x < KV) {
+    double s = 0.0;
+    for (int ww = 0; ww < C::NWARPS; ++ww) s += (double)sc->fred[ww * 10 + threadIdx.x];
+    sc->dout[threadIdx.x] = s;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < KV; ++k) out[k] = sc->dout[k];
 }
 
 // fp64 block sum (used once per outer iteration): warp shuffles, then warps 0..KV-1 finish.
@@ -639,37 +664,47 @@ struct ProjImplicit {
       }
       a[8] = fmaf(Dp[idx], val, a[8]);
     }
-    float r[9];
+    // the warps' partial sums are combined in fp64, and so are J_raw^T v and D_hat^T v, which
+    // cancel in K^T v = L'(J_raw^T v) - c'(D_hat^T v): with fp32 coefficients and combination the
+    // projected residual of the LADMAP iteration carried ~1e-6 relative errors that the dual step
+    // integrates (tools/inner_drift.py: A 1e-4 off the fp64 iterate after 400 iterations, inner
+    // loops running to max_inner); in fp64 the solve path tracks the oracle as the explicit entry does
+    float a9[9];
 #pragma unroll
-    for (int k = 0; k < 9; ++k) r[k] = a[k];
-    block_sum_f<C, 9>(r, cx.sc);
+    for (int k = 0; k < 9; ++k) a9[k] = a[k];
+    double r[9];
+    block_sum_fd<C, 9>(a9, r, cx.sc);
     // s = L' r[0:p] - c' r[8]  (K^T v)
-    const float* Lp = cx.sc->Lp;
-    const float* cp = cx.sc->cp;
+    const double* Lp = cx.sc->Lp;
+    const double* cp = cx.sc->cp;
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
-      float acc = -cp[q] * r[8];
+      double acc = -cp[q] * r[8];
 #pragma unroll
-      for (int b = 0; b <= q; ++b) acc = fmaf(Lp[q * 8 + b], r[b], acc);
-      s[q] = acc;
+      for (int b = 0; b <= q; ++b) acc = fma(Lp[q * 8 + b], r[b], acc);
+      s[q] = (float)acc;
+      cx.sc->sd[q] = acc;  // (every thread writes the same value)
     }
   }
-  // coefficients for apply: z = L'^T s (8), w = c'^T s
+  // coefficients for apply: z = L'^T s (8), w = c'^T s (from the fp64 s of the last reduce)
   template <class C>
   static __device__ __forceinline__ void coeffs(const Ctx<C>& cx, const float (&s)[8], float (&z)[9]) {
-    const float* Lp = cx.sc->Lp;
-    const float* cp = cx.sc->cp;
+    const double* Lp = cx.sc->Lp;
+    const double* cp = cx.sc->cp;
+    double sd[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) sd[q] = cx.sc->sd[q];
 #pragma unroll
     for (int b = 0; b < 8; ++b) {
-      float acc = 0.f;
+      double acc = 0.0;
 #pragma unroll
-      for (int q = b; q < 8; ++q) acc = fmaf(Lp[q * 8 + b], s[q], acc);
-      z[b] = acc;
+      for (int q = b; q < 8; ++q) acc = fma(Lp[q * 8 + b], sd[q], acc);
+      z[b] = (float)acc;
     }
-    float w = 0.f;
+    double w = 0.0;
 #pragma unroll
-    for (int q = 0; q < 8; ++q) w = fmaf(cp[q], s[q], w);
-    z[8] = w;
+    for (int q = 0; q < 8; ++q) w = fma(cp[q], sd[q], w);
+    z[8] = (float)w;
   }
   // (K y)(pixel) with y the K^T v of reduce(); z from coeffs()
   template <class C>
@@ -791,10 +826,10 @@ __device__ int orthonormalise_implicit(Ctx<C>& cx, const double* qrows, int l) {
       for (int a = 0; a < 8; ++a) {
         double cpa = 0.0;
         for (int b = 0; b < 8; ++b) {
-          sc->Lp[a * 8 + b] = (float)(sc->Linv[a * 8 + b] * ind);
+          sc->Lp[a * 8 + b] = sc->Linv[a * 8 + b] * ind;
           cpa += sc->Linv[a * 8 + b] * c[b];
         }
-        sc->cp[a] = (float)(cpa * ind);
+        sc->cp[a] = cpa * ind;
       }
     }
   }

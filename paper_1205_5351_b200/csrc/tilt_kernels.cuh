@@ -532,11 +532,14 @@ __device__ void solve_patch(const SolveArgs& a, Ctx<C>& cx, int b) {
     svt_rank = cx.sc->svt_rank;
     // Step 3: dtau = G^{-1} J^T (A + E - D_hat) = L^{-T} K^T (A + E - D_hat)  (Eq. Delta_tau)
     float s[8];
+    double sd[8];
     if (P.inner_solver == 1) {  // the ADM's own dtau (Eq. update_detla_Tau)
 #pragma unroll
-      for (int q = 0; q < 8; ++q) s[q] = s_adm[q];
+      for (int q = 0; q < 8; ++q) sd[q] = s_adm[q];
     } else {
-      PR::reduce(cx, [&](int idx) { return cx.A[idx] + cx.E[idx] - cx.D[idx]; }, s);
+      PR::reduce(cx, [&](int idx) { return res3(cx.A[idx], cx.E[idx], cx.D[idx]); }, s);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) sd[q] = cx.sc->sd[q];  // K^T (A + E - D_hat) in fp64
     }
     const float l1 = plane_l1<C>(cx, cx.E);
     const double* Li = cx.sc->Linv;
@@ -544,7 +547,7 @@ __device__ void solve_patch(const SolveArgs& a, Ctx<C>& cx, int b) {
     bool finite = true;
     for (int q = 0; q < p; ++q) {  // Step 4: tau += dtau
       double dq = 0.0;
-      for (int r = q; r < p; ++r) dq += Li[r * 8 + q] * (double)s[r];
+      for (int r = q; r < p; ++r) dq += Li[r * 8 + q] * sd[r];
       tau[q] = (double)(float)(tau[q] + dq);  // tau carried in fp32 between outer iterations (Z28)
       dt_inf = fmax(dt_inf, fabs(dq));
       finite = finite && isfinite(tau[q]);

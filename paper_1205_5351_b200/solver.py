@@ -158,7 +158,7 @@ class TiltSolver:
 
     def svt(self, M, eps, V=None, path: int = 0):
         """tilt_svt_batch; path 0 = auto (CTA kernel up to 256 x 256, else multi-CTA), 1 = CTA kernel,
-        2 = warp-per-patch kernel, 3 = multi-CTA block-Jacobi path (any m, n <= 1024)."""
+        3 = multi-CTA block-Jacobi path (any m, n <= 1024); 2 (warp-per-patch) is retired."""
         dev = self.device
         check(lib.tilt_set_svt_path(self._h, path), "tilt_set_svt_path")
         M = _dev(M, torch.float32, dev)

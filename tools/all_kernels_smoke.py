@@ -1,7 +1,7 @@
 """Small invocations of every kernel family: the CTA-per-patch solve (S32 and S64 classes), the
-warp-per-patch solve, the SVT, projector and inner entries, and the multi-CTA path (LADMAP and
-LADMAP+SVDWS) -- a quick "everything launches and returns" check (and the command to run under
-compute-sanitizer where that tool is available; it is closed on the GPU pool used this round).
+K1 warp, SVT, projector and inner entries, and the multi-CTA path (LADMAP and LADMAP+SVDWS with
+the LU-solved Cayley step) -- a quick "everything launches and returns" check, and the program the
+compute-sanitizer runs use (profiles/r02/sanitizer_*.log).
 Usage: python tools/all_kernels_smoke.py [--only NAME]"""
 import argparse
 import os
@@ -41,10 +41,11 @@ def solve(cfg_id, path, K=3):
 
 run("solve_s32", lambda: solve(1, 1))
 run("solve_s64", lambda: solve(2, 1))
-run("solve_rj", lambda: solve(2, 2))
 
 
 def entries():
+    b = ts.gen_batch(ts.CONFIGS[2], 0, 2)
+    s.warp(b["images"], b["patch_image"], b["boxes"], b["tau0"], ts.CONFIGS[2].kind)
     rng = np.random.default_rng(0)
     M = rng.normal(size=(2, 50, 50)).astype(np.float32)
     s.svt(M, [0.1, 0.2])
