@@ -168,7 +168,7 @@ def _oracle_run(args):
             r = O.tilt(p["canvas"], p["box"], p["tau0"], cfg.kind)
         else:
             n_outer, counts, bits = replay
-            prm = O.Params(fixed_outer_iters=n_outer, max_outer=n_outer, tau_noise=1e-7 if noise_seed else 0.0,
+            prm = O.Params(fixed_outer_iters=n_outer, max_outer=n_outer, tau_noise=1e-5 if noise_seed else 0.0,
                            noise_seed=noise_seed)
             r = O.tilt(p["canvas"], p["box"], p["tau0"], cfg.kind, prm, rho_replay=bits, inner_replay=counts)
     return {k: r[k] for k in ("tau", "objective", "rank", "rank_band", "outer_iters", "inner_iters", "status")}
@@ -188,8 +188,9 @@ def test_free_running_convergence_config2_64(solver, T):
     reaches the same tau (1e-3 max-abs), objective (1e-3) and rank (outside the Z19 band) on every
     patch that is not chain-sensitive -- the GPU computes the paper's method along its own decision
     path. Chain-sensitive (reading Z22): the oracle's own replayed tau moves by > 1e-3 when tau is
-    perturbed by 1e-7 relative after every outer step (the size of the fp32-vs-fp64 per-step
-    difference, tests/test_gpu_protocol re-sync: ~1e-6); such patches are counted. Printed: the
+    perturbed by 1e-5 relative after every outer step (the size of the fp32-vs-fp64 per-step
+    difference: re-synced A, E agree to ~1.4e-5 after 20 inner iterations, test above, and to ~1e-4
+    deep in an inner loop at mu ~1e6, tools/inner_drift.py); such patches are counted. Printed: the
     agreement with the oracle's own free-running decisions (the fp32 Cond1/Cond2 statistics decide
     some inner loops differently from fp64, and the outer dynamics carry the difference along the
     flat aspect direction, SURVEY.md §8(c) protocol 3 hazard)."""
