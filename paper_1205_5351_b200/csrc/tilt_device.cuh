@@ -475,12 +475,18 @@ __device__ __forceinline__ WarpGeom make_geom(const int* box, const double* tau,
 // the warp-per-patch and multi-CTA paths): the source coordinate in fp64 (an fp32 coordinate of a
 // 100-pixel canvas would carry ~6e-6 px of rounding into the fractions), the 4 taps, the bilinear
 // value and the exact interpolant gradient (reading Z2) in fp32 from the fp32 fractions.
-// a + e - d of three fp32 values, exact up to the final rounding (fp64 sum): the LADMAP residual
+// a + e - d of three fp32 values, exact up to the final rounding: the LADMAP residual
 // A + E - D_hat cancels O(1e-2) entries down to O(1e-9), so summed in fp32 its rounding (~ulp(a + e)
 // per entry, ~2e-7 in norm at 50 x 50) was the crit1 floor (Z7) and, through Y += mu R, put a floor
 // of ~mu 1e-6 under crit2: fp32 inner loops that the fp64 oracle ends at mu ~ 2e5 ran to max_inner
+// Knuth's TwoSum gives s + err = a + e exactly in fp32; s - d is then exact when s and d are within a
+// factor 2 (Sterbenz), which is the cancelling case; otherwise its rounding is relative to a result
+// that is not small. 8 fp32 operations instead of the fp64 sum's conversions.
 __device__ __forceinline__ float res3(float a, float e, float d) {
-  return (float)(((double)a + (double)e) - (double)d);
+  const float s = __fadd_rn(a, e);
+  const float bb = __fsub_rn(s, a);
+  const float err = __fadd_rn(__fsub_rn(a, __fsub_rn(s, bb)), __fsub_rn(e, bb));
+  return __fadd_rn(__fsub_rn(s, d), err);
 }
 
 struct WarpTap {

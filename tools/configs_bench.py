@@ -27,7 +27,8 @@ a = ap.parse_args()
 for cid in [int(c) for c in a.configs.split(",")]:
     cfg = ts.CONFIGS[cid]
     B = min(cfg.batch, a.cap)
-    b = bench.gen_shard(cid, 0, B)
+    b = bench.gen_shard(cid, range(B))
+    b["patch_image"] = np.arange(B, dtype=np.int32)
     m, n, p = cfg.m, cfg.n, cfg.p
     s = T.TiltSolver(0, max_batch=B, max_m=m, max_n=n, max_p=p, max_image_elems=int(b["images"].size))
     prm = T.default_params(win_h=m, win_w=n, pyramid_levels=cfg.pyramid_levels, pyramid_warm=a.pyramid_warm,
@@ -49,6 +50,7 @@ for cid in [int(c) for c in a.configs.split(",")]:
            "pyramid_warm": a.pyramid_warm, "kernel_path": a.kernel_path, "seconds": t,
            "converged_patches_per_s": conv / t, "converged_fraction": conv / B, "inner_iters_per_s": it / t,
            "mean_inner_iters": it / B, "sweeps_per_svt": float(np.sum(rep["jacobi_sweeps"]) / max(it, 1)),
-           "model_tflops": bench.flops_per_launch(rep, m, n, p, int(prm.ns_period)) / t / 1e12}
+           "max_inner_iters_patch": int(np.max(rep["inner_iters"])),
+           "model_tflops": bench.flops_model(rep, m, n, p, int(prm.ns_period)) / t / 1e12}
     print(json.dumps(row), flush=True)
     s.close()
