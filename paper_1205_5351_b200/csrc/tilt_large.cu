@@ -766,7 +766,7 @@ __global__ void __launch_bounds__(ENT) k_svt_scale(Args a) {
 // ns [NCOL] (alpha, d, 1/d, -) of the fast rotations (tilt_jacobi.cuh).
 // ---------------------------------------------------------------------------------------------
 template <int RPL, int CROSS>
-__global__ void __launch_bounds__(RNT, 1) k_round(Args a, int r) {
+__global__ void __launch_bounds__(RNT, RPL <= 8 ? 2 : 1) k_round(Args a, int r) {  // 2 CTAs/SM up to 256 rows
   constexpr int MAXD = 32 * RPL;
   constexpr int NCOL = CROSS ? 2 * BW : BW;
   extern __shared__ float4 sm4[];
@@ -930,31 +930,37 @@ __global__ void __launch_bounds__(RNT, 1) k_round(Args a, int r) {
   }
   for (int e = tid; e < NCOL * NCOL; e += RNT) W[e] *= ns[e / NCOL].y;
   __syncthreads();
-  // V[:, cols] <- V[:, cols] W_eff, one row per thread
-  for (int row = tid; row < L.n; row += RNT) {
-    float v[NCOL];  // the row is in registers, so each output can be stored as soon as it is formed
+  // V[:, cols] <- V[:, cols] W_eff: two threads per row, each forming 16 of the 32 outputs from the
+  // row's inputs in chunks of 8 (at most ~40 live registers, so two 512-thread CTAs fit an SM)
+  constexpr int HALF = NCOL / 2;
+  for (int t = tid; t < 2 * L.n; t += RNT) {
+    const int row = t >> 1, h = t & 1;
+    float o[HALF];
 #pragma unroll
-    for (int c = 0; c < NCOL; ++c) v[c] = cvalid(c) ? V[(size_t)gcol(c) * L.ldn + row] : 0.f;
+    for (int q = 0; q < HALF; ++q) o[q] = 0.f;
 #pragma unroll 1
-    for (int c2 = 0; c2 < NCOL; c2 += 8) {  // 8 outputs at a time: 8 independent FMA chains
-      float o[8];
+    for (int c0 = 0; c0 < NCOL; c0 += 8) {
+      float v[8];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) o[u] = 0.f;
+      for (int u = 0; u < 8; ++u) v[u] = cvalid(c0 + u) ? V[(size_t)gcol(c0 + u) * L.ldn + row] : 0.f;
 #pragma unroll
-      for (int c = 0; c < NCOL; c += 4) {
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const float4 ww = *reinterpret_cast<const float4*>(W + (c2 + u) * NCOL + c);
-          o[u] = fmaf(v[c], ww.x, o[u]);
-          o[u] = fmaf(v[c + 1], ww.y, o[u]);
-          o[u] = fmaf(v[c + 2], ww.z, o[u]);
-          o[u] = fmaf(v[c + 3], ww.w, o[u]);
-        }
+      for (int q = 0; q < HALF; ++q) {
+        const float4 w0 = *reinterpret_cast<const float4*>(W + (h * HALF + q) * NCOL + c0);
+        const float4 w1 = *reinterpret_cast<const float4*>(W + (h * HALF + q) * NCOL + c0 + 4);
+        o[q] = fmaf(v[0], w0.x, o[q]);
+        o[q] = fmaf(v[1], w0.y, o[q]);
+        o[q] = fmaf(v[2], w0.z, o[q]);
+        o[q] = fmaf(v[3], w0.w, o[q]);
+        o[q] = fmaf(v[4], w1.x, o[q]);
+        o[q] = fmaf(v[5], w1.y, o[q]);
+        o[q] = fmaf(v[6], w1.z, o[q]);
+        o[q] = fmaf(v[7], w1.w, o[q]);
       }
-#pragma unroll
-      for (int u = 0; u < 8; ++u)
-        if (cvalid(c2 + u)) V[(size_t)gcol(c2 + u) * L.ldn + row] = o[u];
     }
+    __syncwarp();  // every lane read its inputs before its partner overwrites the shared row
+#pragma unroll
+    for (int q = 0; q < HALF; ++q)
+      if (cvalid(h * HALF + q)) V[(size_t)gcol(h * HALF + q) * L.ldn + row] = o[q];
   }
 }
 
