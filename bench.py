@@ -173,20 +173,42 @@ def cpu_sample(batch: dict, count: int, procs: int) -> dict:
             "patches_per_s": count / dt}
 
 
+def cpp_sample(batch: dict, count: int, threads: int) -> dict:
+    """The C++17 fp64 oracle twin (oracle/tilt_oracle.cpp: its own Jacobi SVD, OpenMP
+    over patches) on the first ``count`` patches of ``batch`` with ``threads`` OpenMP threads."""
+    from oracle import cpp
+    imgs = np.ascontiguousarray(batch["images"][:count], dtype=np.float64)
+    t0 = time.perf_counter()
+    _, _, _, reps = cpp.solve_batch(imgs, np.arange(count, dtype=np.int32), batch["boxes"][:count],
+                                    batch["tau0"][:count].astype(np.float64), ts.HOMOGRAPHY, n_threads=threads)
+    dt = time.perf_counter() - t0
+    conv = sum(1 for r in reps if r["status"] == 0)
+    inner = sum(r["inner_iters"] for r in reps)
+    return {"seconds": dt, "converged": conv, "inner_iters": inner, "threads": threads, "count": count,
+            "patches_per_s": count / dt}
+
+
 def cpu_baseline(batch: dict, cores: int) -> dict:
-    """All host cores (one patch per core) and one thread (2 patches), on the first patches of the
-    bench workload. Reports converged patches/s (the metric) and all-patches/s."""
-    allc = cpu_sample(batch, cores, cores)
-    one = cpu_sample(batch, 2, 1)
+    """the C++ oracle on all host cores (one patch per core) and on one thread (one
+    patch), first patches of the bench workload; CPU model read at run time. For context, the numpy
+    oracle (LAPACK SVD, one process per patch) on the same all-core sample."""
+    allc = cpp_sample(batch, cores, cores)
+    one = cpp_sample(batch, 1, 1)
+    npy = cpu_sample(batch, cores, cores)
     return {"value": allc["converged"] / allc["seconds"], "unit": "patches/s", "cores": cores, "kind": "oracle",
+            "impl": "C++17 fp64 oracle twin (oracle/tilt_oracle.cpp, own Jacobi SVD, OpenMP over patches, "
+                    "-O3 -march=x86-64-v3)",
             "cpu_model": cpu_model(), "inner_iters_per_s": allc["inner_iters"] / allc["seconds"],
             "all_patches_per_s": allc["patches_per_s"],
-            "sample": f"first {cores} patches of config 5 (one process per patch, {cores} cores, "
-                      f"{allc['seconds']:.1f} s)",
+            "sample": f"first {cores} patches of config 5 ({cores} OpenMP threads, {allc['seconds']:.1f} s)",
             "one_thread": {"patches_per_s": one["patches_per_s"],
                            "converged_per_s": one["converged"] / one["seconds"],
                            "inner_iters_per_s": one["inner_iters"] / one["seconds"],
-                           "sample": f"first 2 patches, 1 thread ({one['seconds']:.1f} s)"}}
+                           "sample": f"first patch, 1 thread ({one['seconds']:.1f} s)"},
+            "numpy_oracle": {"converged_per_s": npy["converged"] / npy["seconds"],
+                             "inner_iters_per_s": npy["inner_iters"] / npy["seconds"],
+                             "sample": f"the same {cores} patches, numpy + LAPACK SVD, one process per patch "
+                                       f"({npy['seconds']:.1f} s)"}}
 
 
 def run_reference(args, rank: int) -> None:
@@ -197,9 +219,9 @@ def run_reference(args, rank: int) -> None:
     batch = gen_shard(CFG_ID, range(count))
     vals, inners, secs = [], [], []
     for _ in range(args.warmup if args.ref_warmup else 0):
-        cpu_sample(batch, count, min(cores, count))
+        cpp_sample(batch, count, min(cores, count))
     for _ in range(args.steps):
-        r = cpu_sample(batch, count, min(cores, count))
+        r = cpp_sample(batch, count, min(cores, count))
         vals.append(r["converged"] / r["seconds"])
         inners.append(r["inner_iters"] / r["seconds"])
         secs.append(r["seconds"])
@@ -208,12 +230,13 @@ def run_reference(args, rank: int) -> None:
         "impl": "reference", "metric": METRIC, "value": value, "unit": "patches/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * float(np.mean(secs)),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"config 5 sample: first {count} of 65536 patches 50x50 homography (fp64 oracle)",
+        "config": {"workload": f"config 5 sample: first {count} of 65536 patches 50x50 homography (C++ fp64 oracle)",
                    "global_batch": count, "patch": "50x50", "transform": "homography"},
         "inner_iters_per_s": float(np.mean(inners)),
         "cpu_baseline": {"value": value, "unit": "patches/s", "cores": min(cores, count), "kind": "oracle",
                          "cpu_model": cpu_model(),
-                         "sample": f"first {count} patches of config 5 per step, one process per patch"},
+                         "impl": "C++17 fp64 oracle twin (oracle/tilt_oracle.cpp, OpenMP over patches)",
+                         "sample": f"first {count} patches of config 5 per step, {min(cores, count)} OpenMP threads"},
         "e2e": {"value": value, "unit": "patches/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -514,8 +537,11 @@ def e2e(solvers, batch, slabs, kind, prm, p, m, n) -> dict:
     def hp(a):
         return a.ctypes.data_as(ctypes.c_void_p)
 
-    def run(slab_ids, sv):
-        sv._bind_stream()
+    streams = [torch.cuda.Stream() for _ in solvers]
+
+    def run(slab_ids, sv, stream):
+        with torch.cuda.stream(stream):  # each handle on its own stream: the slabs of the threads overlap
+            sv._bind_stream()
         for s in slab_ids:
             lo, hi = slabs[s]
             check(lib.tilt_solve_batch_host(sv._h, hp(pin["images"][lo:hi]), hi - lo, 2 * m, 2 * n, hp(pimg),
@@ -524,9 +550,10 @@ def e2e(solvers, batch, slabs, kind, prm, p, m, n) -> dict:
                                             hp(rep[lo:hi])), "tilt_solve_batch_host")
 
     nst = len(solvers)
-    run([0], solvers[0])  # warm-up of the host entry (one slab)
+    run([0], solvers[0], streams[0])  # warm-up of the host entry (one slab)
     t0 = time.perf_counter()
-    threads = [threading.Thread(target=run, args=(list(range(j, len(slabs), nst)), solvers[j])) for j in range(nst)]
+    threads = [threading.Thread(target=run, args=(list(range(j, len(slabs), nst)), solvers[j], streams[j]))
+               for j in range(nst)]
     for th in threads:
         th.start()
     for th in threads:

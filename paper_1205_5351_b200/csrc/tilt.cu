@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -473,7 +474,9 @@ tilt_status tilt_create(tilt_handle** out, const tilt_create_opts* o) {
   // sizes still allocate on first use, as tilt.h states)
   {  // L2 residency for the CTA kernels' plane slots (device-wide limit: the largest set-aside)
     int maxp = 0, maxw = 0;
-    if (cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, h->device) == cudaSuccess &&
+    const char* env = getenv("TILT_L2_PERSIST");  // experiment knob: "0" disables the window
+    if ((!env || env[0] != '0') &&
+        cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, h->device) == cudaSuccess &&
         cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, h->device) == cudaSuccess && maxp > 0 &&
         maxw > 0) {
       size_t cur = 0;

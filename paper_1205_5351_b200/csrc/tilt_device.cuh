@@ -72,6 +72,7 @@ struct Scal {
   double dred[16 * 12];
   double dout[12];
   double sd[8];      // K^T v of the last implicit-projector reduce (fp64)
+  float zc[9];       // its apply coefficients L'^T s, c'^T s
   double Lp[64];     // L^{-1} / ||d|| (implicit projector; fp64 so that L'(J_raw^T v) - c'(D_hat^T v)
   double cp[8];      // does not cancel in fp32);  L^{-1} c / ||d||, c = D_hat^T J_raw
   float fred[32 * 10];
@@ -680,37 +681,36 @@ struct ProjImplicit {
     for (int k = 0; k < 9; ++k) a9[k] = a[k];
     double r[9];
     block_sum_fd<C, 9>(a9, r, cx.sc);
-    // s = L' r[0:p] - c' r[8]  (K^T v)
+    // s = L' r[0:p] - c' r[8]  (K^T v), then the apply coefficients z = L'^T s, w = c'^T s: formed
+    // once (threads 0..8) in fp64 and published through shared memory
     const double* Lp = cx.sc->Lp;
     const double* cp = cx.sc->cp;
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
+    if (threadIdx.x < 8) {
+      const int q = threadIdx.x;
       double acc = -cp[q] * r[8];
-#pragma unroll
       for (int b = 0; b <= q; ++b) acc = fma(Lp[q * 8 + b], r[b], acc);
-      s[q] = (float)acc;
-      cx.sc->sd[q] = acc;  // (every thread writes the same value)
+      cx.sc->sd[q] = acc;
     }
+    __syncthreads();
+    if (threadIdx.x < 9) {
+      const int t = threadIdx.x;
+      double acc = 0.0;
+      if (t < 8) {
+        for (int q = t; q < 8; ++q) acc = fma(Lp[q * 8 + t], cx.sc->sd[q], acc);
+      } else {
+        for (int q = 0; q < 8; ++q) acc = fma(cp[q], cx.sc->sd[q], acc);
+      }
+      cx.sc->zc[t] = (float)acc;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 8; ++q) s[q] = (float)cx.sc->sd[q];
   }
-  // coefficients for apply: z = L'^T s (8), w = c'^T s (from the fp64 s of the last reduce)
+  // coefficients for apply (formed by reduce())
   template <class C>
   static __device__ __forceinline__ void coeffs(const Ctx<C>& cx, const float (&s)[8], float (&z)[9]) {
-    const double* Lp = cx.sc->Lp;
-    const double* cp = cx.sc->cp;
-    double sd[8];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) sd[q] = cx.sc->sd[q];
-#pragma unroll
-    for (int b = 0; b < 8; ++b) {
-      double acc = 0.0;
-#pragma unroll
-      for (int q = b; q < 8; ++q) acc = fma(Lp[q * 8 + b], sd[q], acc);
-      z[b] = (float)acc;
-    }
-    double w = 0.0;
-#pragma unroll
-    for (int q = 0; q < 8; ++q) w = fma(cp[q], sd[q], w);
-    z[8] = (float)w;
+    for (int k = 0; k < 9; ++k) z[k] = cx.sc->zc[k];
   }
   // (K y)(pixel) with y the K^T v of reduce(); z from coeffs()
   template <class C>
