@@ -75,8 +75,6 @@ struct tilt_handle {
                      // 3 multi-CTA
   tilt::lp::Ctx lp;  // multi-CTA path for large windows (workspace on first use)
   size_t lp_budget = 0;  // bytes of multi-CTA workspace (batches above it run in chunks)
-  size_t l2_persist = 0;     // persisting-L2 bytes set aside on the device (cudaLimitPersistingL2CacheSize)
-  size_t l2_window_max = 0;  // cudaDevAttrMaxAccessPolicyWindowSize
 };
 
 namespace {
@@ -207,29 +205,7 @@ struct Launch {
     if (s != TILT_OK) return s;
     set_ws(h, a, geo);
     TILT_CUDA(cudaMemsetAsync(a.counter, 0, sizeof(int), h->stream));
-    // the per-CTA plane slots are re-read every LADMAP iteration: ask L2 to keep them resident
-    // (persisting access-policy window over the slots this launch uses; without it ncu counted
-    // ~90 KB of DRAM writes per patch-iteration, the planes cycling through HBM)
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(g);
-    cfg.blockDim = dim3(C::NT);
-    cfg.dynamicSmemBytes = smem(geo);
-    cfg.stream = h->stream;
-    cudaLaunchAttribute attr[1];
-    cfg.numAttrs = 0;
-    const size_t win = a.ws ? (size_t)g * a.ws_stride * sizeof(float) : 0;
-    if (win > 0 && h->l2_persist > 0) {
-      attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
-      attr[0].val.accessPolicyWindow.base_ptr = a.ws;
-      attr[0].val.accessPolicyWindow.num_bytes = win < h->l2_window_max ? win : h->l2_window_max;
-      const double cap = (double)h->l2_persist / (double)attr[0].val.accessPolicyWindow.num_bytes;
-      attr[0].val.accessPolicyWindow.hitRatio = (float)(cap < 1.0 ? cap : 1.0);
-      attr[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-      attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-      cfg.attrs = attr;
-      cfg.numAttrs = 1;
-    }
-    TILT_CUDA(cudaLaunchKernelEx(&cfg, k_solve<C>, a));
+    k_solve<C><<<g, C::NT, smem(geo), h->stream>>>(a);
     h->launches++;
     TILT_CUDA(cudaGetLastError());
     return TILT_OK;
@@ -472,22 +448,6 @@ tilt_status tilt_create(tilt_handle** out, const tilt_create_opts* o) {
   // windows above 128 x 128 take the multi-CTA path by default: its workspace is
   // made here, so the solve entries allocate nothing (SVDWS or a forced kernel_path = 3 at smaller
   // sizes still allocate on first use, as tilt.h states)
-  {  // L2 residency for the CTA kernels' plane slots (device-wide limit: the largest set-aside)
-    int maxp = 0, maxw = 0;
-    const char* env = getenv("TILT_L2_PERSIST");  // experiment knob: "0" disables the window
-    if ((!env || env[0] != '0') &&
-        cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, h->device) == cudaSuccess &&
-        cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, h->device) == cudaSuccess && maxp > 0 &&
-        maxw > 0) {
-      size_t cur = 0;
-      cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
-      if (cur < (size_t)maxp && cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)maxp) != cudaSuccess)
-        cudaGetLastError();
-      cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
-      h->l2_persist = cur;
-      h->l2_window_max = (size_t)maxw;
-    }
-  }
   {
     size_t fr = 0, tot = 0;
     if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) fr = (size_t)8 << 30;
