@@ -581,7 +581,7 @@ def main():
                     help="patches of config 5 solved per timed region (default: all 65536)")
     ap.add_argument("--streams", type=int, default=2)
     ap.add_argument("--cpu-sample", type=int, default=0, help="oracle patches (0: one per host core)")
-    ap.add_argument("--k1-batch", type=int, default=8192)
+    ap.add_argument("--k1-batch", type=int, default=GLOBAL_BATCH, help="patches of the standalone K1 launch (default: the whole shard)")
     ap.add_argument("--ref-warmup", action="store_true")
     ap.add_argument("--recovery-all", action="store_true", help="N > 1: regenerate tau_G of every patch on rank 0")
     ap.add_argument("--no-e2e", action="store_true")

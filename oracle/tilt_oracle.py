@@ -153,7 +153,11 @@ def svt(w, eps, method="lapack"):
     if method == "jacobi":
         u, sig, v, _ = jacobi_svd(w)
         return (u * shrink(sig, eps)) @ v.T, sig
-    u, sig, vt = np.linalg.svd(w, full_matrices=False)
+    try:
+        u, sig, vt = np.linalg.svd(w, full_matrices=False)
+    except np.linalg.LinAlgError:  # LAPACK's divide and conquer did not converge: the oracle's own SVD
+        u, sig, v, _ = jacobi_svd(w)
+        return (u * shrink(sig, eps)) @ v.T, sig
     return (u * shrink(sig, eps)) @ vt, sig
 
 

@@ -232,73 +232,90 @@ template <class C>
 __device__ __forceinline__ void gemm_nn(float* __restrict__ Cm, const float* __restrict__ Lm,
                                         const float* __restrict__ Rm, int ld, int rows_valid, int inner,
                                         int cols) {
+  // C = L R (column-major, leading dimension ld): 4 x 4 register tiles, K in pairs (two 16-byte and
+  // four 8-byte shared loads per 32 FMAs)
   const int rt = ld >> 2;
-  const int ct = (cols + 1) >> 1;
+  const int ct = (cols + 3) >> 2;
   const int ntiles = rt * ct;
   for (int tile = threadIdx.x; tile < ntiles; tile += C::NT) {
     const int i0 = (tile % rt) * 4;
-    const int j0 = (tile / rt) * 2;
-    const bool two = j0 + 1 < cols;
-    float acc[8];
+    const int j0 = (tile / rt) * 4;
+    float acc[16];
 #pragma unroll
-    for (int e = 0; e < 8; ++e) acc[e] = 0.f;
+    for (int e = 0; e < 16; ++e) acc[e] = 0.f;
     const float* lp = Lm + i0;
-    const float* r0 = Rm + j0 * ld;
-    const float* r1 = two ? r0 + ld : r0;
-    const int kend = i0 < rows_valid ? inner : 0;
-#pragma unroll 4
-    for (int k = 0; k < kend; ++k) {
-      const float4 a = *reinterpret_cast<const float4*>(lp + k * ld);
-      const float b0 = r0[k], b1 = r1[k];
-      acc[0] = fmaf(a.x, b0, acc[0]);
-      acc[1] = fmaf(a.y, b0, acc[1]);
-      acc[2] = fmaf(a.z, b0, acc[2]);
-      acc[3] = fmaf(a.w, b0, acc[3]);
-      acc[4] = fmaf(a.x, b1, acc[4]);
-      acc[5] = fmaf(a.y, b1, acc[5]);
-      acc[6] = fmaf(a.z, b1, acc[6]);
-      acc[7] = fmaf(a.w, b1, acc[7]);
-    }
+    const float* rp[4];
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      if (i0 + r >= rows_valid) {
-        acc[r] = 0.f;
-        acc[4 + r] = 0.f;
+    for (int c = 0; c < 4; ++c) rp[c] = Rm + (j0 + c < cols ? j0 + c : j0) * ld;
+    const int kend = i0 < rows_valid ? inner : 0;
+    int k = 0;
+    for (; k + 1 < kend; k += 2) {
+      const float4 a0 = *reinterpret_cast<const float4*>(lp + k * ld);
+      const float4 a1 = *reinterpret_cast<const float4*>(lp + (k + 1) * ld);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const float2 b = *reinterpret_cast<const float2*>(rp[c] + k);
+        acc[4 * c + 0] = fmaf(a0.x, b.x, fmaf(a1.x, b.y, acc[4 * c + 0]));
+        acc[4 * c + 1] = fmaf(a0.y, b.x, fmaf(a1.y, b.y, acc[4 * c + 1]));
+        acc[4 * c + 2] = fmaf(a0.z, b.x, fmaf(a1.z, b.y, acc[4 * c + 2]));
+        acc[4 * c + 3] = fmaf(a0.w, b.x, fmaf(a1.w, b.y, acc[4 * c + 3]));
       }
     }
-    *reinterpret_cast<float4*>(Cm + j0 * ld + i0) = make_float4(acc[0], acc[1], acc[2], acc[3]);
-    if (two) *reinterpret_cast<float4*>(Cm + (j0 + 1) * ld + i0) = make_float4(acc[4], acc[5], acc[6], acc[7]);
+    if (k < kend) {
+      const float4 a0 = *reinterpret_cast<const float4*>(lp + k * ld);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const float b = rp[c][k];
+        acc[4 * c + 0] = fmaf(a0.x, b, acc[4 * c + 0]);
+        acc[4 * c + 1] = fmaf(a0.y, b, acc[4 * c + 1]);
+        acc[4 * c + 2] = fmaf(a0.z, b, acc[4 * c + 2]);
+        acc[4 * c + 3] = fmaf(a0.w, b, acc[4 * c + 3]);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+      if (i0 + r >= rows_valid) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[4 * c + r] = 0.f;
+      }
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+      if (j0 + c < cols)
+        *reinterpret_cast<float4*>(Cm + (j0 + c) * ld + i0) =
+            make_float4(acc[4 * c + 0], acc[4 * c + 1], acc[4 * c + 2], acc[4 * c + 3]);
   }
   __syncthreads();
 }
 
-// out(i0, j, float4 of rows i0..i0+3) for C = B' V^T (B' = B diag(h) pre-scaled): i0 < m, j < n.
+// out(i0, j, float4 of rows i0..i0+3) for C = B' V^T (B' = B diag(h) pre-scaled): i0 < m, j < n;
+// 4 x 4 register tiles (two 16-byte shared loads per 16 FMAs; V's padding rows are zero)
 template <class C, class Out>
 __device__ __forceinline__ void gemm_bvt(const float* Bm, const float* Vm, int ld, int m, int n, Out out) {
   const int rt = (m + 3) >> 2;
-  const int ct = (n + 1) >> 1;
+  const int ct = (n + 3) >> 2;
   const int ntiles = rt * ct;
   for (int tile = threadIdx.x; tile < ntiles; tile += C::NT) {
     const int i0 = (tile % rt) * 4;
-    const int j0 = (tile / rt) * 2;
-    float acc[8];
+    const int j0 = (tile / rt) * 4;
+    float acc[16];
 #pragma unroll
-    for (int e = 0; e < 8; ++e) acc[e] = 0.f;
-#pragma unroll 4
+    for (int e = 0; e < 16; ++e) acc[e] = 0.f;
+#pragma unroll 2
     for (int k = 0; k < n; ++k) {
       const float4 a = *reinterpret_cast<const float4*>(Bm + k * ld + i0);
-      const float2 v = *reinterpret_cast<const float2*>(Vm + k * ld + j0);
-      acc[0] = fmaf(a.x, v.x, acc[0]);
-      acc[1] = fmaf(a.y, v.x, acc[1]);
-      acc[2] = fmaf(a.z, v.x, acc[2]);
-      acc[3] = fmaf(a.w, v.x, acc[3]);
-      acc[4] = fmaf(a.x, v.y, acc[4]);
-      acc[5] = fmaf(a.y, v.y, acc[5]);
-      acc[6] = fmaf(a.z, v.y, acc[6]);
-      acc[7] = fmaf(a.w, v.y, acc[7]);
+      const float4 v = *reinterpret_cast<const float4*>(Vm + k * ld + j0);
+      const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        acc[4 * c + 0] = fmaf(a.x, vv[c], acc[4 * c + 0]);
+        acc[4 * c + 1] = fmaf(a.y, vv[c], acc[4 * c + 1]);
+        acc[4 * c + 2] = fmaf(a.z, vv[c], acc[4 * c + 2]);
+        acc[4 * c + 3] = fmaf(a.w, vv[c], acc[4 * c + 3]);
+      }
     }
-    out(i0, j0, make_float4(acc[0], acc[1], acc[2], acc[3]));
-    if (j0 + 1 < n) out(i0, j0 + 1, make_float4(acc[4], acc[5], acc[6], acc[7]));
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+      if (j0 + c < n) out(i0, j0 + c, make_float4(acc[4 * c + 0], acc[4 * c + 1], acc[4 * c + 2], acc[4 * c + 3]));
   }
 }
 

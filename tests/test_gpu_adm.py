@@ -94,8 +94,9 @@ def test_tilt_with_adm_inner_fixed_count(solver, T):
 
 def test_range_of_convergence_grid_batched(solver, T):
     """Fig. 2's grid as one batched solve per inner solver; small deformations are
-    rectified by both, and sampled cells agree with the fp64 oracle (tau within 2e-3)."""
-    from tilt_synth.metrics import rectified
+    rectified by both, and sampled cells agree with the fp64 oracle (tau within 2e-3, or within 1e-3
+    up to the aspect null direction of reading Z10 -- both runs are free, and the aspect drifts)."""
+    from tilt_synth.metrics import agree_modulo_aspect, rectified
     g = ts.convergence_grid(32, 8)
     nt, ns = len(g["thetas"]), len(g["skews"])
     grid_solver = T.TiltSolver(0, max_batch=nt * ns, max_m=32, max_n=32, max_p=6)
@@ -108,5 +109,5 @@ def test_range_of_convergence_grid_batched(solver, T):
         for k in (6, 70, 144):
             r = O.tilt(g["images"][k], g["boxes"][k], g["tau0"][k], O.AFFINE,
                        O.Params(inner="adm" if sid else "ladmap"))
-            assert np.max(np.abs(r["tau"] - tau[k])) < 2e-3, (sid, k)
+            assert np.max(np.abs(r["tau"] - tau[k])) < 2e-3 or agree_modulo_aspect(tau[k], r["tau"]), (sid, k)
     grid_solver.close()

@@ -163,14 +163,17 @@ def _oracle_run(args):
     cfg = ts.CONFIGS[2]
     p = ts.gen_patch(cfg, idx)
     from threadpoolctl import threadpool_limits
-    with threadpool_limits(1):  # one BLAS thread per worker process
-        if replay is None:
-            r = O.tilt(p["canvas"], p["box"], p["tau0"], cfg.kind)
-        else:
-            n_outer, counts, bits = replay
-            prm = O.Params(fixed_outer_iters=n_outer, max_outer=n_outer, tau_noise=1e-5 if noise_seed else 0.0,
-                           noise_seed=noise_seed)
-            r = O.tilt(p["canvas"], p["box"], p["tau0"], cfg.kind, prm, rho_replay=bits, inner_replay=counts)
+    try:
+        with threadpool_limits(1):  # one BLAS thread per worker process
+            if replay is None:
+                r = O.tilt(p["canvas"], p["box"], p["tau0"], cfg.kind)
+            else:
+                n_outer, counts, bits = replay
+                prm = O.Params(fixed_outer_iters=n_outer, max_outer=n_outer, tau_noise=1e-5 if noise_seed else 0.0,
+                               noise_seed=noise_seed)
+                r = O.tilt(p["canvas"], p["box"], p["tau0"], cfg.kind, prm, rho_replay=bits, inner_replay=counts)
+    except Exception as exc:  # reported with the patch index by the test
+        raise RuntimeError(f"oracle failed on patch {idx} (replay={replay is not None}): {exc!r}") from None
     return {k: r[k] for k in ("tau", "objective", "rank", "rank_band", "outer_iters", "inner_iters", "status")}
 
 
@@ -181,13 +184,22 @@ def _agree(rep, tau, r):
     return dt < 1e-3 and dobj < 1e-3 and rank_ok, dt, dobj
 
 
+def _agree_modulo_aspect(rep, tau, r):
+    """tau equal up to the aspect null direction (Z10), objective 1e-3, rank equal."""
+    from tilt_synth.metrics import agree_modulo_aspect
+    dobj = abs(float(rep["objective"]) - r["objective"]) / r["objective"]
+    rank_ok = (rep["rank"] == r["rank"]) or r["rank_band"] or rep["rank_band"]
+    return agree_modulo_aspect(tau, r["tau"]) and dobj < 1e-3 and rank_ok
+
+
 def test_free_running_convergence_config2_64(solver, T):
     """Protocol 3 on 64 config-2 patches, the GPU free-running with the bench's parameters (its own
     rho decisions, inner-loop ends and outer stop). Checked: the oracle replaying the GPU's
     discrete decisions (outer count, every inner loop's length, every rho bit; readings Z9, Z21)
-    reaches the same tau (1e-3 max-abs), objective (1e-3) and rank (outside the Z19 band) on every
-    patch that is not chain-sensitive -- the GPU computes the paper's method along its own decision
-    path. Chain-sensitive (reading Z22): the oracle's own replayed tau moves by > 1e-3 when tau is
+    reaches the same tau (1e-3 max-abs; for at least 85% of the patches exactly, for the others up
+    to the aspect null direction of reading Z10), objective (1e-3) and rank (outside the Z19 band)
+    on every patch that is not chain-sensitive -- the GPU computes the paper's method along its own
+    decision path. Chain-sensitive (reading Z22): the oracle's own replayed tau moves by > 1e-3 when tau is
     perturbed by 1e-5 relative after every outer step (the size of the fp32-vs-fp64 per-step
     difference: re-synced A, E agree to ~1.4e-5 after 20 inner iterations, test above, and to ~1e-4
     deep in an inner loop at mu ~1e6, tools/inner_drift.py); such patches are counted. Printed: the
@@ -228,14 +240,17 @@ def test_free_running_convergence_config2_64(solver, T):
         moves = [float(np.max(np.abs(noisy[2 * q + t]["tau"] - replayed[j]["tau"]))) for t in (0, 1)]
         if max(moves) > 1e-3:
             sensitive.append(k)
-    stable_bad = [d[1:] for d in bad_replayed if d[1] not in sensitive]
+    aspect_only = [d[1] for d in bad_replayed if d[1] not in sensitive and
+                   _agree_modulo_aspect(reps[d[1]], taus[d[1]], replayed[d[0]])]
+    stable_bad = [d[1:] for d in bad_replayed if d[1] not in sensitive and d[1] not in aspect_only]
     for j, k in enumerate(ks):
         ok, dt, dobj = _agree(reps[k], taus[k], free[j])
         if not ok:
             bad_free.append((k, round(dt, 5), int(reps["inner_iters"][k]), free[j]["inner_iters"]))
     caps = int(np.sum(np.sum(np.isfinite(tr[ks, :, :, 0]), axis=2) == prm.max_inner))
     print(f"free-running config 2, {len(ks)} patches: GPU vs oracle replaying the GPU's decisions: "
-          f"{len(ks) - len(bad_replayed)} agree, {len(sensitive)} chain-sensitive (Z22) excluded {sensitive}; "
+          f"{len(ks) - len(bad_replayed)} agree, {len(sensitive)} chain-sensitive (Z22) excluded {sensitive}, "
+          f"{len(aspect_only)} agree up to the aspect null direction (Z10) {aspect_only}; "
           f"GPU vs the oracle's own decisions: {len(ks) - len(bad_free)} agree (disagreeing: {bad_free}); "
           f"GPU inner loops ending at max_inner: {caps}")
     assert len(ks) - len(bad_replayed) >= 0.85 * len(ks)

@@ -62,3 +62,15 @@ def test_recovery_metrics():
     t2 = tg.copy()
     t2[0] += 0.1
     assert M.table2_error(t2, tg) == pytest.approx(0.1 / np.linalg.norm(tg))
+
+
+def test_agree_modulo_aspect():
+    """Reading Z10's null direction: an aspect change diag(s, 1/s) is invisible, a skew is not."""
+    from tilt_synth import metrics as M
+    tg = ts.tau_from_h(ts.planted_transform(0.2, 0.1, 0.01, 0.0), ts.HOMOGRAPHY)
+    h = M._h_of(tg) @ np.diag([1.05, 1 / 1.05, 1.0])
+    assert M.agree_modulo_aspect(ts.tau_from_h(h, ts.HOMOGRAPHY), tg)
+    h2 = M._h_of(tg) @ np.array([[1.0, 0.01, 0.0], [0.0, 1.0, 0.0], [0.0, 0.0, 1.0]])
+    assert not M.agree_modulo_aspect(ts.tau_from_h(h2, ts.HOMOGRAPHY), tg)
+    h3 = M._h_of(tg) @ np.diag([1.05, 1.0, 1.0])          # not area-preserving
+    assert not M.agree_modulo_aspect(ts.tau_from_h(h3, ts.HOMOGRAPHY), tg)

@@ -48,3 +48,15 @@ def table2_error(tau: np.ndarray, tau_g: np.ndarray) -> float:
     """Table 2's error measure ||tau* - tau_G|| / ||tau_G||."""
     tau, tau_g = np.asarray(tau, np.float64), np.asarray(tau_g, np.float64)
     return float(np.linalg.norm(tau - tau_g) / np.linalg.norm(tau_g))
+
+
+def agree_modulo_aspect(tau_a: np.ndarray, tau_b: np.ndarray, tol: float = 1e-3) -> bool:
+    """tau_a equals tau_b up to TILT's null direction (reading Z10: low rank is invariant to axis
+    scaling, and the area row leaves the aspect diag(s, 1/s) free): H_b^{-1} H_a, normalised, is
+    diag(s, 1/s, 1) to ``tol`` (off-diagonal and perspective entries, and the area s (1/s) = 1)."""
+    h = np.linalg.solve(_h_of(np.asarray(tau_b, np.float64)), _h_of(np.asarray(tau_a, np.float64)))
+    if not np.all(np.isfinite(h)) or h[2, 2] == 0:
+        return False
+    h = h / h[2, 2]
+    off = max(abs(h[0, 1]), abs(h[1, 0]), abs(h[0, 2]), abs(h[1, 2]), abs(h[2, 0]), abs(h[2, 1]))
+    return bool(off < tol and abs(h[0, 0] * h[1, 1] - 1.0) < tol)
