@@ -23,6 +23,21 @@
 // rows [4(lu + qL), 4(lu + qL) + 4) (interleaved, so the 8 lanes of a shared-memory phase touch 128
 // consecutive bytes: conflict-free); a chunk exists iff its first row is < ld (ld % 4 == 0).
 // Addresses passed in point at the lane's first chunk (column base + 4 lu floats).
+// Packed FP32x2 (sm_100: one FFMA2 issues two FMAs; the scalar operand broadcast as {s, s})
+__device__ __forceinline__ unsigned long long pk2(float a, float b) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void up2(unsigned long long x, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(x));
+}
+__device__ __forceinline__ unsigned long long fma2(unsigned long long a, unsigned long long b, unsigned long long c) {
+  unsigned long long d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+
 template <int RPL, int L>
 struct Col {
   static_assert(RPL % 4 == 0, "float4 chunks");
@@ -76,13 +91,22 @@ struct Col {
           : "memory");
   }
   __device__ __forceinline__ float dot(const Col& o) const {
-    float a = 0.f, b = 0.f;  // two chains
+    unsigned long long acc = 0ull;  // two chains, one FFMA2 per row pair
+#pragma unroll
+    for (int e = 0; e < RPL; e += 2) acc = fma2(pk2(v[e], v[e + 1]), pk2(o.v[e], o.v[e + 1]), acc);
+    float a, b;
+    up2(acc, a, b);
+    return a + b;
+  }
+  // the fast rotation of a column pair (x, y) <- (x - ca y, y + cb x), one FFMA2 per row pair
+  static __device__ __forceinline__ void rotate(Col& x, Col& y, float ca, float cb) {
+    const unsigned long long mca = pk2(-ca, -ca), pcb = pk2(cb, cb);
 #pragma unroll
     for (int e = 0; e < RPL; e += 2) {
-      a = fmaf(v[e], o.v[e], a);
-      b = fmaf(v[e + 1], o.v[e + 1], b);
+      const unsigned long long x2 = pk2(x.v[e], x.v[e + 1]), y2 = pk2(y.v[e], y.v[e + 1]);
+      up2(fma2(y2, mca, x2), x.v[e], x.v[e + 1]);
+      up2(fma2(x2, pcb, y2), y.v[e], y.v[e + 1]);
     }
-    return a + b;
   }
   __device__ __forceinline__ float sq() const { return dot(*this); }
   __device__ __forceinline__ void scale(float s) {
@@ -270,23 +294,13 @@ __device__ int jacobi_sweeps(Ctx<C>& cx, float tol, int max_sweeps, bool* capped
         const bool doit = valid && ni.x > 0.f && nj.x > 0.f && gam * gam > tol2 * ab;
         if (__any_sync(FULL, doit)) {
           const Rot rp = rot_params(ni, nj, gam, doit);
-#pragma unroll
-          for (int e = 0; e < RPL; ++e) {
-            const float o = xi.v[e];
-            xi.v[e] = fmaf(-rp.ca, xj.v[e], o);
-            xj.v[e] = fmaf(rp.cb, o, xj.v[e]);
-          }
+          Col<RPL, L>::rotate(xi, xj, rp.ca, rp.cb);
           float* vi = Vm + i * ld + 4 * lu;
           float* vj = Vm + j * ld + 4 * lu;
           Col<RPL, L> yi, yj;
           yi.gload(vi, doit ? cm : 0u);
           yj.gload(vj, doit ? cm : 0u);
-#pragma unroll
-          for (int e = 0; e < RPL; ++e) {
-            const float o = yi.v[e];
-            yi.v[e] = fmaf(-rp.ca, yj.v[e], o);
-            yj.v[e] = fmaf(rp.cb, o, yj.v[e]);
-          }
+          Col<RPL, L>::rotate(yi, yj, rp.ca, rp.cb);
           if (doit) {
             xi.gstore(bi, cm);
             xj.gstore(bj, cm);
@@ -361,24 +375,14 @@ __device__ __noinline__ int jacobi_sweeps_smem(float* Bp, float* Vp, float4* nsp
         const Rot rp = rot_params(ni, nj, gam, doit);
         const uint32_t vi = sV + ii * colb + lane_off, vj = sV + jj * colb + lane_off;
         const uint32_t cmr = doit ? cm : 0u;
-#pragma unroll
-        for (int e = 0; e < RPL; ++e) {
-          const float o = xi.v[e];
-          xi.v[e] = fmaf(-rp.ca, xj.v[e], o);
-          xj.v[e] = fmaf(rp.cb, o, xj.v[e]);
-        }
+        Col<RPL, L>::rotate(xi, xj, rp.ca, rp.cb);
         xi.sstore(ai, cmr);
         xj.sstore(aj, cmr);
         // V columns after B's are stored: only two columns live in registers at a time
         Col<RPL, L> yi, yj;
         yi.sload(vi, cmr);  // only units that rotate read (and write) their V columns
         yj.sload(vj, cmr);
-#pragma unroll
-        for (int e = 0; e < RPL; ++e) {
-          const float o = yi.v[e];
-          yi.v[e] = fmaf(-rp.ca, yj.v[e], o);
-          yj.v[e] = fmaf(rp.cb, o, yj.v[e]);
-        }
+        Col<RPL, L>::rotate(yi, yj, rp.ca, rp.cb);
         yi.sstore(vi, cmr);
         yj.sstore(vj, cmr);
         const float sx = rp.c * fmaf(rp.t, rp.t, 1.f);  // sqrt(1 + t^2)

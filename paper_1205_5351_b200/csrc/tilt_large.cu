@@ -829,12 +829,7 @@ __global__ void __launch_bounds__(RNT, RPL <= 8 ? 2 : 1) k_round(Args a, int r) 
     const bool doit = ni.x > amin && nj.x > amin && gam * gam > tol2 * ab;
     if (doit) {  // warp-uniform
       const Rot rp = rot_params(ni, nj, gam, true);
-#pragma unroll
-      for (int e = 0; e < RPL; ++e) {
-        const float o = xi.v[e];
-        xi.v[e] = fmaf(-rp.ca, xj.v[e], o);
-        xj.v[e] = fmaf(rp.cb, o, xj.v[e]);
-      }
+      CL::rotate(xi, xj, rp.ca, rp.cb);
       const float w0 = wi;
       wi = fmaf(-rp.ca, wj, w0);
       wj = fmaf(rp.cb, w0, wj);
