@@ -518,7 +518,8 @@ __device__ __forceinline__ WarpTap warp_tap(const WarpGeom& g, int H, int W, int
   const double du = j - 0.5 * (g.n - 1);
   const double dv = i - 0.5 * (g.m - 1);
   const double w = 1.0 + (g.h31 * du + g.h32 * dv) * g.inv_s;
-  const double iw = g.kind == TILT_HOMOGRAPHY ? 1.0 / w : 1.0;  // the one fp64 division per pixel
+  const bool persp = g.kind == TILT_HOMOGRAPHY && (g.h31 != 0.0 || g.h32 != 0.0);
+  const double iw = persp ? 1.0 / w : 1.0;  // the one fp64 division per pixel (w = 1 exactly otherwise)
   const double X = g.cx + (g.h11 * du + g.h12 * dv + g.s * g.h13) * iw;
   const double Y = g.cy + (g.h21 * du + g.h22 * dv + g.s * g.h23) * iw;
   const double X0 = floor(X), Y0 = floor(Y);

@@ -364,8 +364,13 @@ __device__ __noinline__ int jacobi_sweeps_smem(float* Bp, float* Vp, float4* nsp
       const int ii = valid ? i : 0, jj = valid ? j : 0;
       const uint32_t ai = sB + ii * colb + lane_off, aj = sB + jj * colb + lane_off;
       Col<RPL, L> xi, xj;
-      xi.sload_full(ai);
-      xj.sload_full(aj);
+      if (unit_on) {  // units beyond n/2 pairs (a whole quarter-warp or warp) issue no loads
+        xi.sload_full(ai);
+        xj.sload_full(aj);
+      } else {
+#pragma unroll
+        for (int e = 0; e < RPL; ++e) xi.v[e] = xj.v[e] = 0.f;
+      }
       const float4 ni = lds4(sNS + 16 * ii), nj = lds4(sNS + 16 * jj);  // (alpha, d, 1/d, -)
       const float g = unit_sum<L>(xi.dot(xj));
       const float gam = g * ni.y * nj.y;
