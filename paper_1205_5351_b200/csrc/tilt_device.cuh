@@ -467,6 +467,7 @@ __device__ SvtOut svt(Ctx<C>& cx, const float* X, float eps, float tol, int max_
 struct WarpGeom {
   double s, inv_s, cx, cy, h11, h12, h13, h21, h22, h23, h31, h32;
   int m, n, p, kind;
+  bool persp;  // homography with h31 or h32 nonzero (w != 1)
 };
 
 __device__ __forceinline__ WarpGeom make_geom(const int* box, const double* tau, int kind) {
@@ -483,6 +484,7 @@ __device__ __forceinline__ WarpGeom make_geom(const int* box, const double* tau,
   g.h32 = kind == TILT_HOMOGRAPHY ? tau[7] : 0.0;
   g.kind = kind;
   g.p = kind == TILT_HOMOGRAPHY ? 8 : 6;
+  g.persp = g.h31 != 0.0 || g.h32 != 0.0;
   return g;
 }
 
@@ -513,15 +515,26 @@ struct WarpTap {
   bool ok;                    // the 4-tap stencil lies inside the image
 };
 
-// fp64 geometry of window pixel (i, j): source coordinate (Z15, Z16), cell by floor, escape test (Z2)
-__device__ __forceinline__ WarpTap warp_tap(const WarpGeom& g, int H, int W, int i, int j) {
+// fp64 source coordinate (X, Y) of window pixel (i, j) (Z15, Z16); iw = 1 / w
+__device__ __forceinline__ void warp_xy(const WarpGeom& g, int i, int j, double& X, double& Y, double& iw) {
   const double du = j - 0.5 * (g.n - 1);
   const double dv = i - 0.5 * (g.m - 1);
-  const double w = 1.0 + (g.h31 * du + g.h32 * dv) * g.inv_s;
-  const bool persp = g.kind == TILT_HOMOGRAPHY && (g.h31 != 0.0 || g.h32 != 0.0);
-  const double iw = persp ? 1.0 / w : 1.0;  // the one fp64 division per pixel (w = 1 exactly otherwise)
-  const double X = g.cx + (g.h11 * du + g.h12 * dv + g.s * g.h13) * iw;
-  const double Y = g.cy + (g.h21 * du + g.h22 * dv + g.s * g.h23) * iw;
+  // 1 / w: fp32 reciprocal refined by one fp64 Newton step, relative error ~(2^-23)^2 (the fp64
+  // division's multi-instruction sequence was ~5% of K1's instructions); w = 1 exactly when affine
+  iw = 1.0;
+  if (g.persp) {
+    const double w = 1.0 + (g.h31 * du + g.h32 * dv) * g.inv_s;
+    const double r = (double)__frcp_rn((float)w);
+    iw = r * fma(-w, r, 2.0);
+  }
+  X = g.cx + (g.h11 * du + g.h12 * dv + g.s * g.h13) * iw;
+  Y = g.cy + (g.h21 * du + g.h22 * dv + g.s * g.h23) * iw;
+}
+
+// fp64 geometry of window pixel (i, j): source coordinate, cell by floor, escape test (Z2)
+__device__ __forceinline__ WarpTap warp_tap(const WarpGeom& g, int H, int W, int i, int j) {
+  double X, Y, iw;
+  warp_xy(g, i, j, X, Y, iw);
   const double X0 = floor(X), Y0 = floor(Y);
   WarpTap t;
   t.ok = X0 >= 0.0 && X0 + 1.0 <= W - 1 && Y0 >= 0.0 && Y0 + 1.0 <= H - 1;
