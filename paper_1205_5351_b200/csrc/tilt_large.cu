@@ -788,8 +788,11 @@ __global__ void __launch_bounds__(RNT, RPL <= 8 ? 2 : 1) k_round(Args a, int r) 
     I = blockIdx.x;
   }
   const int nI = min(BW, L.n - I * BW), nJ = CROSS ? min(BW, L.n - J * BW) : 0;
-  auto gcol = [&](int c) { return c < BW ? I * BW + c : J * BW + (c - BW); };
-  auto cvalid = [&](int c) { return c < BW ? c < nI : (c - BW) < nJ; };
+  // valid local columns as a bit mask; global column of local c: c + (c < BW ? gI : gJ)
+  const uint32_t vmask = ((1u << nI) - 1u) | (CROSS ? ((1u << nJ) - 1u) << BW : 0u);
+  const int gI = I * BW, gJ = J * BW - BW;
+  auto gcol = [&](int c) { return c + (c < BW ? gI : gJ); };
+  auto cvalid = [&](int c) { return ((vmask >> c) & 1u) != 0u; };
   float* w = slot(a, b);
   float* Bm = w + L.oB;
   float* V = w + a.oV;
@@ -853,7 +856,7 @@ __global__ void __launch_bounds__(RNT, RPL <= 8 ? 2 : 1) k_round(Args a, int r) 
     float4 ni = ns[i];
     float wi = W[i * NCOL + lane];
     for (int s = 0; s < BW; ++s) {
-      const int j = BW + (warp + s) % BW;
+      const int j = BW + ((warp + s) & (BW - 1));
       if (vi && cvalid(j)) {  // warp-uniform
         const uint32_t aj = sX + j * MAXD * 4 + lane * 16;
         CL xj;
@@ -925,19 +928,24 @@ __global__ void __launch_bounds__(RNT, RPL <= 8 ? 2 : 1) k_round(Args a, int r) 
   }
   for (int e = tid; e < NCOL * NCOL; e += RNT) W[e] *= ns[e / NCOL].y;
   __syncthreads();
-  // V[:, cols] <- V[:, cols] W_eff: two threads per row, each forming 16 of the 32 outputs from the
-  // row's inputs in chunks of 8 (at most ~40 live registers, so two 512-thread CTAs fit an SM)
+  // V[:, cols] <- V[:, cols] W_eff: two threads per row, each forming HALF of the NCOL outputs from
+  // the row's inputs in chunks of 8 (at most ~40 live registers, so two 512-thread CTAs fit an SM).
+  // Thread tid: row r0 + tid % (RNT / 2), half tid / (RNT / 2), so a warp reads one W row at a time
+  // (a broadcast, no bank conflict between the halves); both halves of a row are in the same pass and
+  // all inputs are read before the CTA barrier, then written.
   constexpr int HALF = NCOL / 2;
-  for (int t = tid; t < 2 * L.n; t += RNT) {
-    const int row = t >> 1, h = t & 1;
+  for (int r0 = 0; r0 < L.n; r0 += RNT / 2) {
+    const int h = tid / (RNT / 2), row = r0 + (tid & (RNT / 2 - 1));
+    const bool on = row < L.n;
     float o[HALF];
 #pragma unroll
     for (int q = 0; q < HALF; ++q) o[q] = 0.f;
 #pragma unroll 1
     for (int c0 = 0; c0 < NCOL; c0 += 8) {
+      const float* vc = V + (size_t)(c0 + (c0 < BW ? gI : gJ)) * L.ldn + row;
       float v[8];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) v[u] = cvalid(c0 + u) ? V[(size_t)gcol(c0 + u) * L.ldn + row] : 0.f;
+      for (int u = 0; u < 8; ++u) v[u] = (on && cvalid(c0 + u)) ? vc[(size_t)u * L.ldn] : 0.f;
 #pragma unroll
       for (int q = 0; q < HALF; ++q) {
         const float4 w0 = *reinterpret_cast<const float4*>(W + (h * HALF + q) * NCOL + c0);
@@ -952,10 +960,13 @@ __global__ void __launch_bounds__(RNT, RPL <= 8 ? 2 : 1) k_round(Args a, int r) 
         o[q] = fmaf(v[7], w1.w, o[q]);
       }
     }
-    __syncwarp();  // every lane read its inputs before its partner overwrites the shared row
+    __syncthreads();  // every thread read its inputs before the other half of its row is overwritten
+    if (on) {
+      float* vo = V + (size_t)(h * HALF + (h * HALF < BW ? gI : gJ)) * L.ldn + row;
 #pragma unroll
-    for (int q = 0; q < HALF; ++q)
-      if (cvalid(h * HALF + q)) V[(size_t)gcol(h * HALF + q) * L.ldn + row] = o[q];
+      for (int q = 0; q < HALF; ++q)
+        if (cvalid(h * HALF + q)) vo[(size_t)q * L.ldn] = o[q];
+    }
   }
 }
 
