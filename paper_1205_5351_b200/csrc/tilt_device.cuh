@@ -86,6 +86,8 @@ struct Scal {
   int flag;
   int patch;
   int rot_acc;       // Jacobi rotations of the current SVT
+  int nk;            // columns with h_j > 0 in the last SVT ...
+  short kidx[256];   // ... and their indices, ascending (the terms of A = sum_j h_j b_j v_j^T)
 };
 
 // --------------------------------------------------------------------------------------------
@@ -289,8 +291,11 @@ __device__ __forceinline__ void gemm_nn(float* __restrict__ Cm, const float* __r
 
 // out(i0, j, float4 of rows i0..i0+3) for C = B' V^T (B' = B diag(h) pre-scaled): i0 < m, j < n;
 // 4 x 4 register tiles (two 16-byte shared loads per 16 FMAs; V's padding rows are zero)
+// A = B V^T over the nk columns listed in kidx (the SVT's columns with h_j > 0; the others are
+// exactly zero after col_scale and are skipped: the sum keeps the ascending order of the full one)
 template <class C, class Out>
-__device__ __forceinline__ void gemm_bvt(const float* Bm, const float* Vm, int ld, int m, int n, Out out) {
+__device__ __forceinline__ void gemm_bvt(const float* Bm, const float* Vm, int ld, int m, int n, Out out,
+                                         const short* kidx, int nk) {
   const int rt = (m + 3) >> 2;
   const int ct = (n + 3) >> 2;
   const int ntiles = rt * ct;
@@ -301,7 +306,8 @@ __device__ __forceinline__ void gemm_bvt(const float* Bm, const float* Vm, int l
 #pragma unroll
     for (int e = 0; e < 16; ++e) acc[e] = 0.f;
 #pragma unroll 2
-    for (int k = 0; k < n; ++k) {
+    for (int t = 0; t < nk; ++t) {
+      const int k = kidx[t];
       const float4 a = *reinterpret_cast<const float4*>(Bm + k * ld + i0);
       const float4 v = *reinterpret_cast<const float4*>(Vm + k * ld + j0);
       const float vv[4] = {v.x, v.y, v.z, v.w};
@@ -353,6 +359,17 @@ __device__ __forceinline__ void col_scale(Ctx<C>& cx) {
     b.z *= f;
     b.w *= f;
     *bp = b;
+  }
+  if (threadIdx.x < 32) {  // the columns with h_j > 0, compacted in ascending order
+    int base = 0;
+    for (int jb = 0; jb < n; jb += 32) {
+      const int j = jb + threadIdx.x;
+      const bool on = j < n && cx.hv[j] > 0.f;
+      const unsigned msk = __ballot_sync(FULL, on);
+      if (on) cx.sc->kidx[base + __popc(msk & ((1u << threadIdx.x) - 1u))] = (short)j;
+      base += __popc(msk);
+    }
+    if (threadIdx.x == 0) cx.sc->nk = base;
   }
   __syncthreads();
 }
@@ -453,7 +470,7 @@ __device__ SvtOut svt(Ctx<C>& cx, const float* X, float eps, float tol, int max_
   svt_stats<C>(cx, eps);
   if constexpr (DO_OUT) {
     col_scale<C>(cx);
-    gemm_bvt<C>(cx.B, cx.V, cx.lds, cx.m, cx.n, out);  // A = B diag(h) V^T
+    gemm_bvt<C>(cx.B, cx.V, cx.lds, cx.m, cx.n, out, cx.sc->kidx, cx.sc->nk);  // A = B diag(h) V^T
   }
   __syncthreads();
   if (ns_after) ns_step<C>(cx);
