@@ -59,6 +59,34 @@ def test_warp_jacobian_parity(solver, kind):
             assert err < 1e-5, (k, q, err)
 
 
+@pytest.mark.parametrize("hw", [(45, 47), (50, 51)])
+def test_warp_jacobian_parity_ragged_window(solver, hw):
+    """K1's scalar store path (m n not a multiple of 4: the 16-byte plane stores need m n % 4 == 0)
+    and odd window sizes, homography with perspective terms (the fp32-reciprocal + Newton 1/w)."""
+    cfg = ts.CONFIGS[2]
+    kind, p = O.HOMOGRAPHY, 8
+    b = ts.gen_batch(cfg, 0, 4)
+    m, n = hw
+    boxes = b["boxes"].copy()
+    boxes[:, 2], boxes[:, 3] = n, m
+    rng = np.random.default_rng(11)
+    taus = np.tile(ts.identity_tau(kind), (4, 1))
+    taus[:, :6] += rng.uniform(-0.05, 0.05, size=(4, 6))
+    taus[:, 6:] = rng.uniform(-0.03, 0.03, size=(4, 2))
+    taus = taus.astype(np.float32)
+    out = solver.warp(b["images"], b["patch_image"], boxes, taus, kind)
+    dh = out["Dhat"].double().cpu().numpy().reshape(4, m, n)
+    J = out["J"].double().cpu().numpy().reshape(4, p, m, n)
+    for k in range(4):
+        d, jraw, st = O.warp(b["images"][k], boxes[k], taus[k].astype(np.float64), kind)
+        assert st == O.CONVERGED and int(out["status"][k]) == O.CONVERGED
+        rdh, rj, nd = O.normalise(d, jraw)
+        assert abs(float(out["norm"][k]) - nd) <= 1e-6 * nd
+        np.testing.assert_allclose(dh[k], rdh, atol=2e-6 * np.abs(rdh).max())
+        for q in range(p):
+            assert np.linalg.norm(J[k, q] - rj[q]) < 1e-5 * np.linalg.norm(rj[q]), (k, q)
+
+
 def test_warp_full_batch_sampled(T):
     """K1 at the bench's full size and launch configuration (config 2: 1024 patches at tau0, the
     roofline_k1 call of bench.py), sampled patches against the oracle's warp."""
