@@ -44,7 +44,13 @@ struct Cfg {
 // (L2-resident, touched only by the elementwise passes); B, V, S (31 KB) stay in shared memory, so
 // 4 independent patches share an SM and hide each other's per-round barrier and shuffle latency.
 using CfgS32 = Cfg<8, 4, 8, true, true, 4>;
-using CfgS64 = Cfg<8, 8, 8, false, true, 4>;
+#ifndef TILT_S64_L  // experiment hooks (tools/build_variant.sh); the defaults are the product
+#define TILT_S64_L 8
+#define TILT_S64_RPL 8
+#define TILT_S64_NW 8
+#define TILT_S64_MINB 4
+#endif
+using CfgS64 = Cfg<TILT_S64_L, TILT_S64_RPL, TILT_S64_NW, false, true, TILT_S64_MINB>;
 using CfgS128 = Cfg<16, 8, 32, false, true, 1>;
 // S256: B (256 x n floats, 205 KB at n = 200) in shared memory; V and S in the L2-resident slot
 using CfgS256 = Cfg<32, 8, 32, false, false, 1, true>;

@@ -854,8 +854,13 @@ struct WarpArgs {
   int* status;
 };
 
-constexpr int K1_NT = 256;
-constexpr int K1_ILP = 2;
+#ifndef TILT_K1_NT  // experiment hooks (tools/build_variant.sh); the defaults are the product
+#define TILT_K1_NT 128
+#define TILT_K1_ILP 5
+#define TILT_K1_MINB 4
+#endif
+constexpr int K1_NT = TILT_K1_NT;
+constexpr int K1_ILP = TILT_K1_ILP;
 
 // One CTA per patch, two passes over its pixels:
 //   1. geometry (fp64, warp_tap), the 4 taps, the fp32 interpolant (warp_interp) -> shared memory
@@ -864,11 +869,14 @@ constexpr int K1_ILP = 2;
 //      J_raw / ||D||), written four consecutive pixels per thread as 16-byte stores (one for D_hat,
 //      p for J) when m n % 4 == 0.
 // The patch geometry is built once per CTA (thread 0) and broadcast through shared memory.
-// Measured variants: ILP 2 at 80 registers and 3 CTAs/SM is the fastest; ILP 4,
-// 4 CTAs/SM at 64 registers (spills), the window footprint staged in shared memory by cp.async,
-// a persistent grid and a two-kernel split (reductions, then a streaming output pass that redoes
-// the warp) were each slower or no faster.
-__global__ void __launch_bounds__(K1_NT, 3) k_warp(WarpArgs a) {
+// Measured variants (tools/build_variant.sh): pass 1 is bound by the latency of the
+// tap gathers, so what counts is gathers in flight per SM. 128 threads x ILP 5 (~20 pixels per
+// thread in 4 waves of 20 loads) at 128 registers and 4 CTAs/SM (164 KB of shared memory) is the
+// fastest: 0.646 of HBM at 65 536 patches, vs 0.539 for 256 threads x ILP 2 at 3 CTAs/SM; 256 x
+// ILP 3-5 at 2 CTAs/SM, 512 x ILP 5 at 1 CTA/SM, 128 x ILP 3-8 at 3-5 CTAs/SM, the window
+// footprint staged in shared memory by cp.async, a persistent grid and a two-kernel split
+// (reductions, then a streaming output pass that redoes the warp) were each slower.
+__global__ void __launch_bounds__(K1_NT, TILT_K1_MINB) k_warp(WarpArgs a) {
   extern __shared__ float4 k1s[];  // per pixel (d, gx, gy, gz)
   __shared__ double red[K1_NT / 32][9];
   __shared__ double tot[9];
