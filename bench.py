@@ -384,10 +384,11 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     value = conv_all / elapsed
     achieved = fl_model_all / elapsed / 1e12
     achieved_rot = fl_rot_all / elapsed / 1e12
-    traffic = None
+    traffic = traffic_note = None
     try:
         prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))
         traffic = prof.get("k_solve_dram_bytes_per_launch")
+        traffic_note = prof.get("k_solve_traffic_note")
     except Exception:
         pass
     binding = None
@@ -423,6 +424,7 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
                        zip(*np.unique(rep_all["stop_rule"], return_counts=True))},
         "roofline": {"bound": "alu", "kernel": "k_solve", "achieved": achieved, "peak": FP32_PEAK_TFLOPS,
                      "unit": "TFLOP/s", "frac": achieved / FP32_PEAK_TFLOPS, "traffic": traffic,
+                     "traffic_note": traffic_note,
                      "peak_note": "FP32 FMA: 148 SMs x 128 lanes x 2 x 1.965 GHz (sm_max_mhz of "
                                   "MEASURED_PEAKS.json; DESIGN.md §4)",
                      "achieved_note": "SURVEY §8(d) model flops from the device counters of all launches / "
@@ -503,13 +505,16 @@ def k1_roofline(solver, images, patch_image, boxes, tau0, kind, m, n, p, peaks) 
     byts = B * 4.0 * ((m + 1) * (n + 1) + m * n * (1 + p))
     achieved = byts / t / 1e9
     peak = float(peaks.get("hbm_gbs", 6536.4))
-    traffic = None
+    traffic = traffic_note = None
     try:
-        traffic = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json"))).get("k_warp_dram_bytes_per_launch")
+        prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))
+        traffic = prof.get("k_warp_dram_bytes_per_launch")
+        traffic_note = prof.get("k_warp_traffic_note")
     except Exception:
         pass
     return {"bound": "hbm", "kernel": "k_warp", "achieved": achieved, "peak": peak, "unit": "GB/s",
-            "frac": achieved / peak, "traffic": traffic, "bytes_per_launch": byts, "us_per_launch": 1e6 * t,
+            "frac": achieved / peak, "traffic": traffic, "traffic_note": traffic_note, "bytes_per_launch": byts,
+            "us_per_launch": 1e6 * t,
             "patches": B,
             "note": f"standalone K1 over the first {B} patches of the bench workload at tau0; L2 flushed before "
                     f"each timed launch (median of {reps})"}
