@@ -1603,6 +1603,9 @@ __global__ void k_report_solve(Args a, tilt_report* rep, float* tau_out, const t
 // ---------------------------------------------------------------------------------------------
 // Host side
 // ---------------------------------------------------------------------------------------------
+template <int RPL>
+constexpr int RPL_TAG = RPL;
+
 struct Run {
   Ctx& ctx;
   Args a;
@@ -1716,16 +1719,52 @@ struct Run {
                                        (int)sm_intra),
                   "cudaFuncSetAttribute(k_round)"))
       return true;
-    for (int sw = 0; sw < a.max_sweeps; ++sw) {
-      k_round<RPL, 0><<<dim3(a.NB, a.B), RNT, sm_intra, ctx.stream>>>(a, 0);
-      launched();
-      for (int r = 0; r < a.NBp - 1; ++r) {
-        k_round<RPL, 1><<<dim3(a.NBp / 2, a.B), RNT, sm_cross, ctx.stream>>>(a, r);
-        launched();
+    auto enqueue = [&](cudaStream_t sm) {  // one sweep: intra round, NBp - 1 cross rounds, reset, end
+      k_round<RPL, 0><<<dim3(a.NB, a.B), RNT, sm_intra, sm>>>(a, 0);
+      for (int r = 0; r < a.NBp - 1; ++r)
+        k_round<RPL, 1><<<dim3(a.NBp / 2, a.B), RNT, sm_cross, sm>>>(a, r);
+      cudaMemsetAsync(ctx.counter, 0, 4 * sizeof(int), sm);
+      k_sweep_end<<<sgrid(), 128, 0, sm>>>(a);
+    };
+    // The sweep's NBp + 1 launches replayed as one graph: the host's launch cost, not the GPU, set
+    // the pace once few problems are active (one 200x200 problem: 1.48 ms per LADMAP iteration of
+    // which 0.64 ms on the GPU). Keyed by the argument bytes (the V buffer offset
+    // changes with every Newton-Schulz step: two cached executables). Captured on a private
+    // stream (capture is not allowed on the legacy default stream), launched on ctx.stream.
+    cudaGraphExec_t exec = nullptr;
+    if (!ctx.cap_stream &&
+        fail_cuda(cudaStreamCreateWithFlags(&ctx.cap_stream, cudaStreamNonBlocking), "cudaStreamCreate(capture)"))
+      return true;
+    {
+      std::string key(reinterpret_cast<const char*>(&a), sizeof(Args));
+      key.append(reinterpret_cast<const char*>(&RPL_TAG<RPL>), sizeof(int));
+      for (int c = 0; c < 2; ++c)
+        if (ctx.sweep_exec[c] && ctx.sweep_key[c] == key) exec = ctx.sweep_exec[c];
+      if (!exec) {
+        cudaGraph_t g = nullptr;
+        if (fail_cuda(cudaStreamBeginCapture(ctx.cap_stream, cudaStreamCaptureModeThreadLocal), "capture(sweep)"))
+          return true;
+        enqueue(ctx.cap_stream);
+        const cudaError_t e1 = cudaStreamEndCapture(ctx.cap_stream, &g);
+        if (fail_cuda(e1, "capture(sweep) end")) return true;
+        const int c = ctx.sweep_next;
+        ctx.sweep_next ^= 1;
+        if (ctx.sweep_exec[c]) cudaGraphExecDestroy(ctx.sweep_exec[c]);
+        ctx.sweep_exec[c] = nullptr;
+        const cudaError_t e2 = cudaGraphInstantiate(&ctx.sweep_exec[c], g, 0);
+        cudaGraphDestroy(g);
+        if (fail_cuda(e2, "cudaGraphInstantiate(sweep)")) return true;
+        ctx.sweep_key[c] = key;
+        exec = ctx.sweep_exec[c];
       }
-      if (zero_counter()) return true;
-      k_sweep_end<<<sgrid(), 128, 0, ctx.stream>>>(a);
-      launched();
+    }
+    for (int sw = 0; sw < a.max_sweeps; ++sw) {
+      if (exec) {
+        if (fail_cuda(cudaGraphLaunch(exec, ctx.stream), "cudaGraphLaunch(sweep)")) return true;
+      } else {
+        enqueue(ctx.stream);
+      }
+      launched(a.NBp + 1);
       if (check("jacobi sweep")) return true;
       const int act = read_counter();
       if (act < 0) return true;
@@ -1904,6 +1943,9 @@ tilt_status ensure(Ctx& ctx, size_t floats, int B) {
 }
 
 void release(Ctx& ctx) {
+  for (auto& g : ctx.sweep_exec)
+    if (g) cudaGraphExecDestroy(g);
+  if (ctx.cap_stream) cudaStreamDestroy(ctx.cap_stream);
   if (ctx.ws) cudaFree(ctx.ws);
   if (ctx.widx) cudaFree(ctx.widx);
   if (ctx.counter) cudaFree(ctx.counter);

@@ -28,6 +28,12 @@ struct Ctx {
   int* h_counter = nullptr;  // pinned host mirror
   int64_t* launches = nullptr;
   std::string* err = nullptr;
+  // one Jacobi sweep (the intra-block and cross rounds, the counter reset, k_sweep_end) captured as a
+  // CUDA graph: two cached executables keyed by the kernels' argument bytes and the row class
+  cudaGraphExec_t sweep_exec[2] = {nullptr, nullptr};
+  std::string sweep_key[2];
+  int sweep_next = 0;
+  cudaStream_t cap_stream = nullptr;  // private stream the sweep is captured on (the user's may be legacy)
 };
 
 // workspace floats of B problems of size m x n with p Jacobian planes
