@@ -100,8 +100,9 @@ typedef struct {
    * TILT_PATCH_BAD_BOX and not solved). 0: read back from boxes[0] with a stream sync;
    * > 0: taken as given. Host syncs: none on the CTA-per-patch kernels when win_h, win_w > 0 (the
    * call is then graph-capturable); the multi-CTA path (kernel_path 3, windows above 128 x 128 on
-   * auto, svd_mode 1) drives its loops from the host and synchronises the stream to read its
-   * active-problem counter (once per Jacobi sweep and per LADMAP / outer iteration), so it returns
+   * auto, svd_mode 1) drives its LADMAP / outer loops from the host and synchronises the stream to
+   * read its active-problem counter once per LADMAP / outer iteration (an SVT's Jacobi sweeps run
+   * as a device-side CUDA-graph loop), so it returns
    * TILT_E_UNSUPPORTED on a capturing stream; the same holds for win_h/win_w = 0. */
   int32_t win_h, win_w;
   /* kernel family: 0 = auto (the CTA-per-patch kernels up to 128 x 128, the multi-CTA path above:
@@ -250,8 +251,8 @@ tilt_status tilt_project_batch(tilt_handle* h, const float* J, const float* Q, i
  * rho_replay [B][max_inner], trace [B][max_inner][4], Jacobi controls). Outputs A, E, Y [B][m][n]
  * (Y may be NULL) and rep [B] (inner_iters, jacobi_sweeps, objective, crit1, crit2, rank...).
  * m, n <= 1024: windows above 128 (or prm->kernel_path = 3) run on the multi-CTA path, which
- * synchronises the handle's stream once per Jacobi sweep and per LADMAP iteration (it reads an
- * active-problem counter). Its workspace (B x ~(10 + p) m n floats, more with svd_mode 1) is made
+ * synchronises the handle's stream once per LADMAP iteration (it reads an active-problem counter;
+ * the Jacobi sweeps of an SVT loop on the device in a CUDA graph). Its workspace (B x ~(10 + p) m n floats, more with svd_mode 1) is made
  * by tilt_create when max_m or max_n exceeds 128, else on first use. */
 tilt_status tilt_inner_batch(tilt_handle* h, const float* D, const float* J, const float* Q,
                              int32_t l, int32_t B, int32_t m, int32_t n, int32_t p,

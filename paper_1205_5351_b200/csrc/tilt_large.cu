@@ -646,6 +646,13 @@ __global__ void k_svt_begin(Args a, const float* __restrict__ eps, int eps_mode)
   if (!st->svt_done) atomicAdd(a.counter, 1);
 }
 
+// Loop condition of the device-side sweep loop (a WHILE node of the sweep graph): another sweep
+// while any problem's SVT is still running; counter[8] tallies the sweeps run (launch accounting)
+__global__ void k_sweep_cond(const int* counter, int* tally, cudaGraphConditionalHandle h) {
+  *tally += 1;
+  cudaGraphSetConditional(h, counter[0] > 0 ? 1u : 0u);
+}
+
 __global__ void k_sweep_end(Args a) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= a.B) return;
@@ -1627,20 +1634,28 @@ struct Run {
   }
   dim3 sgrid() const { return dim3((unsigned)((a.B + 127) / 128)); }
   void launched(int k = 1) { *ctx.launches += k; }
+  // the device tally of graph-run sweeps (counter[8]) since the last read, counted as launches
+  void tally_sweeps() {
+    const int t = ctx.h_counter[8];
+    launched((t - ctx.sweep_tally_seen) * (a.NBp + 2));
+    ctx.sweep_tally_seen = t;
+  }
   int read_counter() {
-    if (fail_cuda(cudaMemcpyAsync(ctx.h_counter, ctx.counter, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream),
+    if (fail_cuda(cudaMemcpyAsync(ctx.h_counter, ctx.counter, 9 * sizeof(int), cudaMemcpyDeviceToHost, ctx.stream),
                   "cudaMemcpyAsync(counter)"))
       return -1;
     if (fail_cuda(cudaStreamSynchronize(ctx.stream), "cudaStreamSynchronize")) return -1;
+    tally_sweeps();
     return *ctx.h_counter;
   }
   bool zero_counter() { return fail_cuda(cudaMemsetAsync(ctx.counter, 0, 4 * sizeof(int), ctx.stream), "memset"); }
   // counters [0..3) after a stream sync (false on error)
   bool read_counters(int* out) {
-    if (fail_cuda(cudaMemcpyAsync(ctx.h_counter, ctx.counter, 3 * sizeof(int), cudaMemcpyDeviceToHost, ctx.stream),
+    if (fail_cuda(cudaMemcpyAsync(ctx.h_counter, ctx.counter, 9 * sizeof(int), cudaMemcpyDeviceToHost, ctx.stream),
                   "cudaMemcpyAsync(counters)"))
       return false;
     if (fail_cuda(cudaStreamSynchronize(ctx.stream), "cudaStreamSynchronize")) return false;
+    tally_sweeps();
     for (int i = 0; i < 3; ++i) out[i] = ctx.h_counter[i];
     return true;
   }
@@ -1726,51 +1741,61 @@ struct Run {
       cudaMemsetAsync(ctx.counter, 0, 4 * sizeof(int), sm);
       k_sweep_end<<<sgrid(), 128, 0, sm>>>(a);
     };
-    // The sweep's NBp + 1 launches replayed as one graph: the host's launch cost, not the GPU, set
-    // the pace once few problems are active (one 200x200 problem: 1.48 ms per LADMAP iteration of
-    // which 0.64 ms on the GPU). Keyed by the argument bytes (the V buffer offset
-    // changes with every Newton-Schulz step: two cached executables). Captured on a private
-    // stream (capture is not allowed on the legacy default stream), launched on ctx.stream.
-    cudaGraphExec_t exec = nullptr;
+    // All sweeps of an SVT as one graph: a WHILE node whose body is one sweep (NBp + 1 launches, the
+    // counter reset) followed by k_sweep_cond, which ends the loop once no problem's SVT runs (each
+    // problem also stops itself at max_sweeps in k_sweep_end). No host round trip per sweep and one
+    // launch call per SVT: with few active problems the host's launches and the per-sweep counter
+    // read, not the GPU, set the pace (one 200x200 problem: 1.48 ms per LADMAP iteration of which
+    // 0.64 ms on the GPU). Cached by the kernels' argument bytes (the V buffer offset
+    // alternates with the Newton-Schulz step: two executables); captured on a private stream
+    // (capture is not allowed on the legacy default stream), launched on ctx.stream.
     if (!ctx.cap_stream &&
         fail_cuda(cudaStreamCreateWithFlags(&ctx.cap_stream, cudaStreamNonBlocking), "cudaStreamCreate(capture)"))
       return true;
-    {
-      std::string key(reinterpret_cast<const char*>(&a), sizeof(Args));
-      key.append(reinterpret_cast<const char*>(&RPL_TAG<RPL>), sizeof(int));
-      for (int c = 0; c < 2; ++c)
-        if (ctx.sweep_exec[c] && ctx.sweep_key[c] == key) exec = ctx.sweep_exec[c];
-      if (!exec) {
-        cudaGraph_t g = nullptr;
-        if (fail_cuda(cudaStreamBeginCapture(ctx.cap_stream, cudaStreamCaptureModeThreadLocal), "capture(sweep)"))
-          return true;
-        enqueue(ctx.cap_stream);
-        const cudaError_t e1 = cudaStreamEndCapture(ctx.cap_stream, &g);
-        if (fail_cuda(e1, "capture(sweep) end")) return true;
-        const int c = ctx.sweep_next;
+    std::string key(reinterpret_cast<const char*>(&a), sizeof(Args));
+    key.append(reinterpret_cast<const char*>(&RPL_TAG<RPL>), sizeof(int));
+    cudaGraphExec_t exec = nullptr;
+    for (int c = 0; c < 2; ++c)
+      if (ctx.sweep_exec[c] && ctx.sweep_key[c] == key) exec = ctx.sweep_exec[c];
+    if (!exec) {
+      cudaGraph_t g = nullptr;
+      if (fail_cuda(cudaGraphCreate(&g, 0), "cudaGraphCreate(sweeps)")) return true;
+      cudaGraphConditionalHandle h;
+      cudaGraphNodeParams cp = {};
+      cp.type = cudaGraphNodeTypeConditional;
+      cudaGraphNode_t node;
+      bool bad = fail_cuda(cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault), "conditional handle");
+      if (!bad) {
+        cp.conditional.handle = h;
+        cp.conditional.type = cudaGraphCondTypeWhile;
+        cp.conditional.size = 1;
+        bad = fail_cuda(cudaGraphAddNode(&node, g, nullptr, 0, &cp), "cudaGraphAddNode(while)");
+      }
+      if (!bad) {
+        cudaGraph_t body = cp.conditional.phGraph_out[0];
+        bad = fail_cuda(cudaStreamBeginCaptureToGraph(ctx.cap_stream, body, nullptr, nullptr, 0,
+                                                      cudaStreamCaptureModeThreadLocal),
+                        "capture(sweep)");
+        if (!bad) {
+          enqueue(ctx.cap_stream);
+          k_sweep_cond<<<1, 1, 0, ctx.cap_stream>>>(ctx.counter, ctx.counter + 8, h);
+          bad = fail_cuda(cudaStreamEndCapture(ctx.cap_stream, &body), "capture(sweep) end");
+        }
+      }
+      const int c = ctx.sweep_next;
+      if (!bad) {
         ctx.sweep_next ^= 1;
         if (ctx.sweep_exec[c]) cudaGraphExecDestroy(ctx.sweep_exec[c]);
         ctx.sweep_exec[c] = nullptr;
-        const cudaError_t e2 = cudaGraphInstantiate(&ctx.sweep_exec[c], g, 0);
-        cudaGraphDestroy(g);
-        if (fail_cuda(e2, "cudaGraphInstantiate(sweep)")) return true;
-        ctx.sweep_key[c] = key;
-        exec = ctx.sweep_exec[c];
+        bad = fail_cuda(cudaGraphInstantiate(&ctx.sweep_exec[c], g, 0), "cudaGraphInstantiate(sweeps)");
       }
+      cudaGraphDestroy(g);
+      if (bad) return true;
+      ctx.sweep_key[c] = key;
+      exec = ctx.sweep_exec[c];
     }
-    for (int sw = 0; sw < a.max_sweeps; ++sw) {
-      if (exec) {
-        if (fail_cuda(cudaGraphLaunch(exec, ctx.stream), "cudaGraphLaunch(sweep)")) return true;
-      } else {
-        enqueue(ctx.stream);
-      }
-      launched(a.NBp + 1);
-      if (check("jacobi sweep")) return true;
-      const int act = read_counter();
-      if (act < 0) return true;
-      if (act == 0) break;
-    }
-    return false;
+    if (fail_cuda(cudaGraphLaunch(exec, ctx.stream), "cudaGraphLaunch(sweeps)")) return true;
+    return check("jacobi sweeps");
   }
 
   // Jacobi sweeps on (B, V) until every problem's SVT stopped (k_svt_begin ran before)
@@ -1921,6 +1946,8 @@ tilt_status ensure(Ctx& ctx, size_t floats, int B) {
   if (!ctx.counter) {
     if (cudaMalloc(&ctx.counter, 64 * sizeof(int)) != cudaSuccess) return TILT_E_OOM;
     if (cudaMallocHost(&ctx.h_counter, 64 * sizeof(int)) != cudaSuccess) return TILT_E_OOM;
+    if (cudaMemset(ctx.counter, 0, 64 * sizeof(int)) != cudaSuccess) return TILT_E_CUDA;
+    ctx.sweep_tally_seen = 0;
   }
   if (ctx.cap_b < B) {
     if (ctx.widx) cudaFree(ctx.widx);

@@ -34,6 +34,7 @@ struct Ctx {
   std::string sweep_key[2];
   int sweep_next = 0;
   cudaStream_t cap_stream = nullptr;  // private stream the sweep is captured on (the user's may be legacy)
+  int sweep_tally_seen = 0;           // counter[8] (sweeps run by the graphs) at the last host read
 };
 
 // workspace floats of B problems of size m x n with p Jacobian planes
