@@ -30,7 +30,7 @@
  * the handle's stream (tilt_set_stream); the caller synchronises. A handle is not thread-safe.
  * Exception: the multi-CTA path (windows above 128 x 128) creates, on its first call, a private
  * capture stream and up to two CUDA-graph executables of an SVT's device-side Jacobi sweep loop
- * (rebuilt when the call's arguments change); they are released by tilt_destroy. */
+ * (rebuilt when the call's arguments change); they are released by tilt_destroy.
  *
  * Errors: every entry point returns a tilt_status; no exception crosses the ABI. Per-patch
  * failures never abort a batch: they are reported in tilt_report.status and the patch keeps its
