@@ -23,6 +23,7 @@ ap.add_argument("--cfg", type=int, default=2)
 ap.add_argument("--reps", type=int, default=2)
 ap.add_argument("--path", type=int, default=0, help="tilt_params.kernel_path (0 auto, 1 CTA, 2 warp)")
 ap.add_argument("--ns", type=int, default=1, help="tilt_params.ns_period")
+ap.add_argument("--max-sweeps", type=int, default=0, help="tilt_params.jacobi_max_sweeps (0: default)")
 ap.add_argument("--jtol", type=float, default=0.0, help="tilt_params.jacobi_tol (0: 8 sqrt(m) 2^-24, reading Z14)")
 a = ap.parse_args()
 cfg = ts.CONFIGS[a.cfg]
@@ -30,7 +31,7 @@ b = ts.gen_batch(cfg, 0, a.batch)
 s = T.TiltSolver(0, max_batch=a.batch, max_m=cfg.m, max_n=cfg.n, max_p=cfg.p, max_image_elems=b["images"].size)
 prm = T.default_params(fixed_inner_iters=a.inner, fixed_outer_iters=a.outer, max_inner=max(a.inner, 1),
                        max_outer=max(a.outer, 1), win_h=cfg.m, win_w=cfg.n, kernel_path=a.path, ns_period=a.ns,
-                       jacobi_tol=a.jtol)
+                       jacobi_tol=a.jtol, **({"jacobi_max_sweeps": a.max_sweeps} if a.max_sweeps else {}))
 ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 for r in range(a.reps):
     ev0.record()
