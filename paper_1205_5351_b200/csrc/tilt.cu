@@ -88,6 +88,16 @@ tilt::lp::Ctx& lp_ctx(tilt_handle* h) {
   return h->lp;
 }
 
+// Opt in to `sm` bytes of dynamic shared memory when static + dynamic exceeds the 48 KB default (the
+// static part counts: a 32 x 32 homography solve has 45.7 KB dynamic plus its static block).
+inline tilt_status allow_dynamic_smem(const void* fn, size_t sm) {
+  cudaFuncAttributes fa;
+  TILT_CUDA(cudaFuncGetAttributes(&fa, fn));
+  if (sm + fa.sharedSizeBytes > 48 * 1024)
+    TILT_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  return TILT_OK;
+}
+
 template <class C>
 int occupancy_for(const void* fn, size_t smem) {
   int nb = 0;
@@ -161,10 +171,7 @@ struct Launch {
   static size_t smem(Geo g) { return Layout<C>::smem_bytes(g.ld, g.n, g.gplanes); }
   static size_t wsf(Geo g) { return Layout<C>::ws_floats(g.ld, g.n, g.gplanes); }
 
-  static tilt_status prep(const void* fn, size_t sm) {
-    if (sm > 48 * 1024) TILT_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    return TILT_OK;
-  }
+  static tilt_status prep(const void* fn, size_t sm) { return allow_dynamic_smem(fn, sm); }
 
   // grid size (persistent): num_sms * occupancy, capped by B and by the workspace slots
   static tilt_status grid(tilt_handle* h, const void* fn, Geo geo, int B, int* g, int cap_per_sm = 0) {
@@ -719,7 +726,10 @@ tilt_status tilt_warp_batch(tilt_handle* h, const float* images, int32_t n_image
   a.status = status;
   const size_t k1_smem = (size_t)m * n * sizeof(float4);  // (d, gx, gy, gz) per window pixel
   if (k1_smem > 227 * 1024) return TILT_E_ARG;
-  if (k1_smem > 48 * 1024) TILT_CUDA(cudaFuncSetAttribute((const void*)k_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k1_smem));
+  {
+    const tilt_status s1 = allow_dynamic_smem((const void*)k_warp, k1_smem);
+    if (s1 != TILT_OK) return s1;
+  }
   k_warp<<<B, K1_NT, k1_smem, h->stream>>>(a);
   h->launches++;
   TILT_CUDA(cudaGetLastError());
