@@ -449,6 +449,8 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
             "fraction_of_converged": float(np.mean(np.asarray(rec)[convm])) if convm.any() else None,
             "table2_error_median": float(np.median(err)), "table2_error_mean": float(np.mean(err)),
             "table2_note": "||tau* - tau_G|| / ||tau_G|| (P:1380-1381), normalised coordinates"}
+    if world == 1 and not args.no_k1:
+        line["recovery_in_basin"] = recovery_in_basin(T, dev)
     if world > 1:
         line["gather"] = {"bytes_to_rank0": gather_bytes, "backend": dist.get_backend(),
                           "note": "tau, reports, A, E of every patch to rank 0, inside the timed region"}
@@ -463,6 +465,31 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     print(json.dumps(line), flush=True)
     for s in solvers:
         s.close()
+
+
+def recovery_in_basin(T, dev, count: int = 256) -> dict:
+    """Untimed: free-running solves of SURVEY P9(ii)'s planted-recovery recipe (clean smooth rank-2/3
+    textures, 32x32 homography, rotation <= 15 deg, skew <= 0.2, perspective +-1e-3 px; the generator
+    of tests/test_gpu_recovery.py, seeds [905, idx]) -- the rectification rate inside TILT's basin,
+    beside the config-5 recovery (mostly outside it)."""
+    import dataclasses
+
+    import torch
+    cfg = dataclasses.replace(ts.CONFIGS[1], corrupt=0.0, config_id=905, rank_lo=2, rank_hi=3,
+                              kind=ts.HOMOGRAPHY, persp_px=1e-3)
+    pats = [ts.gen_patch(cfg, k, blur_px=1.0) for k in range(count)]
+    s = T.TiltSolver(dev.index or 0, max_batch=count, max_m=cfg.m, max_n=cfg.n, max_p=8,
+                     max_image_elems=count * 4 * cfg.m * cfg.n)
+    out = s.solve(np.stack([q["canvas"] for q in pats]), np.arange(count, dtype=np.int32),
+                  np.stack([q["box"] for q in pats]), np.stack([q["tau0"] for q in pats]), cfg.kind,
+                  T.default_params(win_h=cfg.m, win_w=cfg.n))
+    tau = out["tau"].double().cpu().numpy()
+    rep = T.reports_to_numpy(out["rep"])
+    s.close()
+    ok = [TM.recovered_p9(tau[k], pats[k]["tau_g"]) for k in range(count)]
+    return {"recipe": "SURVEY P9(ii): 32x32 homography, clean smooth rank 2-3, theta <= 15 deg, skew <= 0.2",
+            "patches": count, "fraction": float(np.mean(ok)),
+            "converged_fraction": float(np.mean(rep["status"] == T.CONVERGED)), "timed": False}
 
 
 def k1_roofline(solver, images, patch_image, boxes, tau0, kind, m, n, p, peaks) -> dict:
