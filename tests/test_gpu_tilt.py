@@ -235,7 +235,11 @@ def test_edge_cases(solver, T):
     del torch
 
 
-@pytest.mark.parametrize("m,n,kind", [(33, 33, O.AFFINE), (40, 56, O.HOMOGRAPHY), (63, 45, O.AFFINE)])
+@pytest.mark.parametrize("m,n,kind", [(33, 33, O.AFFINE), (40, 56, O.HOMOGRAPHY), (63, 45, O.AFFINE),
+                                      # size-class edges, where dynamic + static shared memory crosses
+                                      # the 48 KB default (the 32 x 32 homography once failed there)
+                                      (32, 32, O.HOMOGRAPHY), (61, 61, O.HOMOGRAPHY), (62, 60, O.AFFINE),
+                                      (64, 64, O.HOMOGRAPHY), (128, 128, O.HOMOGRAPHY)])
 def test_ragged_sizes_fixed_count(solver, T, m, n, kind):
     cfg = dataclasses.replace(ts.CONFIGS[1], m=m, n=n, kind=kind, config_id=950 + m)
     B, K = 2, 20
