@@ -59,10 +59,11 @@ def test_warp_jacobian_parity(solver, kind):
             assert err < 1e-5, (k, q, err)
 
 
-@pytest.mark.parametrize("hw", [(45, 47), (50, 51)])
+@pytest.mark.parametrize("hw", [(45, 47), (50, 51), (51, 60), (56, 56)])  # 51x60: 48.96 KB of dynamic shared memory, static on top crosses 48 KB
 def test_warp_jacobian_parity_ragged_window(solver, hw):
     """K1's scalar store path (m n not a multiple of 4: the 16-byte plane stores need m n % 4 == 0)
-    and odd window sizes, homography with perspective terms (the fp32-reciprocal + Newton 1/w)."""
+    and odd window sizes, homography with perspective terms (the fp32-reciprocal + Newton 1/w), and
+    windows whose (d, gx, gy, gz) staging sits at the 48 KB dynamic shared-memory default."""
     cfg = ts.CONFIGS[2]
     kind, p = O.HOMOGRAPHY, 8
     b = ts.gen_batch(cfg, 0, 4)
