@@ -33,11 +33,12 @@ tilt_status cuda_fail(cudaError_t e, const char* what) {
     if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
   } while (0)
 
-enum SizeClass { SC32 = 0, SC64 = 1, SC128 = 2, SC256 = 3, SC_NONE = 4, SC256G = 5 };
+enum SizeClass { SC32 = 0, SC64 = 1, SC128 = 2, SC256 = 3, SC_NONE = 4, SC256G = 5, SC56 = 6 };
 
 SizeClass size_class(int m, int n) {
   const int d = m > n ? m : n;
   if (d <= 32) return SC32;
+  if (d <= 56) return SC56;
   if (d <= 64) return SC64;
   if (d <= 128) return SC128;
   if (d <= 256) return n <= 216 ? SC256 : SC256G;  // B in shared memory while MAXD x n floats fit
@@ -262,6 +263,7 @@ template <template <class> class F, class... Args>
 tilt_status dispatch(SizeClass c, Args... args) {
   switch (c) {
     case SC32: return F<CfgS32>::run(args...);
+    case SC56: return F<CfgS56>::run(args...);
     case SC64: return F<CfgS64>::run(args...);
     case SC128: return F<CfgS128>::run(args...);
     case SC256: return F<CfgS256>::run(args...);
@@ -291,6 +293,7 @@ struct ProjF {
 size_t ws_need(SizeClass c, int m, int n, int gpl) {
   switch (c) {
     case SC32: return Launch<CfgS32>::wsf(geo_of<CfgS32>(m, n, gpl));
+    case SC56: return Launch<CfgS56>::wsf(geo_of<CfgS56>(m, n, gpl));
     case SC64: return Launch<CfgS64>::wsf(geo_of<CfgS64>(m, n, gpl));
     case SC128: return Launch<CfgS128>::wsf(geo_of<CfgS128>(m, n, gpl));
     case SC256: return Launch<CfgS256>::wsf(geo_of<CfgS256>(m, n, gpl));
@@ -316,6 +319,7 @@ int occ_of(Geo g) {
 int occ_need(SizeClass c, int m, int n, int gpl) {
   switch (c) {
     case SC32: return occ_of<CfgS32>(geo_of<CfgS32>(m, n, gpl));
+    case SC56: return occ_of<CfgS56>(geo_of<CfgS56>(m, n, gpl));
     case SC64: return occ_of<CfgS64>(geo_of<CfgS64>(m, n, gpl));
     case SC128: return occ_of<CfgS128>(geo_of<CfgS128>(m, n, gpl));
     case SC256: return occ_of<CfgS256>(geo_of<CfgS256>(m, n, gpl));

@@ -51,6 +51,11 @@ using CfgS32 = Cfg<8, 4, 8, true, true, 4>;
 #define TILT_S64_MINB 4
 #endif
 using CfgS64 = Cfg<TILT_S64_L, TILT_S64_RPL, TILT_S64_NW, false, true, TILT_S64_MINB>;
+// S56 (windows up to 56: the 50 x 50 of configs 2 and 5): S64's layout with 7 warps, 28 pair units
+// >= n/2. An eighth warp would own no Jacobi pair at n <= 56 yet run every round's loop and barrier;
+// without it a CTA issues fewer instructions per round and gets 72 registers at 4 CTAs/SM:
+// +5% LADMAP iterations/s (`profiles/r02/jacobi_layouts/r2s3_seven_warps.log`).
+using CfgS56 = Cfg<8, 8, 7, false, true, 4>;
 using CfgS128 = Cfg<16, 8, 32, false, true, 1>;
 // S256: B (256 x n floats, 205 KB at n = 200) in shared memory; V and S in the L2-resident slot
 using CfgS256 = Cfg<32, 8, 32, false, false, 1, true>;

@@ -1,7 +1,7 @@
 #!/bin/bash
 # Build a libtilt variant with overridden compile-time tunables (experiment helper, not product):
-#   tools/build_variant.sh NAME -DTILT_S64_L=4 -DTILT_S64_RPL=16 ...   (S64 layout, tilt_device.cuh)
-#   tools/build_variant.sh NAME -DTILT_K1_NT=256 -DTILT_K1_ILP=4 -DTILT_K1_MINB=2  (K1, tilt_kernels.cuh)
+#   tools/build_variant.sh NAME -DTILT_S64_L=8 -DTILT_S64_RPL=8 -DTILT_S64_NW=7 -DTILT_S64_MINB=4   (S64 layout)
+#   tools/build_variant.sh NAME -DTILT_K1_NT=128 -DTILT_K1_ILP=4 -DTILT_K1_MINB=4                    (K1 shape)
 # Output: build/var/libtilt_NAME.so (load with TILT_LIB=...), ptxas report build/var/ptxas_NAME.txt.
 set -e
 cd "$(dirname "$0")/.."
