@@ -33,13 +33,14 @@ tilt_status cuda_fail(cudaError_t e, const char* what) {
     if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
   } while (0)
 
-enum SizeClass { SC32 = 0, SC64 = 1, SC128 = 2, SC256 = 3, SC_NONE = 4, SC256G = 5, SC56 = 6 };
+enum SizeClass { SC32 = 0, SC64 = 1, SC128 = 2, SC256 = 3, SC_NONE = 4, SC256G = 5, SC56 = 6, SC100 = 7 };
 
 SizeClass size_class(int m, int n) {
   const int d = m > n ? m : n;
   if (d <= 32) return SC32;
   if (d <= 56) return SC56;
   if (d <= 64) return SC64;
+  if (d <= 100) return SC100;
   if (d <= 128) return SC128;
   if (d <= 256) return n <= 216 ? SC256 : SC256G;  // B in shared memory while MAXD x n floats fit
   return SC_NONE;
@@ -265,6 +266,7 @@ tilt_status dispatch(SizeClass c, Args... args) {
     case SC32: return F<CfgS32>::run(args...);
     case SC56: return F<CfgS56>::run(args...);
     case SC64: return F<CfgS64>::run(args...);
+    case SC100: return F<CfgS100>::run(args...);
     case SC128: return F<CfgS128>::run(args...);
     case SC256: return F<CfgS256>::run(args...);
     case SC256G: return F<CfgS256G>::run(args...);
@@ -295,6 +297,7 @@ size_t ws_need(SizeClass c, int m, int n, int gpl) {
     case SC32: return Launch<CfgS32>::wsf(geo_of<CfgS32>(m, n, gpl));
     case SC56: return Launch<CfgS56>::wsf(geo_of<CfgS56>(m, n, gpl));
     case SC64: return Launch<CfgS64>::wsf(geo_of<CfgS64>(m, n, gpl));
+    case SC100: return Launch<CfgS100>::wsf(geo_of<CfgS100>(m, n, gpl));
     case SC128: return Launch<CfgS128>::wsf(geo_of<CfgS128>(m, n, gpl));
     case SC256: return Launch<CfgS256>::wsf(geo_of<CfgS256>(m, n, gpl));
     case SC256G: return Launch<CfgS256G>::wsf(geo_of<CfgS256G>(m, n, gpl));
@@ -321,6 +324,7 @@ int occ_need(SizeClass c, int m, int n, int gpl) {
     case SC32: return occ_of<CfgS32>(geo_of<CfgS32>(m, n, gpl));
     case SC56: return occ_of<CfgS56>(geo_of<CfgS56>(m, n, gpl));
     case SC64: return occ_of<CfgS64>(geo_of<CfgS64>(m, n, gpl));
+    case SC100: return occ_of<CfgS100>(geo_of<CfgS100>(m, n, gpl));
     case SC128: return occ_of<CfgS128>(geo_of<CfgS128>(m, n, gpl));
     case SC256: return occ_of<CfgS256>(geo_of<CfgS256>(m, n, gpl));
     case SC256G: return occ_of<CfgS256G>(geo_of<CfgS256G>(m, n, gpl));

@@ -56,6 +56,9 @@ using CfgS64 = Cfg<TILT_S64_L, TILT_S64_RPL, TILT_S64_NW, false, true, TILT_S64_
 // without it a CTA issues fewer instructions per round and gets 72 registers at 4 CTAs/SM:
 // +5% LADMAP iterations/s (`profiles/r02/jacobi_layouts/r2s3_seven_warps.log`).
 using CfgS56 = Cfg<8, 8, 7, false, true, 4>;
+// S100 (windows 65..100: the 100 x 100 fine level of config 3): S128's layout with 25 warps, 50 pair
+// units of 16 lanes >= n/2 (S128's 32 warps leave 7 warps without a pair at n <= 100); 80 registers.
+using CfgS100 = Cfg<16, 8, 25, false, true, 1>;
 using CfgS128 = Cfg<16, 8, 32, false, true, 1>;
 // S256: B (256 x n floats, 205 KB at n = 200) in shared memory; V and S in the L2-resident slot
 using CfgS256 = Cfg<32, 8, 32, false, false, 1, true>;
