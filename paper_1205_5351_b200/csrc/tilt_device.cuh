@@ -56,10 +56,12 @@ using CfgS64 = Cfg<TILT_S64_L, TILT_S64_RPL, TILT_S64_NW, false, true, TILT_S64_
 // without it a CTA issues fewer instructions per round and gets 72 registers at 4 CTAs/SM:
 // +5% LADMAP iterations/s (`profiles/r02/jacobi_layouts/r2s3_seven_warps.log`).
 #ifndef TILT_S56_NW  // experiment hooks (tools/build_variant.sh); the defaults are the product
+#define TILT_S56_L 8
+#define TILT_S56_RPL 8
 #define TILT_S56_NW 7
 #define TILT_S56_MINB 4
 #endif
-using CfgS56 = Cfg<8, 8, TILT_S56_NW, false, true, TILT_S56_MINB>;
+using CfgS56 = Cfg<TILT_S56_L, TILT_S56_RPL, TILT_S56_NW, false, true, TILT_S56_MINB>;
 // S100 (windows 65..100: the 100 x 100 fine level of config 3): S128's layout with 25 warps, 50 pair
 // units of 16 lanes >= n/2 (S128's 32 warps leave 7 warps without a pair at n <= 100); 80 registers.
 using CfgS100 = Cfg<16, 8, 25, false, true, 1>;
